@@ -1,0 +1,396 @@
+"""bench.py -- exact squared-EDT throughput on B200 (BASELINE.json metric).
+
+Workload (config.workload): BASELINE.json configs[1] ("c2"): one 4096x4096
+uint8 image of 200 seeded discs (radii 8..64), exact squared EDT in BOTH
+directions (background->object = edt(img), object->background =
+edt(img.inverted())) as int32 plus float32 distances.  A step = one pass of
+the hot path over that image.  Under torchrun (N>1) every rank transforms its
+own replica (seed + rank): C2 is a single image the spec does not shard, so
+N>1 is replicas only ("scaling": "weak"), and the value is the whole-job
+pixel rate (N * pixels / max-over-ranks time).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c1|c2|c3|c4|c5]   (default c2; others for study)
+
+Timing: W >= 3 untimed warm-ups; every timed step is bracketed by CUDA events
+on the launching stream, with a 256 MiB L2 flush (> 126 MB L2) BETWEEN steps
+outside the events; barrier + synchronize on both sides of the timed region;
+max over ranks.  The dominant kernel (the row pass) is timed by events the C
+ABI records on the same stream (dfc_set_profile_events).  Clocks and
+throttle reasons are sampled with NVML during the timed region.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified proj/core sources compiled in this repo) on the host cores, same
+config/metric; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+CONFIGS = {
+    "c1": dict(desc="c1: 600x500 uint8 Bernoulli p=0.01 (reference generator), exact squared EDT "
+                    "int32 + float32 distances", bytes_alg=9, bytes_kernel=4 + 8),
+    "c2": dict(desc="c2: 4096x4096 uint8, 200 seeded discs (r 8..64), exact squared EDT both "
+                    "polarities int32 + float32 distances", bytes_alg=17, bytes_kernel=4 + 16),
+    "c3": dict(desc="c3: 1024 images 1024x1024 uint8, 30 seeded points each, exact squared EDT "
+                    "int32 + int32 Voronoi labels", bytes_alg=9, bytes_kernel=2 + 8),
+    "c4": dict(desc="c4: 8192x8192 uint8, 2000 seeded discs/rectangles, city-block + chessboard + "
+                    "chamfer-3-4 int32", bytes_alg=13, bytes_kernel=2 + 12),
+    "c5": dict(desc="c5: 32768x32768 uint8, Bernoulli 1e-4 in 256 of 1024 tiles, exact squared "
+                    "EDT int32", bytes_alg=5, bytes_kernel=2 + 4),
+}
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index):
+        self.ok = False
+        self.samples, self.reasons = [], set()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for bit, name in self.REASONS.items():
+            if r & bit and bit != 0x1:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self._sample()
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+            self._sample()
+            return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+
+
+def make_input(cfg, rank):
+    from paper_2106_03503_b200 import workloads
+    seed = workloads.SEEDS[cfg] + rank
+    return workloads.config(cfg, seed=seed), seed
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2106_03503_b200 as dfc
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg = args.config
+    img_np, seed = make_input(cfg, rank)
+    img = torch.from_numpy(img_np).to(dev)
+    npx = img_np.size
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    # preallocated outputs (a step writes them; no allocation in the timed region)
+    if cfg == "c2":
+        out = {k: torch.empty(img_np.shape, dtype=dt, device=dev)
+               for k, dt in (("sqdist_bg", torch.int32), ("dist_bg", torch.float32),
+                             ("sqdist_obj", torch.int32), ("dist_obj", torch.float32))}
+        step = lambda: dfc.edt_dual(img, out=out)
+    elif cfg == "c1" or cfg == "c5":
+        out = {"sqdist": torch.empty(img_np.shape, dtype=torch.int32, device=dev)}
+        if cfg == "c1":
+            out["dist"] = torch.empty(img_np.shape, dtype=torch.float32, device=dev)
+        step = lambda: dfc.edt(img, dist=cfg == "c1", out=out)
+    elif cfg == "c3":
+        out = {k: torch.empty(img_np.shape, dtype=torch.int32, device=dev) for k in ("sqdist", "label")}
+        step = lambda: dfc.edt_batched(img, dist=False, label=True, out=out)
+    else:  # c4
+        out = {k: torch.empty(img_np.shape, dtype=torch.int32, device=dev)
+               for k in ("cityblock", "chessboard", "chamfer34")}
+        step = lambda: dfc.raster(img, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = dfc.last_launch_count()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)  # evict L2 between timed steps (outside the events)
+        e0, e1, e2, e3 = ev[k]
+        if cfg != "c4":
+            dfc.set_profile_events(None, e1, e2)
+        e0.record(stream)
+        step()
+        e3.record(stream)
+    torch.cuda.synchronize()
+    dfc.set_profile_events(None, None, None)
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(d) for a, _, _, d in ev]
+    total_ms = float(sum(step_ms))
+    if cfg != "c4":
+        row_ms = float(np.mean([b.elapsed_time(c) for _, b, c, _ in ev]))
+    else:
+        row_ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([total_ms, row_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, row_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = world * npx * args.steps / (total_ms * 1e-3) / 1e6
+
+    # ---- e2e through the public API with HOST buffers (pinned), copies timed ----
+    host_in = torch.from_numpy(img_np).pin_memory()
+    host_out = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in out.items()}
+    dev_in = torch.empty_like(img)
+
+    def e2e_step():
+        dev_in.copy_(host_in, non_blocking=True)
+        nonlocal_img = dev_in
+        if cfg == "c2":
+            dfc.edt_dual(nonlocal_img, out=out)
+        elif cfg in ("c1", "c5"):
+            dfc.edt(nonlocal_img, dist=cfg == "c1", out=out)
+        elif cfg == "c3":
+            dfc.edt_batched(nonlocal_img, dist=False, label=True, out=out)
+        else:
+            dfc.raster(nonlocal_img, out=out)
+        for k2, v in out.items():
+            host_out[k2].copy_(v, non_blocking=True)
+
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    a.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    h2d = int(host_in.numel() * host_in.element_size())
+    d2h = int(sum(v.numel() * v.element_size() for v in host_out.values()))
+
+    if rank != 0:
+        return None
+    peak, peak_src = peaks()
+    c = CONFIGS[cfg]
+    kernel_bytes = c["bytes_kernel"] * npx
+    achieved = kernel_bytes / (row_ms * 1e-3) / 1e9
+    step_achieved = c["bytes_alg"] * npx / (ms_per_step * 1e-3) / 1e9
+    line = {
+        "metric": "exact squared-EDT Mpixel/s (bit-exact)" if cfg != "c4" else "raster DT Mpixel/s (bit-exact)",
+        "value": round(value, 1),
+        "unit": "Mpixel/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8->int32" + ("+f32" if cfg in ("c1", "c2") else ""),
+        "data": "synthetic (seeded stand-in, SURVEY.md 8(d))",
+        "config": {"workload": c["desc"], "seed": seed, "pixels_per_gpu_step": npx,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "256 MiB flush between timed steps (outside the events)"},
+        "roofline": {
+            "bound": "hbm", "kernel": "k_rows (row envelope)" if cfg != "c4" else "k_band_* + k_raster (whole step)",
+            "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "bytes_per_px": c["bytes_kernel"], "kernel_ms": round(row_ms, 5),
+            "step": {"bytes_alg_per_px": c["bytes_alg"], "achieved": round(step_achieved, 1),
+                     "frac": round(step_achieved / peak, 4)},
+        },
+        "e2e": {"value": round(world * npx / (e2e_ms * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "clocks": clk,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, img_np)
+    return line
+
+
+# ------------------------------------------------------------- CPU reference
+def _ref_step(cfg, img, threads):
+    """One bounded sample of the workload on the reference CPU path; returns
+    (pixels, seconds) measured by the reference shim's steady_clock."""
+    import oracle
+    if cfg in ("c1", "c2", "c5"):
+        _, ns = oracle.ref_edt(img, threads=threads, want_time=True)
+        t = ns
+        if cfg == "c2":
+            _, ns2 = oracle.ref_edt((img == 0).astype(np.uint8), threads=threads, want_time=True)
+            t += ns2
+        return img.size, t * 1e-9
+    if cfg == "c3":
+        sub = np.ascontiguousarray(img[:4])
+        import ctypes as C
+        ns = C.c_double(0)
+        oracle.ref.dfref_edt_labels_batch(sub, sub.shape[0], sub.shape[1], sub.shape[2], threads,
+                                          None, None, C.byref(ns))
+        return sub.size, ns.value * 1e-9
+    # c4: cityblock_sequential + chamfer34 (single-threaded by API) + chessboard restatement
+    _, t1 = oracle.ref_propagation(img, 0, want_time=True)
+    _, t2 = oracle.ref_propagation(img, 2, want_time=True)
+    t0 = time.perf_counter()
+    oracle.chessboard(img)
+    return img.size, (t1 + t2) * 1e-9 + (time.perf_counter() - t0)
+
+
+def cpu_baseline(cfg, img):
+    import oracle
+    threads = os.cpu_count() or 1
+    if not oracle.ref_available():
+        return {"value": None, "unit": "Mpixel/s", "cores": threads, "kind": "reference",
+                "sample": "oracle/_ref/libdfref.so missing"}
+    sample_img = img
+    note = "full image"
+    if cfg == "c5":  # 1 Gpixel is ~1 min: bound the sample to a 8192x8192 crop
+        sample_img = np.ascontiguousarray(img[:8192, :8192])
+        note = "top-left 8192x8192 crop of the c5 image"
+    if cfg == "c3":
+        note = "4 of the 1024 images (edt + voronoi_labels each)"
+    px, sec = _ref_step(cfg, sample_img, threads)
+    if cfg == "c2":
+        note = "full image, edt(img) + edt(img.inverted())"
+    return {"value": round(px / sec / 1e6, 3), "unit": "Mpixel/s", "cores": threads,
+            "kind": "reference", "sample": note + f", threads={threads}", "seconds": round(sec, 3)}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    import oracle
+    cfg = args.config
+    img, seed = make_input(cfg, 0)
+    threads = os.cpu_count() or 1
+    if not oracle.ref_available():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libdfref.so not built"}
+    if cfg == "c5":
+        img = np.ascontiguousarray(img[:8192, :8192])
+    for _ in range(min(args.warmup, 1)):
+        _ref_step(cfg, img, threads)
+    tot_px, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        px, s = _ref_step(cfg, img, threads)
+        tot_px += px
+        tot_s += s
+    value = tot_px / tot_s / 1e6
+    c = CONFIGS[cfg]
+    sample = {"c2": "full 4096x4096 image, edt(img) + edt(img.inverted())",
+              "c1": "full image", "c3": "4 of the 1024 images per step",
+              "c4": "full image: cityblock_sequential + chamfer34 + chessboard restatement",
+              "c5": "top-left 8192x8192 crop"}[cfg]
+    return {
+        "impl": "reference", "metric": "exact squared-EDT Mpixel/s (bit-exact)", "value": round(value, 3),
+        "unit": "Mpixel/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tot_s / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8->uint64", "data": "synthetic",
+        "config": {"workload": c["desc"], "seed": seed, "parallelism": f"std::jthread x{threads}"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpixel/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl")
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

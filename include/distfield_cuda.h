@@ -1,0 +1,140 @@
+/*
+ * distfield_cuda.h -- the C ABI of the B200-native distance-transform hot path.
+ *
+ * This is the thin, never-throwing boundary the C++ drop-in library
+ * (paper_2106_03503_b200/cpp, namespace distfield) and the Python host mirror
+ * (paper_2106_03503_b200/__init__.py, via ctypes) call.  Plain pointers and
+ * sizes only; all image/distance pointers are DEVICE pointers owned by the
+ * caller; every call is stream-ordered on `stream` (0 = legacy default) with
+ * no hidden host synchronisation.  Scratch comes from the device's default
+ * stream-ordered memory pool (cudaMallocAsync / cudaFreeAsync).
+ *
+ * Conventions (reference: /root/reference/proj/core):
+ *   - input: row-major uint8, object pixel = any nonzero byte (grid.hpp:82),
+ *     rows of `pitch_bytes` bytes (>= cols);
+ *   - outputs: dense row-major, row stride = cols elements;
+ *   - squared distances int32; the reference's uint64 infinity marker
+ *     (DistanceMap::kInfinity, grid.hpp:113) maps to DFC_INF_I32.  Infinity
+ *     only occurs for an image without any object pixel (grid.hpp:109-110);
+ *   - float distances: (float)sqrt((double)D) -- exactly the value the
+ *     reference prints via to_text_sqrt (grid.cpp:146) -- and +inf for
+ *     DFC_INF_I32;
+ *   - labels: int32 LINEAR index row*cols+col of the nearest object pixel,
+ *     ties broken exactly as voronoi_labels (exact_edt.cpp:319-371): the
+ *     smallest minimising column, then the upper feature in that column.
+ *     -1 for a featureless image (the reference throws std::domain_error,
+ *     exact_edt.cpp:321; the C++ adapter rethrows);
+ *   - nearest_col: meijster_scan().nearest_col (exact_edt.cpp:272-283): the
+ *     LARGEST minimising column (take_new), -1 for kNoColumn.
+ *   - supported shapes: 1 <= rows, cols <= 65535 and
+ *     (rows-1)^2 + (cols-1)^2 <= DFC_MAX_SQDIST (the int32 result range;
+ *     32768 x 32768 fits).  Larger shapes return DFC_ERR_SHAPE.
+ */
+#ifndef DISTFIELD_CUDA_H
+#define DISTFIELD_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dfc_stream_t; /* == cudaStream_t */
+
+#define DFC_INF_I32 0x7FFFFFFF
+#define DFC_MAX_SQDIST 0x7FFFFFFE
+
+enum dfc_status {
+    DFC_OK = 0,
+    DFC_ERR_SHAPE = 1,       /* rows/cols out of the supported range        */
+    DFC_ERR_ARG = 2,         /* null/misaligned pointer, bad pitch or flag  */
+    DFC_ERR_CUDA = 3,        /* a CUDA runtime error; see dfc_last_cuda_error */
+    DFC_ERR_NCCL = 4,        /* multi-GPU exchange failed                   */
+    DFC_ERR_NO_FEATURES = 5  /* label ordinals requested on a featureless image */
+};
+
+/* Polarity of the transform. BG_TO_OBJ is the reference `edt(img)`;
+ * OBJ_TO_BG is `edt(img.inverted())` (grid.cpp:38-44, CLI --polarity inside). */
+enum dfc_polarity { DFC_BG_TO_OBJ = 0, DFC_OBJ_TO_BG = 1 };
+
+/*
+ * Exact squared Euclidean distance transform of one image.
+ * Replaces distfield::edt(img, EdtAlgorithm::envelope, ...)
+ *   (exact_edt.hpp:100-102 / exact_edt.cpp:285-317) = vertical_pass
+ *   (exact_edt.cpp:112-117) + meijster_scan(...).map (exact_edt.cpp:272-283);
+ * with d_label != NULL also voronoi_labels (exact_edt.cpp:319-371), and with
+ * d_nearest_col != NULL also meijster_scan().nearest_col.
+ * d_sqdist is required; d_dist, d_label, d_nearest_col are optional (NULL).
+ */
+int dfc_edt_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+               int polarity, int32_t* d_sqdist, float* d_dist, int32_t* d_label,
+               int32_t* d_nearest_col, dfc_stream_t stream);
+
+/*
+ * Both polarities from ONE read of the input (config 2): background-to-object
+ * (= edt(img)) and object-to-background (= edt(img.inverted())).
+ * Any of the four outputs may be NULL except the two squared maps.
+ */
+int dfc_edt_u8_dual(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                    int32_t* d_sqdist_bg, float* d_dist_bg, int32_t* d_sqdist_obj,
+                    float* d_dist_obj, dfc_stream_t stream);
+
+/*
+ * A batch of n same-shape images (config 3), image b at
+ * d_imgs + b*image_stride_bytes; outputs dense [n][rows][cols].
+ * Labels are linear indices WITHIN each image (-1 for a featureless image).
+ */
+int dfc_edt_u8_batched(const uint8_t* d_imgs, int64_t n, int64_t rows, int64_t cols,
+                       int64_t pitch_bytes, int64_t image_stride_bytes, int32_t* d_sqdist,
+                       float* d_dist, int32_t* d_label, dfc_stream_t stream);
+
+/*
+ * The stage-one vertical pass alone (exact_edt.cpp:112-117): per column the
+ * squared vertical distance to the nearest object pixel in that column,
+ * DFC_INF_I32 for a featureless column.  Replaces distfield::vertical_pass.
+ */
+int dfc_vertical_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                    int32_t* d_vert, dfc_stream_t stream);
+
+/*
+ * The three approximate raster transforms of config 4, each bit-exact with
+ * the reference two-pass raster scans: city-block = cityblock_sequential
+ * (propagation.cpp:90-95), chamfer-3-4 = chamfer34 (propagation.cpp:104-109),
+ * chessboard = oracle::chessboard (proj/tests/oracles.hpp:52-55; the
+ * reference has no library transform for it).  Any output may be NULL.
+ */
+int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                  int32_t* d_cityblock, int32_t* d_chessboard, int32_t* d_chamfer34,
+                  dfc_stream_t stream);
+
+/*
+ * Converts linear-index labels to the reference's LabelMap ordinals (the
+ * row-major enumeration index among object pixels, grid.cpp:29-36) with an
+ * exclusive prefix count of object pixels.  d_ordinal may alias d_label.
+ */
+int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                       const int32_t* d_label, uint32_t* d_ordinal, dfc_stream_t stream);
+
+/*
+ * Measurement hook (bench.py): cudaEvent_t handles recorded on the call's
+ * stream by the next dfc_edt_u8* calls on this thread -- ev_col_begin before
+ * the column pass, ev_row_begin between column and row pass, ev_row_end
+ * after the row pass.  NULL disables a record.  Costs nothing when unset.
+ */
+int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_end);
+
+/* Number of kernels the last successful call on this thread enqueued. */
+int dfc_last_launch_count(void);
+/* Human-readable status; never NULL. */
+const char* dfc_status_string(int status);
+/* The cudaError_t behind the last DFC_ERR_CUDA on this thread (0 if none). */
+int dfc_last_cuda_error(void);
+/* Library version string, e.g. "distfield-b200 0.1 sm_100a". */
+const char* dfc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DISTFIELD_CUDA_H */

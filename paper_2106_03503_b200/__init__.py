@@ -1,0 +1,207 @@
+"""distfield-b200: B200-native exact distance transforms (Strutz, arXiv 2106.03503).
+
+Python host mirror of the reference ``distfield`` hot path
+(/root/reference/proj/core/include/distfield/{exact_edt,propagation}.hpp) over
+the C ABI in ``include/distfield_cuda.h`` (``lib/libdfc.so``, hand-written
+sm_100a CUDA).  Two layers:
+
+* device layer (``edt``, ``edt_dual``, ``edt_batched``, ``vertical``,
+  ``raster``, ``label_ordinals``): torch CUDA tensors in and out, int32 maps
+  with ``INF_I32`` as the infinity marker, stream-ordered, no host sync;
+* reference-shaped host layer in :mod:`paper_2106_03503_b200.distfield`
+  (``edt``, ``voronoi_labels``, ``meijster_scan``, ``vertical_pass``,
+  ``cityblock_sequential``, ``chamfer34``, ``chessboard``): numpy uint8 image
+  in, reference-typed numpy maps out (uint64 with ``2**64-1`` infinity,
+  uint32 ordinal labels), same exceptions as the reference.
+
+There is no CPU fallback: importing this package without the built CUDA
+library raises, and every call needs a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libdfc.so")
+INF_I32 = 0x7FFFFFFF
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the sm_100a library first "
+        "(python -c 'import __graft_entry__ as g; g.build()' or make -C paper_2106_03503_b200/csrc)")
+
+_lib = C.CDLL(LIB_PATH)
+_i64 = C.c_int64
+_vp = C.c_void_p
+_lib.dfc_edt_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp]
+_lib.dfc_edt_u8_dual.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]
+_lib.dfc_edt_u8_batched.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]
+_lib.dfc_vertical_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp]
+_lib.dfc_raster_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]
+_lib.dfc_label_ordinals.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp]
+_lib.dfc_status_string.restype = C.c_char_p
+_lib.dfc_status_string.argtypes = [C.c_int]
+_lib.dfc_version.restype = C.c_char_p
+_lib.dfc_last_launch_count.restype = C.c_int
+_lib.dfc_last_cuda_error.restype = C.c_int
+_lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
+
+EXPORTED_SYMBOLS = (
+    "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
+    "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
+    "dfc_version", "dfc_set_profile_events",
+)
+
+
+class DfcError(RuntimeError):
+    def __init__(self, status: int):
+        msg = _lib.dfc_status_string(status).decode()
+        if status == 3:
+            msg += f" (cudaError {_lib.dfc_last_cuda_error()})"
+        super().__init__(msg)
+        self.status = status
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise DfcError(status)
+
+
+def version() -> str:
+    return _lib.dfc_version().decode()
+
+
+def set_profile_events(col_begin=None, row_begin=None, row_end=None) -> None:
+    """Record torch.cuda.Event objects around the column / row pass of the next
+    edt* calls on this thread (measurement hook for bench.py); None disables."""
+    h = lambda e: None if e is None else C.c_void_p(e.cuda_event)
+    _check(_lib.dfc_set_profile_events(h(col_begin), h(row_begin), h(row_end)))
+
+
+def last_launch_count() -> int:
+    """Kernels enqueued by the last successful call on this thread."""
+    return _lib.dfc_last_launch_count()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _img2d(img: torch.Tensor):
+    if not img.is_cuda:
+        raise ValueError("device layer expects a CUDA tensor; use paper_2106_03503_b200.distfield for host arrays")
+    if img.dtype not in (torch.uint8, torch.bool) or img.dim() != 2:
+        raise ValueError("image must be a 2-D uint8 (or bool) CUDA tensor")
+    if img.dtype == torch.bool:
+        img = img.view(torch.uint8)
+    if img.stride(1) != 1:
+        img = img.contiguous()
+    return img, img.shape[0], img.shape[1], img.stride(0)
+
+
+def _empty(shape, dtype, like):
+    return torch.empty(shape, dtype=dtype, device=like.device)
+
+
+def edt(img: torch.Tensor, polarity: int = 0, dist: bool = True, label: bool = False,
+        nearest_col: bool = False, stream=None, out=None):
+    """Exact squared EDT of one image (``edt(img, envelope)``, exact_edt.cpp:285-317).
+
+    polarity 0: background -> nearest object (the reference ``edt(img)``);
+    polarity 1: object -> nearest background (``edt(img.inverted())``).
+    Returns a dict with int32 ``sqdist`` and optionally float32 ``dist``,
+    int32 ``label`` (linear index, voronoi_labels tie rule) and int32
+    ``nearest_col`` (meijster_scan's take_new rule)."""
+    img, h, w, pitch = _img2d(img)
+    o = dict(out or {})
+    o.setdefault("sqdist", _empty((h, w), torch.int32, img))
+    if dist:
+        o.setdefault("dist", _empty((h, w), torch.float32, img))
+    if label:
+        o.setdefault("label", _empty((h, w), torch.int32, img))
+    if nearest_col:
+        o.setdefault("nearest_col", _empty((h, w), torch.int32, img))
+    _check(_lib.dfc_edt_u8(_ptr(img), h, w, pitch, polarity, _ptr(o["sqdist"]), _ptr(o.get("dist")),
+                           _ptr(o.get("label")), _ptr(o.get("nearest_col")), _stream(stream)))
+    return o
+
+
+def edt_dual(img: torch.Tensor, dist: bool = True, stream=None, out=None):
+    """Both polarities from one input read (config 2): keys sqdist_bg, dist_bg,
+    sqdist_obj, dist_obj."""
+    img, h, w, pitch = _img2d(img)
+    o = dict(out or {})
+    for k in ("sqdist_bg", "sqdist_obj"):
+        o.setdefault(k, _empty((h, w), torch.int32, img))
+    if dist:
+        for k in ("dist_bg", "dist_obj"):
+            o.setdefault(k, _empty((h, w), torch.float32, img))
+    _check(_lib.dfc_edt_u8_dual(_ptr(img), h, w, pitch, _ptr(o["sqdist_bg"]), _ptr(o.get("dist_bg")),
+                                _ptr(o["sqdist_obj"]), _ptr(o.get("dist_obj")), _stream(stream)))
+    return o
+
+
+def edt_batched(imgs: torch.Tensor, dist: bool = False, label: bool = True, stream=None, out=None):
+    """A batch [n, rows, cols] of images (config 3): int32 sqdist and labels
+    (linear index within each image, -1 for a featureless image)."""
+    if not imgs.is_cuda or imgs.dim() != 3 or imgs.dtype not in (torch.uint8, torch.bool):
+        raise ValueError("batch must be a 3-D uint8 CUDA tensor [n, rows, cols]")
+    if imgs.dtype == torch.bool:
+        imgs = imgs.view(torch.uint8)
+    if imgs.stride(2) != 1:
+        imgs = imgs.contiguous()
+    n, h, w = imgs.shape
+    o = dict(out or {})
+    o.setdefault("sqdist", _empty((n, h, w), torch.int32, imgs))
+    if dist:
+        o.setdefault("dist", _empty((n, h, w), torch.float32, imgs))
+    if label:
+        o.setdefault("label", _empty((n, h, w), torch.int32, imgs))
+    _check(_lib.dfc_edt_u8_batched(_ptr(imgs), n, h, w, imgs.stride(1), imgs.stride(0),
+                                   _ptr(o["sqdist"]), _ptr(o.get("dist")), _ptr(o.get("label")),
+                                   _stream(stream)))
+    return o
+
+
+def vertical(img: torch.Tensor, stream=None) -> torch.Tensor:
+    """Stage one alone (vertical_pass, exact_edt.cpp:112-117): int32 squared
+    vertical distance, INF_I32 in featureless columns."""
+    img, h, w, pitch = _img2d(img)
+    out = _empty((h, w), torch.int32, img)
+    _check(_lib.dfc_vertical_u8(_ptr(img), h, w, pitch, _ptr(out), _stream(stream)))
+    return out
+
+
+def raster(img: torch.Tensor, cityblock: bool = True, chessboard: bool = True,
+           chamfer34: bool = True, stream=None, out=None):
+    """City-block / chessboard / chamfer-3-4 maps (config 4), int32, bit-exact
+    with the reference raster scans (propagation.cpp:90-109)."""
+    img, h, w, pitch = _img2d(img)
+    o = dict(out or {})
+    for key, want in (("cityblock", cityblock), ("chessboard", chessboard), ("chamfer34", chamfer34)):
+        if want:
+            o.setdefault(key, _empty((h, w), torch.int32, img))
+    _check(_lib.dfc_raster_u8(_ptr(img), h, w, pitch, _ptr(o.get("cityblock")),
+                              _ptr(o.get("chessboard")), _ptr(o.get("chamfer34")), _stream(stream)))
+    return o
+
+
+def label_ordinals(img: torch.Tensor, label: torch.Tensor, stream=None) -> torch.Tensor:
+    """Linear-index labels -> the reference LabelMap feature ordinals
+    (grid.cpp:29-36); int64 tensor holding uint32 values (2**32-1 = none)."""
+    img, h, w, pitch = _img2d(img)
+    out = _empty((h, w), torch.int32, img)
+    _check(_lib.dfc_label_ordinals(_ptr(img), h, w, pitch, _ptr(label.contiguous()), _ptr(out),
+                                   _stream(stream)))
+    return out.to(torch.int64) & 0xFFFFFFFF
+
+
+from . import distfield  # noqa: E402,F401  (reference-shaped host API)

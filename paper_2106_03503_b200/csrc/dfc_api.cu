@@ -1,0 +1,386 @@
+// dfc_api.cu -- the extern "C" entry points declared in include/distfield_cuda.h.
+//
+// Plumbing only: argument validation, scratch from the stream-ordered memory
+// pool, launch geometry, status codes.  Never throws, never synchronises.
+#include <cstdio>
+#include <cstring>
+
+#include "dfc_kernels.cuh"
+
+
+
+using namespace dfc;
+
+namespace {
+
+thread_local int g_last_cuda = 0;
+thread_local int g_launches = 0;
+thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+
+void prof(int k, cudaStream_t st) {
+    if (g_ev[k]) cudaEventRecord(g_ev[k], st);
+}
+
+constexpr int kMaxRowCols = 32768;  // widest row the shared-memory row pass holds
+
+int cuda_fail(cudaError_t e) {
+    g_last_cuda = (int)e;
+    return DFC_ERR_CUDA;
+}
+
+bool shape_ok(int64_t rows, int64_t cols) {
+    if (rows < 1 || cols < 1 || rows > 65535 || cols > kMaxRowCols) return false;
+    const int64_t b = (rows - 1) * (rows - 1) + (cols - 1) * (cols - 1);
+    return b <= DFC_MAX_SQDIST;
+}
+
+bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Keep freed scratch in the pool: after the first call no cudaMalloc happens.
+void init_pool_once() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+    done = true;
+}
+
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t st;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, st); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+struct RowGeom {
+    int T, L, R, row_words, smem_bytes;
+};
+
+RowGeom row_geom(int W) {
+    RowGeom g;
+    g.T = 32;
+    while (g.T < 1024 && (int64_t)g.T * 32 < W) g.T <<= 1;
+    g.L = (int)round_up((W + g.T - 1) / g.T, 4);
+    g.R = g.T >= 256 ? 1 : 256 / g.T;
+    g.row_words = (g.T * (g.L + 2)) / 2 + g.T * (g.L + 1) + 2 * g.T;
+    g.smem_bytes = (g.R * g.row_words + (g.R * g.T) / 32) * 4;
+    return g;
+}
+
+// Stage 1 into a uint16 nearest-row plane [npol][n][H][Wp].
+int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
+                int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
+                cudaStream_t st, int32_t* vsq = nullptr) {
+    ColArgs c;
+    c.img = img;
+    c.pitch = pitch;
+    c.img_stride = istride;
+    c.n_img = (int)n;
+    c.H = (int)H;
+    c.W = (int)W;
+    c.Wp = Wp;
+    c.nb = (int)((H + kBand - 1) / kBand);
+    c.pol0 = pol0;
+    c.npol = npol;
+    c.vec = aligned(img, 4) && pitch % 4 == 0 && istride % 4 == 0;
+    const int tpb = 128;
+    dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
+    k_band_summary<<<grid, tpb, 0, st>>>(c, first, last);
+    dim3 gs((unsigned)((W + 255) / 256), (unsigned)(npol * n));
+    k_band_scan<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
+    if (vsq)
+        k_band_fill<true><<<grid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
+    else
+        k_band_fill<false><<<grid, tpb, 0, st>>>(c, first, last, nr, nullptr);
+    g_launches += 3;
+    return DFC_OK;
+}
+
+struct OutSet {
+    int32_t* D[2] = {nullptr, nullptr};
+    float* S[2] = {nullptr, nullptr};
+    int32_t* LB[2] = {nullptr, nullptr};
+    int32_t* NC[2] = {nullptr, nullptr};
+};
+
+bool out_vec_ok(const void* p, int64_t stride) {
+    return p == nullptr || (aligned(p, 16) && stride % 16 == 0);
+}
+
+// Stage 2 over `nimg` planes of H rows.  Plane b writes its outputs at
+// base + b*stride.  take_new selects meijster_scan's tie rule.
+int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
+             int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
+             int64_t sN, cudaStream_t st) {
+    const RowGeom g = row_geom((int)W);
+    RowArgs a;
+    a.nr = nr;
+    a.nr_img_stride = H * Wp;
+    a.Wp = Wp;
+    a.H = (int)H;
+    a.W = (int)W;
+    a.total_rows = nimg * H;
+    a.T = g.T;
+    a.L = g.L;
+    a.R = g.R;
+    a.row_smem_words = g.row_words;
+    a.D = reinterpret_cast<char*>(D);
+    a.sD = sD;
+    a.S = reinterpret_cast<char*>(S);
+    a.sS = sS;
+    a.LB = reinterpret_cast<char*>(LB);
+    a.sL = sL;
+    a.NC = reinterpret_cast<char*>(NC);
+    a.sN = sN;
+    a.vec = W % 4 == 0 && out_vec_ok(D, sD) && out_vec_ok(S, sS) && out_vec_ok(LB, sL) &&
+            out_vec_ok(NC, sN);
+    const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
+    if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
+    cudaError_t e;
+    if (take_new) {
+        e = cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
+        if (e != cudaSuccess) return cuda_fail(e);
+        k_rows<true><<<(unsigned)blocks, g.R * g.T, g.smem_bytes, st>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
+        if (e != cudaSuccess) return cuda_fail(e);
+        k_rows<false><<<(unsigned)blocks, g.R * g.T, g.smem_bytes, st>>>(a);
+    }
+    ++g_launches;
+    return DFC_OK;
+}
+
+int64_t pstride(const void* a, const void* b) {
+    return reinterpret_cast<const char*>(b) - reinterpret_cast<const char*>(a);
+}
+
+// Shared driver for dfc_edt_u8 / _dual / _batched.
+int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
+             int pol0, int npol, const OutSet& o, cudaStream_t st) {
+    if (!img || !o.D[0] || (npol == 2 && !o.D[1])) return DFC_ERR_ARG;
+    if (!shape_ok(H, W)) return DFC_ERR_SHAPE;
+    if (pitch < W || n < 1 || n > 65535 || (n > 1 && istride < H * pitch)) return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    const int Wp = (int)round_up(W, 8);
+    const int64_t nb = (H + kBand - 1) / kBand;
+    const int64_t planes = (int64_t)npol * n;
+    const size_t carry_elems = (size_t)(planes * nb * Wp);
+    const size_t nr_elems = (size_t)(planes * H * Wp);
+    Scratch sc(st);
+    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 256);
+    if (e != cudaSuccess) return cuda_fail(e);
+    uint16_t* first = static_cast<uint16_t*>(sc.p);
+    uint16_t* last = first + carry_elems;
+    uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry_elems), 16));
+    prof(0, st);
+    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st);
+    if (rc != DFC_OK) return rc;
+    prof(1, st);
+
+    // one launch per tie policy when every output is present for all planes
+    // with a uniform stride; otherwise per plane
+    const int64_t plane_bytes = H * W * 4;
+    auto stride_of = [&](const void* p0, const void* p1) -> int64_t {
+        return npol == 2 ? pstride(p0, p1) : plane_bytes;
+    };
+    bool uniform = true;
+    if (npol == 2) {
+        uniform = ((o.S[0] == nullptr) == (o.S[1] == nullptr)) &&
+                  ((o.LB[0] == nullptr) == (o.LB[1] == nullptr)) &&
+                  ((o.NC[0] == nullptr) == (o.NC[1] == nullptr));
+    }
+    const bool want_keep = o.D[0] || o.S[0] || o.LB[0];
+    if (uniform) {
+        const int64_t nimg = planes;
+        if (want_keep) {
+            rc = row_pass(nr, nimg, H, W, Wp, false, o.D[0], stride_of(o.D[0], o.D[1]), o.S[0],
+                          o.S[0] ? stride_of(o.S[0], o.S[1]) : 0, o.LB[0],
+                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st);
+            if (rc != DFC_OK) return rc;
+        }
+        if (o.NC[0]) {
+            rc = row_pass(nr, nimg, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[0],
+                          stride_of(o.NC[0], o.NC[1]), st);
+            if (rc != DFC_OK) return rc;
+        }
+    } else {
+        for (int s = 0; s < npol; ++s) {
+            const uint16_t* pl = nr + (int64_t)s * H * Wp;
+            rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st);
+            if (rc != DFC_OK) return rc;
+            if (o.NC[s]) {
+                rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st);
+                if (rc != DFC_OK) return rc;
+            }
+        }
+    }
+    prof(2, st);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+    return DFC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfc_edt_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes, int polarity,
+               int32_t* d_sqdist, float* d_dist, int32_t* d_label, int32_t* d_nearest_col,
+               dfc_stream_t stream) {
+    if (polarity != DFC_BG_TO_OBJ && polarity != DFC_OBJ_TO_BG) return DFC_ERR_ARG;
+    OutSet o;
+    o.D[0] = d_sqdist;
+    o.S[0] = d_dist;
+    o.LB[0] = d_label;
+    o.NC[0] = d_nearest_col;
+    return edt_core(d_img, 1, rows, cols, pitch_bytes, 0, polarity, 1, o, (cudaStream_t)stream);
+}
+
+int dfc_edt_u8_dual(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                    int32_t* d_sqdist_bg, float* d_dist_bg, int32_t* d_sqdist_obj, float* d_dist_obj,
+                    dfc_stream_t stream) {
+    OutSet o;
+    o.D[0] = d_sqdist_bg;
+    o.D[1] = d_sqdist_obj;
+    o.S[0] = d_dist_bg;
+    o.S[1] = d_dist_obj;
+    return edt_core(d_img, 1, rows, cols, pitch_bytes, 0, 0, 2, o, (cudaStream_t)stream);
+}
+
+int dfc_edt_u8_batched(const uint8_t* d_imgs, int64_t n, int64_t rows, int64_t cols,
+                       int64_t pitch_bytes, int64_t image_stride_bytes, int32_t* d_sqdist,
+                       float* d_dist, int32_t* d_label, dfc_stream_t stream) {
+    OutSet o;
+    o.D[0] = d_sqdist;
+    o.S[0] = d_dist;
+    o.LB[0] = d_label;
+    return edt_core(d_imgs, n, rows, cols, pitch_bytes, image_stride_bytes, 0, 1, o,
+                    (cudaStream_t)stream);
+}
+
+int dfc_vertical_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                    int32_t* d_vert, dfc_stream_t stream) {
+    if (!d_img || !d_vert) return DFC_ERR_ARG;
+    if (!shape_ok(rows, cols)) return DFC_ERR_SHAPE;
+    if (pitch_bytes < cols) return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int Wp = (int)round_up(cols, 8);
+    const int64_t nb = (rows + kBand - 1) / kBand;
+    Scratch sc(st);
+    cudaError_t e = sc.alloc(2 * (size_t)nb * Wp * sizeof(uint16_t));
+    if (e != cudaSuccess) return cuda_fail(e);
+    uint16_t* first = static_cast<uint16_t*>(sc.p);
+    uint16_t* last = first + nb * Wp;
+    column_pass(d_img, 1, rows, cols, pitch_bytes, 0, 0, 1, nullptr, first, last, Wp, st, d_vert);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                  int32_t* d_cityblock, int32_t* d_chessboard, int32_t* d_chamfer34,
+                  dfc_stream_t stream) {
+    if (!d_img) return DFC_ERR_ARG;
+    if (!shape_ok(rows, cols)) return DFC_ERR_SHAPE;
+    if (pitch_bytes < cols) return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int Wp = (int)round_up(cols, 8);
+    const int64_t nb = (rows + kBand - 1) / kBand;
+    const size_t carry = (size_t)nb * Wp, nre = (size_t)rows * Wp;
+    Scratch sc(st);
+    cudaError_t e = sc.alloc((2 * carry + nre) * sizeof(uint16_t) + 256);
+    if (e != cudaSuccess) return cuda_fail(e);
+    uint16_t* first = static_cast<uint16_t*>(sc.p);
+    uint16_t* last = first + carry;
+    uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry), 16));
+    column_pass(d_img, 1, rows, cols, pitch_bytes, 0, 0, 1, nr, first, last, Wp, st);
+    RasterArgs r;
+    r.nr = nr;
+    r.Wp = Wp;
+    r.H = (int)rows;
+    r.W = (int)cols;
+    r.T = 32;
+    while (r.T < 1024 && (int64_t)r.T * 32 < cols) r.T <<= 1;
+    r.L = (int)((cols + r.T - 1) / r.T);
+    r.city = d_cityblock;
+    r.chess = d_chessboard;
+    r.cham = d_chamfer34;
+    const int padW = (int)(cols + cols / r.L + 1);
+    const int smem = (2 * padW + 2 * r.T) * 4;
+    e = cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    k_raster<<<(unsigned)rows, r.T, smem, st>>>(r);
+    ++g_launches;
+    e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                       const int32_t* d_label, uint32_t* d_ordinal, dfc_stream_t stream) {
+    if (!d_img || !d_label || !d_ordinal) return DFC_ERR_ARG;
+    if (!shape_ok(rows, cols)) return DFC_ERR_SHAPE;
+    if (pitch_bytes < cols) return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nw = (int)((cols + 31) / 32);
+    Scratch sc(st);
+    const size_t words = 2 * (size_t)rows * nw + 2 * (size_t)rows;
+    cudaError_t e = sc.alloc(words * 4);
+    if (e != cudaSuccess) return cuda_fail(e);
+    uint32_t* masks = static_cast<uint32_t*>(sc.p);
+    uint32_t* wpre = masks + rows * nw;
+    uint32_t* rowcnt = wpre + rows * nw;
+    uint32_t* rowbase = rowcnt + rows;
+    k_ord_rows<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, st>>>(d_img, pitch_bytes, (int)rows,
+                                                                   (int)cols, nw, masks, wpre, rowcnt);
+    k_ord_scan<<<1, 1024, 0, st>>>(rowcnt, rowbase, (int)rows);
+    const int64_t n = rows * cols;
+    k_ord_map<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(
+        d_label, n, (int)cols, nw, masks, wpre, rowbase, d_ordinal);
+    g_launches += 3;
+    e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_end) {
+    g_ev[0] = static_cast<cudaEvent_t>(ev_col_begin);
+    g_ev[1] = static_cast<cudaEvent_t>(ev_row_begin);
+    g_ev[2] = static_cast<cudaEvent_t>(ev_row_end);
+    return DFC_OK;
+}
+
+int dfc_last_launch_count(void) { return g_launches; }
+
+int dfc_last_cuda_error(void) { return g_last_cuda; }
+
+const char* dfc_status_string(int status) {
+    switch (status) {
+        case DFC_OK: return "ok";
+        case DFC_ERR_SHAPE: return "unsupported shape (rows/cols range or int32 distance bound)";
+        case DFC_ERR_ARG: return "invalid argument";
+        case DFC_ERR_CUDA: return "CUDA error";
+        case DFC_ERR_NCCL: return "NCCL error";
+        case DFC_ERR_NO_FEATURES: return "no features: voronoi labels undefined";
+        default: return "unknown status";
+    }
+}
+
+const char* dfc_version(void) { return "distfield-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// k_columns.cu -- stage 1 of the separable EDT: the per-column nearest-object scan.
+//
+// Replaces vertical_pass = init_distance_map + vertical_down_pass +
+// vertical_up_pass (exact_edt.cpp:74-117, grid.cpp:85-91) and the src_row
+// bookkeeping of voronoi_labels (exact_edt.cpp:327-360).  Instead of walking
+// each column serially through a uint64 map (stride cols*8 B), the image is
+// cut into bands of 32 rows; a thread owns 4 adjacent columns of one band and
+// turns the band into four 32-bit row masks with ONE coalesced 4-byte load
+// per row.  Nearest object above/below inside the band is then a clz/ffs on
+// the mask; across bands it comes from per-(band, column) carries:
+//
+//   K1a k_band_summary : first/last object row of every (band, column)
+//   K1b k_band_scan    : per column, turns them into "nearest object row
+//                        above this band" / "below this band" carries
+//   K1c k_band_fill    : per pixel, the nearest object row in its column
+//                        (uint16, upper row on ties -- the reference's strict
+//                        '>' keeps the down-pass feature, exact_edt.cpp:351),
+//                        or the squared vertical distance itself (int32).
+//
+// Both polarities (object = nonzero, and object = zero for the inverted image,
+// grid.cpp:38-44) come out of one read of the input ("slots").
+#include "dfc_kernels.cuh"
+
+namespace dfc {
+
+// Load the 32 rows of one band for 4 columns [j0, j0+4) and return one row
+// mask per column (bit r = row r0+r is an object pixel, i.e. nonzero byte).
+__device__ __forceinline__ void band_masks(const uint8_t* __restrict__ base, int64_t pitch,
+                                           int nrows, int j0, int W, bool vec,
+                                           uint32_t (&m)[4]) {
+    m[0] = m[1] = m[2] = m[3] = 0u;
+    if (vec && j0 + 3 < W) {
+        uint32_t v[kBand];
+#pragma unroll
+        for (int r = 0; r < kBand; ++r)
+            v[r] = r < nrows ? __ldg(reinterpret_cast<const uint32_t*>(base + r * pitch + j0)) : 0u;
+#pragma unroll
+        for (int r = 0; r < kBand; ++r) {
+            const uint32_t nz = __vcmpne4(v[r], 0u);  // 0xff per nonzero byte
+            m[0] |= (nz & 1u) << r;
+            m[1] |= ((nz >> 8) & 1u) << r;
+            m[2] |= ((nz >> 16) & 1u) << r;
+            m[3] |= ((nz >> 24) & 1u) << r;
+        }
+    } else {
+        for (int r = 0; r < nrows; ++r) {
+            const uint8_t* row = base + r * pitch;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (j0 + c < W && row[j0 + c] != 0) m[c] |= 1u << r;
+        }
+    }
+}
+
+// Mask of the polarity `slot_pol` (0: object = nonzero, 1: object = zero).
+__device__ __forceinline__ uint32_t pol_mask(uint32_t m, int pol, uint32_t valid) {
+    return pol ? (~m & valid) : m;
+}
+
+
+// K1a: grid (ceil(W/4)/blockDim, nb, n_img)
+__global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t* __restrict__ last) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j0 = 4 * g;
+    if (j0 >= a.W) return;
+    const int b = blockIdx.y, im = blockIdx.z;
+    const int r0 = b * kBand;
+    const int nrows = min(kBand, a.H - r0);
+    const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
+    uint32_t m[4];
+    band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    for (int s = 0; s < a.npol; ++s) {
+        const int pol = a.pol0 + s;
+        uint16_t f[4], l[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t mk = (j0 + c < a.W) ? pol_mask(m[c], pol, valid) : 0u;
+            f[c] = mk ? (uint16_t)(r0 + __ffs(mk) - 1) : kNoRow;
+            l[c] = mk ? (uint16_t)(r0 + 31 - __clz(mk)) : kNoRow;
+        }
+        const int64_t off = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
+        *reinterpret_cast<uint2*>(first + off) =
+            make_uint2(f[0] | ((uint32_t)f[1] << 16), f[2] | ((uint32_t)f[3] << 16));
+        *reinterpret_cast<uint2*>(last + off) =
+            make_uint2(l[0] | ((uint32_t)l[1] << 16), l[2] | ((uint32_t)l[3] << 16));
+    }
+}
+
+// K1b: one thread per (column, slot*image); in place: last[b] becomes the
+// nearest object row ABOVE band b, first[b] the nearest object row BELOW it.
+__global__ void k_band_scan(int W, int Wp, int nb, int64_t n_planes, uint16_t* __restrict__ first,
+                            uint16_t* __restrict__ last) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t plane = blockIdx.y;
+    if (j >= W || plane >= n_planes) return;
+    uint16_t* F = first + plane * nb * (int64_t)Wp + j;
+    uint16_t* Lp = last + plane * nb * (int64_t)Wp + j;
+    uint16_t run = kNoRow;
+    int b = 0;
+    for (; b + 4 <= nb; b += 4) {  // 4 independent loads in flight
+        uint16_t t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = Lp[(int64_t)(b + u) * Wp];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            Lp[(int64_t)(b + u) * Wp] = run;
+            if (t[u] != kNoRow) run = t[u];
+        }
+    }
+    for (; b < nb; ++b) {
+        const uint16_t t = Lp[(int64_t)b * Wp];
+        Lp[(int64_t)b * Wp] = run;
+        if (t != kNoRow) run = t;
+    }
+    run = kNoRow;
+    b = nb - 1;
+    for (; b - 3 >= 0; b -= 4) {
+        uint16_t t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = F[(int64_t)(b - u) * Wp];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            F[(int64_t)(b - u) * Wp] = run;
+            if (t[u] != kNoRow) run = t[u];
+        }
+    }
+    for (; b >= 0; --b) {
+        const uint16_t t = F[(int64_t)b * Wp];
+        F[(int64_t)b * Wp] = run;
+        if (t != kNoRow) run = t;
+    }
+}
+
+// K1c: per pixel nearest object row (OUT_SQ=false: uint16 plane [slot][img][H][Wp])
+// or the squared vertical distance (OUT_SQ=true: int32, dense [img][H][W]).
+template <bool OUT_SQ>
+__global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
+                            const uint16_t* __restrict__ above, uint16_t* __restrict__ nr,
+                            int32_t* __restrict__ vsq) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j0 = 4 * g;
+    if (j0 >= a.W) return;
+    const int b = blockIdx.y, im = blockIdx.z;
+    const int r0 = b * kBand;
+    const int nrows = min(kBand, a.H - r0);
+    const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
+    uint32_t m[4];
+    band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    for (int s = 0; s < a.npol; ++s) {
+        const int pol = a.pol0 + s;
+        const int64_t coff = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
+        const uint2 ab = *reinterpret_cast<const uint2*>(above + coff);
+        const uint2 bl = *reinterpret_cast<const uint2*>(below + coff);
+        const uint32_t ca[4] = {ab.x & 0xffffu, ab.x >> 16, ab.y & 0xffffu, ab.y >> 16};
+        const uint32_t cb[4] = {bl.x & 0xffffu, bl.x >> 16, bl.y & 0xffffu, bl.y >> 16};
+        uint32_t mk[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mk[c] = pol_mask(m[c], pol, valid);
+        for (int r = 0; r < nrows; ++r) {
+            const uint32_t i = r0 + r;
+            uint32_t out[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const uint32_t up = mk[c] & (0xffffffffu >> (31 - r));   // rows r0..i
+                const uint32_t dn = mk[c] >> r;                          // rows i..
+                const uint32_t ra = up ? (uint32_t)(r0 + 31 - __clz(up)) : ca[c];
+                const uint32_t rb = dn ? (uint32_t)(i + __ffs(dn) - 1) : cb[c];
+                out[c] = pick_nearest(i, ra, rb);
+            }
+            if (!OUT_SQ) {
+                const int64_t off = (((int64_t)s * a.n_img + im) * a.H + i) * a.Wp + j0;
+                *reinterpret_cast<uint2*>(nr + off) =
+                    make_uint2(out[0] | (out[1] << 16), out[2] | (out[3] << 16));
+            } else {
+                int32_t* row = vsq + (((int64_t)s * a.n_img + im) * a.H + i) * (int64_t)a.W;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (j0 + c >= a.W) break;
+                    const uint32_t r_ = out[c];
+                    const uint32_t d = r_ == kNoRow ? (uint32_t)DFC_INF_I32
+                                                    : sq(i > r_ ? i - r_ : r_ - i);
+                    row[j0 + c] = (int32_t)d;
+                }
+            }
+        }
+    }
+}
+
+template __global__ void k_band_fill<false>(ColArgs, const uint16_t*, const uint16_t*, uint16_t*, int32_t*);
+template __global__ void k_band_fill<true>(ColArgs, const uint16_t*, const uint16_t*, uint16_t*, int32_t*);
+
+}  // namespace dfc

@@ -1,0 +1,196 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the pinned CPU oracle.
+
+Bit-exact for every integer output (squared distances, labels, nearest
+columns, city-block / chessboard / chamfer-3-4); float32 distances must equal
+(float)sqrt((double)D) exactly (0 ulp; north_star allows <= 1 ulp).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def dfc():
+    import paper_2106_03503_b200 as m
+    return m
+
+
+def _dev(img):
+    return torch.from_numpy(np.ascontiguousarray(img)).cuda()
+
+
+def _check_edt(dfc, img, polarity=0):
+    out = dfc.edt(_dev(img), polarity=polarity, dist=True, label=True, nearest_col=True)
+    torch.cuda.synchronize()
+    src = img if polarity == 0 else (img == 0).astype(np.uint8)
+    want = oracle.to_i32(oracle.edt(src))
+    got = out["sqdist"].cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(out["dist"].cpu().numpy().view(np.uint32),
+                                  oracle.sqrt_f32(want).view(np.uint32))
+    lab = oracle.voronoi_labels(src, linear=True)
+    want_lab = np.full(src.shape, -1, np.int32) if lab is None else lab[1]
+    np.testing.assert_array_equal(out["label"].cpu().numpy(), want_lab)
+    _, ncol = oracle.meijster_scan(oracle.vertical_pass(src), take_new=True)
+    np.testing.assert_array_equal(out["nearest_col"].cpu().numpy(), ncol.view(np.int32))
+
+
+def test_six_point_golden(dfc):
+    with open(os.path.join(GOLD, "six_point.json")) as f:
+        g = json.load(f)
+    img = np.zeros((g["rows"], g["cols"]), np.uint8)
+    for r, c in g["points"]:
+        img[r, c] = 1
+    out = dfc.edt(_dev(img), label=True)
+    r = dfc.raster(_dev(img))
+    vert = dfc.vertical(_dev(img))
+    torch.cuda.synchronize()
+    m = lambda k: np.where(np.array(g[k]) < 0, 0x7FFFFFFF, np.array(g[k])).astype(np.int32)
+    np.testing.assert_array_equal(out["sqdist"].cpu().numpy(), m("kSquaredEuclidean"))
+    np.testing.assert_array_equal(vert.cpu().numpy(), m("kVerticalFinal"))
+    np.testing.assert_array_equal(r["cityblock"].cpu().numpy(), m("kCityblockFinal"))
+    np.testing.assert_array_equal(r["chamfer34"].cpu().numpy(), m("kChamferFinal"))
+    # test_exact_edt.cpp:238-259: the (0,0) tie resolves to the feature at (4, 1)
+    assert int(out["label"][0, 0]) == 4 * g["cols"] + 1
+
+
+def _cases():
+    z = np.load(os.path.join(GOLD, "random_cases.npz"))
+    for n in range(int(z["n_cases"][0])):
+        yield {k.split("_", 1)[1]: z[k] for k in z.files if k.startswith(f"c{n}_")}
+
+
+@pytest.mark.parametrize("case", list(_cases()),
+                         ids=lambda c: "x".join(map(str, c["meta"][:2])) + f"@{c['density'][0]}")
+def test_reference_fixtures(dfc, case):
+    """The 60 committed outputs of the reference library itself."""
+    img = case["img"]
+    d = _dev(img)
+    out = dfc.edt(d, label=True, nearest_col=True)
+    r = dfc.raster(d)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out["sqdist"].cpu().numpy(), oracle.to_i32(case["edt"]))
+    np.testing.assert_array_equal(out["nearest_col"].cpu().numpy(), case["nearest_col"].view(np.int32))
+    if case["labels"].size:
+        ords = dfc.label_ordinals(d, out["label"]).cpu().numpy()
+        np.testing.assert_array_equal(ords, case["labels"].astype(np.int64))
+    else:
+        assert (out["label"].cpu().numpy() == -1).all()
+    np.testing.assert_array_equal(r["cityblock"].cpu().numpy(), oracle.to_i32(case["cityblock"]))
+    np.testing.assert_array_equal(r["chamfer34"].cpu().numpy(), oracle.to_i32(case["chamfer34"]))
+    np.testing.assert_array_equal(r["chessboard"].cpu().numpy(), oracle.to_i32(case["chessboard"]))
+
+
+SHAPES = [(1, 1), (1, 2), (2, 1), (1, 100), (100, 1), (7, 33), (33, 7), (64, 64), (31, 97),
+          (5, 1000), (3, 1031), (2, 2048), (2, 4096), (3, 4100), (40, 129), (257, 65), (2, 8191),
+          (1, 16384), (1, 32768), (70, 600)]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: f"{s[0]}x{s[1]}")
+@pytest.mark.parametrize("density", [0.0005, 0.01, 0.2, 0.7])
+def test_edt_random(dfc, shape, density):
+    img = oracle.random_image(shape[0], shape[1], density, 1000 * shape[0] + shape[1] + int(density * 1e4))
+    _check_edt(dfc, img, 0)
+
+
+@pytest.mark.parametrize("shape", [(48, 48), (3, 2000), (129, 300)])
+def test_edt_polarity_inside(dfc, shape):
+    img = oracle.random_image(shape[0], shape[1], 0.6, 77 + shape[1])
+    _check_edt(dfc, img, 1)
+
+
+def test_edt_degenerate(dfc):
+    for img in (np.zeros((5, 7), np.uint8), np.ones((4, 9), np.uint8), np.zeros((1, 1), np.uint8)):
+        _check_edt(dfc, img)
+    corner = np.zeros((300, 2000), np.uint8)
+    corner[299, 1999] = 1
+    _check_edt(dfc, corner)
+    ties = np.zeros((41, 41), np.uint8)
+    for (r, c) in [(0, 0), (0, 40), (40, 0), (40, 40), (20, 20), (10, 30), (30, 10)]:
+        ties[r, c] = 1
+    _check_edt(dfc, ties)
+
+
+def test_pitch_and_bool_input(dfc):
+    img = oracle.random_image(50, 70, 0.03, 5)
+    big = np.zeros((50, 131), np.uint8)
+    big[:, 3:73] = img * 9  # nonzero bytes other than 1 are objects too (grid.hpp:82)
+    t = _dev(big)[:, 3:73]
+    out = dfc.edt(t, dist=False)
+    out_b = dfc.edt(_dev(img.astype(bool)), dist=False)
+    torch.cuda.synchronize()
+    want = oracle.to_i32(oracle.edt(img))
+    np.testing.assert_array_equal(out["sqdist"].cpu().numpy(), want)
+    np.testing.assert_array_equal(out_b["sqdist"].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("shape", [(64, 64), (100, 301), (1, 500), (256, 4096)])
+def test_dual_polarity(dfc, shape):
+    from paper_2106_03503_b200 import workloads
+    img = workloads.discs(shape[0], shape[1], 12, 3 + shape[1])
+    out = dfc.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    w0 = oracle.to_i32(oracle.edt(img))
+    w1 = oracle.to_i32(oracle.edt((img == 0).astype(np.uint8)))
+    np.testing.assert_array_equal(out["sqdist_bg"].cpu().numpy(), w0)
+    np.testing.assert_array_equal(out["sqdist_obj"].cpu().numpy(), w1)
+    np.testing.assert_array_equal(out["dist_bg"].cpu().numpy(), oracle.sqrt_f32(w0))
+    np.testing.assert_array_equal(out["dist_obj"].cpu().numpy(), oracle.sqrt_f32(w1))
+
+
+def test_batched_points(dfc):
+    from paper_2106_03503_b200 import workloads
+    imgs = workloads.points_batch(24, 128, 96, 30, 99)
+    imgs[5] = 0  # a featureless image inside the batch
+    out = dfc.edt_batched(_dev(imgs), dist=True, label=True)
+    torch.cuda.synchronize()
+    d, s, lab = (out[k].cpu().numpy() for k in ("sqdist", "dist", "label"))
+    for b in range(imgs.shape[0]):
+        want = oracle.to_i32(oracle.edt(imgs[b]))
+        np.testing.assert_array_equal(d[b], want)
+        np.testing.assert_array_equal(s[b], oracle.sqrt_f32(want))
+        wl = oracle.voronoi_labels(imgs[b], linear=True)
+        np.testing.assert_array_equal(lab[b], np.full(imgs[b].shape, -1, np.int32) if wl is None else wl[1])
+
+
+def test_vertical_pass(dfc):
+    for shape, dens in (((70, 90), 0.03), ((1, 50), 0.1), ((300, 7), 0.005), ((97, 1000), 0.001)):
+        img = oracle.random_image(*shape, dens, shape[0] + 7)
+        got = dfc.vertical(_dev(img))
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy(), oracle.to_i32(oracle.vertical_pass(img)))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (9, 10), (64, 64), (50, 1500), (3, 5000), (333, 77)])
+@pytest.mark.parametrize("density", [0.0, 0.003, 0.05, 0.5])
+def test_raster_random(dfc, shape, density):
+    img = oracle.random_image(shape[0], shape[1], density, 7 * shape[0] + shape[1])
+    r = dfc.raster(_dev(img))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(r["cityblock"].cpu().numpy(), oracle.to_i32(oracle.cityblock(img)))
+    np.testing.assert_array_equal(r["chamfer34"].cpu().numpy(), oracle.to_i32(oracle.chamfer34(img)))
+    np.testing.assert_array_equal(r["chessboard"].cpu().numpy(), oracle.to_i32(oracle.chessboard(img)))
+
+
+def test_label_ordinals(dfc):
+    img = oracle.random_image(80, 120, 0.02, 11)
+    out = dfc.edt(_dev(img), label=True, dist=False)
+    ords = dfc.label_ordinals(_dev(img), out["label"])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ords.cpu().numpy(), oracle.voronoi_labels(img).astype(np.int64))
+
+
+def test_shape_errors(dfc):
+    with pytest.raises(dfc.DfcError):
+        dfc.edt(torch.zeros((70000, 1), dtype=torch.uint8, device="cuda"))  # more rows than supported
+    with pytest.raises(dfc.DfcError):
+        dfc.edt(torch.zeros((2, 40000), dtype=torch.uint8, device="cuda"))  # row wider than supported
