@@ -167,6 +167,9 @@ def run_ours(args, rank, world, local_rank):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    for tup in ev:  # torch creates the cudaEvent_t lazily at the first record
+        for e in tup:
+            e.record(stream)
     clocks = ClockSampler(local_rank)
     if world > 1:
         dist.barrier()

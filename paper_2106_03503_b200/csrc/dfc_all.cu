@@ -1,0 +1,7 @@
+// dfc_all.cu -- the single translation unit of libdfc.so: every kernel and
+// the C ABI are compiled together (whole-program, no relocatable device
+// code), so kernel host stubs, templates and registrations live in one unit.
+#include "k_columns.cu"
+#include "k_rows.cu"
+#include "k_raster.cu"
+#include "dfc_api.cu"
