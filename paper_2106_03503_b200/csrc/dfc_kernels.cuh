@@ -43,18 +43,9 @@ struct RasterArgs {
     int32_t* cham;
 };
 
-__global__ void k_band_summary(ColArgs a, uint16_t* first, uint16_t* last);
-__global__ void k_band_scan(int W, int Wp, int nb, int64_t n_planes, uint16_t* first, uint16_t* last);
-template <bool OUT_SQ>
-__global__ void k_band_fill(ColArgs a, const uint16_t* below, const uint16_t* above, uint16_t* nr,
-                            int32_t* vsq);
-template <bool TAKE_NEW>
-__global__ void k_rows(RowArgs a);
-__global__ void k_raster(RasterArgs a);
-__global__ void k_ord_rows(const uint8_t* img, int64_t pitch, int H, int W, int nw, uint32_t* masks,
-                           uint32_t* wpre, uint32_t* rowcnt);
-__global__ void k_ord_scan(const uint32_t* rowcnt, uint32_t* rowbase, int H);
-__global__ void k_ord_map(const int32_t* label, int64_t n, int W, int nw, const uint32_t* masks,
-                          const uint32_t* wpre, const uint32_t* rowbase, uint32_t* out);
+// The kernels themselves are defined in k_columns.cu / k_rows.cu / k_raster.cu and
+// compiled in ONE translation unit with the C ABI (dfc_all.cu), so no
+// forward declarations are needed (a declaration whose parameter qualifiers
+// differ from the definition would name a different, undefined kernel).
 
 }  // namespace dfc
