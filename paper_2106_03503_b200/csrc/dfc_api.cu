@@ -67,14 +67,17 @@ struct RowGeom {
     int T, L, R, row_words, smem_bytes;
 };
 
+// T threads per row (power of two, 32..1024), L = 2^k columns per thread.
 RowGeom row_geom(int W) {
     RowGeom g;
     g.T = 32;
     while (g.T < 1024 && (int64_t)g.T * 32 < W) g.T <<= 1;
-    g.L = (int)round_up((W + g.T - 1) / g.T, 4);
+    const int per = (W + g.T - 1) / g.T;
+    g.L = 4;
+    while (g.L < per) g.L <<= 1;
     g.R = g.T >= 256 ? 1 : 256 / g.T;
-    g.row_words = (g.T * (g.L + 2)) / 2 + g.T * (g.L + 1) + 2 * g.T;
-    g.smem_bytes = (g.R * g.row_words + (g.R * g.T) / 32) * 4;
+    g.row_words = dfc::row_words(g.T, g.L);
+    g.smem_bytes = g.R * g.row_words * 4;
     return g;
 }
 
@@ -147,16 +150,12 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             out_vec_ok(NC, sN);
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
-    cudaError_t e;
-    if (take_new) {
-        e = cudaFuncSetAttribute(k_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
-        if (e != cudaSuccess) return cuda_fail(e);
-        k_rows<true><<<(unsigned)blocks, g.R * g.T, g.smem_bytes, st>>>(a);
-    } else {
-        e = cudaFuncSetAttribute(k_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
-        if (e != cudaSuccess) return cuda_fail(e);
-        k_rows<false><<<(unsigned)blocks, g.R * g.T, g.smem_bytes, st>>>(a);
-    }
+    const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e);
+    void* args[] = {&a};
+    e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e);
     ++g_launches;
     return DFC_OK;
 }

@@ -5,113 +5,187 @@
 // (exact_edt.cpp:190-283) and the label assembly of voronoi_labels
 // (exact_edt.cpp:362-369).  The reference walks a row serially with one
 // std::vector stack per row; here a row is owned by T threads (T*L >= cols,
-// L columns per thread) of one CTA and processed in three phases, all in
-// shared memory:
+// L = 2^k columns per thread, compile-time) of one CTA, in shared memory:
 //
 //  1. build   each thread runs the reference's stack algorithm (Meijster,
 //             exact integer boundaries, exact_edt.cpp:200-223) over ITS L
-//             columns, producing the lower envelope of its segment's
-//             parabolas over the whole domain [0, cols);
-//  2. merge   log2(T) levels of pairwise merges of adjacent segment groups.
-//             For groups A < B (all columns of A left of B) E_A - E_B is
-//             strictly increasing in j, so B takes over from A at ONE column
-//             x (the first j where B beats A under the tie rule).  The
-//             2^(l+1) threads of a merge find x with a (2^(l+1)+1)-ary search,
-//             evaluating both group envelopes at their probe columns.  Each
-//             segment keeps a "cut": the first column it may own.
-//  3. fill    each thread walks its own columns, following cuts and segment
-//             stacks (owners are monotone in j), and writes D, sqrt(D),
-//             label and/or nearest column.
+//             columns: the lower envelope of its segment's parabolas over the
+//             whole domain [0, cols), as a stack of (column, start) entries;
+//  2. merge   log2(T) levels of pairwise merges of adjacent segment groups
+//             A < B.  E_A - E_B is strictly increasing in j (all columns of A
+//             are left of B's), so B takes over from A at ONE column x.  One
+//             leader thread per merge finds x by walking envelope "pieces"
+//             (a parabola together with the columns it owns in its group)
+//             outward from B's first column: inside the overlap of the
+//             current A piece and B piece the takeover column of the two
+//             parabolas is a closed-form integer expression, so each step
+//             either lands on x or discards one piece.  Dense rows finish in
+//             O(1) steps, sparse rows have few pieces.  Every segment keeps a
+//             "cut", the first column it may own inside its current group.
+//  3. fill    each thread walks its own columns along cuts and stacks (the
+//             owner column is monotone in j) and writes D, sqrt(D), the
+//             label and/or the nearest column.
 //
 // Tie rules are order-independent and therefore exact under any merge order:
 // keep_old (the label rule, exact_edt.cpp:205/:363) hands a tie to the
-// SMALLER column everywhere -- in the segment stacks (floor(x)+1 boundaries)
-// and in the merges ("B beats A" only when strictly smaller); take_new
+// SMALLER column everywhere -- in the stacks (floor(x)+1 boundaries) and in
+// the merges (B takes over only where strictly smaller); take_new
 // (meijster_scan's nearest_col, exact_edt.cpp:275) to the LARGER column.
-// The label of a cell is then (nearest_row_k, k) of its owner k, the upper
-// feature on vertical ties (stage 1).
+// The label of a cell is (nearest_row_k, k) of its owner k; stage 1 already
+// resolved vertical ties to the upper feature.
 //
-// All arithmetic is int32/int64 and exact: every value is bounded by
-// (rows-1)^2 + (cols-1)^2 <= 2^31-2 (DFC_MAX_SQDIST), see SURVEY.md finding 7.
+// All arithmetic is exact 32/64-bit integer: every value is bounded by
+// (rows-1)^2 + (cols-1)^2 <= 2^31-2 (DFC_MAX_SQDIST, SURVEY.md finding 7).
 #include "dfc_kernels.cuh"
 
 namespace dfc {
 
-
-// Segment-padded index of column j in the per-row nr array: each thread's L
-// columns are followed by 2 pad halfwords so the build phase (thread t reads
-// column t*L + x) is bank-conflict free (word stride L/2+1 is odd).
-__device__ __forceinline__ int nidx(int j, int L) { return (j / L) * (L + 2) + (j % L); }
-
-struct RowSmem {
-    uint16_t* nrs;   // [T*(L+2)]
-    uint32_t* stk;   // [T*(L+1)]  entry = k | start << 16
-    int* cut;        // [T]
-    int* cnt;        // [T]
+template <int L>
+struct RowLayout {
+    static constexpr int kLog = L == 4 ? 2 : L == 8 ? 3 : L == 16 ? 4 : L == 32 ? 5 : L == 64 ? 6 : 7;
+    // Segment-padded index of column j in the per-row nr array: each thread's
+    // L columns are followed by 2 pad halfwords so the build phase (thread t
+    // reads column t*L + x) is bank-conflict free (word stride L/2+1 is odd).
+    __device__ static __forceinline__ int nidx(int j) { return (j >> kLog) * (L + 2) + (j & (L - 1)); }
+    static constexpr int stk_stride = L + 1;  // odd word stride: conflict-free
 };
 
-__device__ __forceinline__ RowSmem row_smem(uint32_t* base, int T, int L) {
-    RowSmem s;
-    s.nrs = reinterpret_cast<uint16_t*>(base);
-    uint32_t* p = base + (T * (L + 2)) / 2;
-    s.stk = p;
-    p += T * (L + 1);
-    s.cut = reinterpret_cast<int*>(p);
-    p += T;
-    s.cnt = reinterpret_cast<int*>(p);
-    return s;
-}
+struct Piece {
+    int s, e;      // segment, stack entry
+    int k;         // parabola column (-1: empty group)
+    uint32_t g;    // its vertical value
+    int lo, hi;    // columns it owns inside its group: [lo, hi)
+};
 
-__device__ __forceinline__ uint32_t g_of(const RowSmem& sm, int L, uint32_t i, uint32_t k) {
-    const uint32_t r = sm.nrs[nidx((int)k, L)];
-    const uint32_t a = i > r ? i - r : r - i;
-    return a * a;
-}
+template <int L, bool TAKE_NEW>
+struct RowCtx {
+    const uint16_t* nrs;
+    const uint32_t* stk;
+    const int* cut;
+    const int* cnt;
+    uint32_t i;
+    int W;
 
-// Envelope value of one segment's stack at column j (kInfU if the segment has
-// no finite parabola); also returns the serving entry.
-__device__ __forceinline__ uint32_t eval_seg(const RowSmem& sm, int L, uint32_t i, int s, int j) {
-    const int n = sm.cnt[s];
-    if (n == 0) return kInfU;
-    const uint32_t* st = sm.stk + s * (L + 1);
-    int lo = 0, hi = n - 1;  // last e with start(e) <= j; start(0) == 0
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if ((int)(st[mid] >> 16) <= j) lo = mid; else hi = mid - 1;
+    __device__ __forceinline__ uint32_t g_of(int k) const {
+        const uint32_t r = nrs[RowLayout<L>::nidx(k)];
+        const uint32_t a = i > r ? i - r : r - i;
+        return a * a;
     }
-    const uint32_t k = st[lo] & 0xffffu;
-    const int dj = j - (int)k;
-    return g_of(sm, L, i, k) + (uint32_t)(dj * dj);
-}
-
-// Owner segment of column j inside segments [s0, s1): the last s with cut[s] <= j.
-__device__ __forceinline__ int owner_seg(const RowSmem& sm, int s0, int s1, int j) {
-    int lo = s0, hi = s1 - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (sm.cut[mid] <= j) lo = mid; else hi = mid - 1;
+    __device__ __forceinline__ int start(int s, int e) const {
+        return (int)(stk[s * RowLayout<L>::stk_stride + e] >> 16);
     }
-    return lo;
-}
+    // last s in [s0, s1) with cut[s] <= j (cut[s0] == 0 inside a group)
+    __device__ __forceinline__ int owner(int s0, int s1, int j) const {
+        int lo = s0, hi = s1 - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cut[mid] <= j) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    }
+    // last entry of segment s with start <= j (start(s, 0) == 0)
+    __device__ __forceinline__ int entry(int s, int n, int j) const {
+        const uint32_t* st = stk + s * RowLayout<L>::stk_stride;
+        int lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int)(st[mid] >> 16) <= j) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    }
+    __device__ __forceinline__ void make_piece(Piece& p, int s, int e, int n, int s1) const {
+        const uint32_t ent = stk[s * RowLayout<L>::stk_stride + e];
+        p.s = s;
+        p.e = e;
+        p.k = (int)(ent & 0xffffu);
+        p.g = g_of(p.k);
+        const int seg_hi = s + 1 < s1 ? cut[s + 1] : W;
+        p.lo = max((int)(ent >> 16), cut[s]);
+        p.hi = min(e + 1 < n ? start(s, e + 1) : W, seg_hi);
+    }
+    // the piece of group [s0, s1) owning column j; k = -1 if the group is empty
+    __device__ __forceinline__ void piece_at(Piece& p, int s0, int s1, int j) const {
+        const int s = owner(s0, s1, j);
+        const int n = cnt[s];
+        if (n == 0) {
+            p.k = -1;
+            return;
+        }
+        make_piece(p, s, entry(s, n, j), n, s1);
+    }
 
-template <bool TAKE_NEW>
-__device__ __forceinline__ bool beats(uint32_t eb, uint32_t ea) {
-    return TAKE_NEW ? (eb <= ea && eb != kInfU) : (eb < ea);
-}
+    // First column x at which group B = [sm, s1) beats group A = [s0, sm)
+    // (W if never).  The predicate is monotone in j; see the file comment.
+    __device__ int takeover(int s0, int sm, int s1) const {
+        const int p0 = min(sm * L, W - 1);
+        Piece a, b;
+        piece_at(b, sm, s1, p0);
+        if (b.k < 0) return W;   // B has no finite parabola: never beats
+        piece_at(a, s0, sm, p0);
+        if (a.k < 0) return 0;   // A empty: B owns everything
+        int moved = 0;           // -1 after a step left, +1 after a step right
+        // each step discards a piece, so 2*W+2 steps bound the walk (defensive)
+        for (int guard = 0; guard < 2 * W + 2; ++guard) {
+            const int lo = max(a.lo, b.lo), hi = min(a.hi, b.hi);
+            // b beats a from xab on, with
+            //   keep_old: xab = floor(num/den) + 1,  take_new: xab = ceil(num/den)
+            const int64_t num = (int64_t)b.g - (int64_t)a.g + (int64_t)b.k * b.k - (int64_t)a.k * a.k;
+            const int64_t den = 2 * (int64_t)(b.k - a.k);
+            const int64_t dlo = den * lo, dhi = den * (hi - 1);
+            if (TAKE_NEW ? num <= dlo : num < dlo) {          // xab <= lo: move left
+                if (lo == 0 || moved > 0) return lo;  // true at lo, false at lo-1
+                moved = -1;
+                const int j = lo - 1;
+                // the previous piece is the previous stack entry unless the segment starts at lo
+                if (a.lo == lo) {
+                    if (a.lo > cut[a.s]) make_piece(a, a.s, a.e - 1, cnt[a.s], sm);
+                    else piece_at(a, s0, sm, j);
+                }
+                if (b.lo == lo) {
+                    if (b.lo > cut[b.s]) make_piece(b, b.s, b.e - 1, cnt[b.s], s1);
+                    else piece_at(b, sm, s1, j);
+                }
+            } else if (TAKE_NEW ? num > dhi : num >= dhi) {   // xab >= hi: move right
+                if (hi == W || moved < 0) return hi;  // false at hi-1, true at hi
+                moved = 1;
+                const int j = hi;
+                // the next piece is the next stack entry unless the segment ends at hi
+                if (a.hi == hi) {
+                    if (hi < (a.s + 1 < sm ? cut[a.s + 1] : W)) make_piece(a, a.s, a.e + 1, cnt[a.s], sm);
+                    else piece_at(a, s0, sm, j);
+                }
+                if (b.hi == hi) {
+                    if (hi < (b.s + 1 < s1 ? cut[b.s + 1] : W)) make_piece(b, b.s, b.e + 1, cnt[b.s], s1);
+                    else piece_at(b, sm, s1, j);
+                }
+            } else {                                           // lo < xab < hi
+                const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
+                return TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
+            }
+        }
+        return W;
+    }
+};
 
-template <bool TAKE_NEW>
+template <int L, bool TAKE_NEW>
 __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
+    using LY = RowLayout<L>;
     extern __shared__ uint32_t smem[];
-    const int T = a.T, L = a.L;
+    const int T = a.T;
     const int rho = threadIdx.x / T;          // row within the CTA
     const int s = threadIdx.x - rho * T;      // segment (thread) within the row
-    const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * a.R + rho;
     const bool active = row < a.total_rows;
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const int W = a.W;
-    RowSmem sm = row_smem(smem + rho * a.row_smem_words, T, L);
+
+    uint32_t* base = smem + rho * a.row_smem_words;
+    uint16_t* nrs = reinterpret_cast<uint16_t*>(base);            // [T*(L+2)]
+    uint32_t* stk = base + (T * (L + 2)) / 2;                     // [T*(L+1)]
+    int* cut = reinterpret_cast<int*>(stk + T * LY::stk_stride);  // [T]
+    int* cnt = cut + T;                                           // [T]
+    int* xs = cnt + T;                                            // [T] takeover per merge
 
     // ---- 0. stage the row's nearest-row values (coalesced 4-byte loads) ----
     if (active) {
@@ -119,47 +193,50 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
                                                                 (int64_t)i * a.Wp);
         const int npairs = (W + 1) >> 1;
         for (int q = s; q < npairs; q += T)
-            *reinterpret_cast<uint32_t*>(sm.nrs + nidx(2 * q, L)) = __ldg(src + q);
+            *reinterpret_cast<uint32_t*>(nrs + LY::nidx(2 * q)) = __ldg(src + q);
     }
     __syncthreads();
 
     // ---- 1. per-segment envelope (exact_edt.cpp:208-223) ----
     {
         const int c0 = s * L, c1 = min(c0 + L, W);
-        uint32_t* st = sm.stk + s * (L + 1);
+        uint32_t* st = stk + s * LY::stk_stride;
         int n = 0;
         int tk = 0, ts = 0;   // top entry: column, start
-        uint32_t tg = 0;      // top entry: vertical value
+        int tg = 0;           // top entry: vertical value
         if (active) {
             for (int m = c0; m < c1; ++m) {
-                const uint32_t r = sm.nrs[nidx(m, L)];
+                const uint32_t r = nrs[LY::nidx(m)];
                 if (r == kNoRow) continue;  // sentinel vertex never enters (:212)
-                const uint32_t am = i > r ? i - r : r - i;
-                const uint32_t gm = am * am;
-                int64_t num = 0, den = 1;
+                const int am = (int)(i > r ? i - r : r - i);
+                const int gm = am * am;
+                const int mm = m * m;
+                int num = 0;
+                uint32_t den = 1;
                 while (n > 0) {
-                    num = (int64_t)gm - (int64_t)tg + (int64_t)m * m - (int64_t)tk * tk;
-                    den = 2 * (int64_t)(m - tk);
-                    const int64_t lim = (int64_t)ts * den;  // start <= js[idx]  (:214)
-                    if (TAKE_NEW ? (num <= lim) : (num < lim)) {
-                        if (--n > 0) {
-                            const uint32_t e = st[n - 1];
-                            tk = (int)(e & 0xffffu);
-                            ts = (int)(e >> 16);
-                            tg = g_of(sm, L, i, (uint32_t)tk);
-                        }
-                    } else {
-                        break;
+                    // num = v_m - v_k - k^2 + m^2 fits int32 (|.| < 2^31); ts*den < 2^32
+                    num = gm - tg + (mm - tk * tk);
+                    den = 2u * (uint32_t)(m - tk);
+                    const uint32_t lim = (uint32_t)ts * den;  // start <= js[idx]  (:214)
+                    const bool pop = num < 0 || (TAKE_NEW ? (uint32_t)num <= lim : (uint32_t)num < lim);
+                    if (!pop) break;
+                    if (--n > 0) {
+                        const uint32_t e = st[n - 1];
+                        tk = (int)(e & 0xffffu);
+                        ts = (int)(e >> 16);
+                        const uint32_t rk = nrs[LY::nidx(tk)];
+                        const int ak = (int)(i > rk ? i - rk : rk - i);
+                        tg = ak * ak;
                     }
                 }
                 int start = 0;
                 if (n > 0) {
-                    // push iff start <= cols-1 (:218); num >= 0 here
-                    const int64_t lim = (int64_t)(W - 1) * den;
-                    if (TAKE_NEW ? (num > lim) : (num >= lim)) continue;
-                    const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
+                    // push iff start <= cols-1 (:218); here 0 <= num
+                    const uint32_t lim = (uint32_t)(W - 1) * den;
+                    if (TAKE_NEW ? (uint32_t)num > lim : (uint32_t)num >= lim) continue;
+                    const uint32_t q = small_udiv((uint32_t)num, den);
                     // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
-                    start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
+                    start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * den)) : (int)q + 1;
                 }
                 st[n++] = (uint32_t)m | ((uint32_t)start << 16);
                 tk = m;
@@ -167,109 +244,45 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
                 tg = gm;
             }
         }
-        sm.cnt[s] = n;
-        sm.cut[s] = 0;
+        cnt[s] = n;
+        cut[s] = 0;
     }
     __syncthreads();
 
-    // ---- 2. merge adjacent segment groups ----
+    RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, i, W};
+
+    // ---- 2. merge adjacent segment groups, one leader per merge ----
     for (int G = 2; G <= T; G <<= 1) {
+        const int gb = s & ~(G - 1);
         const int half = G >> 1;
-        const int gb = (s / G) * G;
-        const int q = s - gb;               // probe index within the merge
-        const bool inB = q >= half;
-        int lo = 0, hi = W;                 // takeover column x lies in [lo, hi]
-        if (G <= 32) {
-            const int sh = (threadIdx.x & 31) & ~(G - 1);
-            const uint32_t gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
-            while (__any_sync(0xffffffffu, active && hi > lo)) {
-                const int n = hi - lo;
-                const int p = lo + (n * (q + 1)) / (G + 1);
-                bool bt = false;
-                if (active && hi > lo) {
-                    const int sa = owner_seg(sm, gb, gb + half, p);
-                    const int sb = owner_seg(sm, gb + half, gb + G, p);
-                    bt = beats<TAKE_NEW>(eval_seg(sm, L, i, sb, p), eval_seg(sm, L, i, sa, p));
-                }
-                const uint32_t bits = (__ballot_sync(0xffffffffu, bt) >> sh) & gmask;
-                if (hi > lo) {
-                    if (bits) {
-                        const int qs = __ffs(bits) - 1;
-                        const int nlo = qs > 0 ? lo + (n * qs) / (G + 1) + 1 : lo;
-                        hi = lo + (n * (qs + 1)) / (G + 1);
-                        lo = nlo;
-                    } else {
-                        lo = lo + (n * G) / (G + 1) + 1;
-                    }
-                }
-            }
-        } else {
-            const int nw = G >> 5;              // warps per merge
-            const int w0 = (rho * T + gb) >> 5; // first warp word of this merge
-            for (;;) {
-                const bool live = active && hi > lo;
-                const int n = hi - lo;
-                const int p = lo + (int)(((int64_t)n * (q + 1)) / (G + 1));
-                bool bt = false;
-                if (live) {
-                    const int sa = owner_seg(sm, gb, gb + half, p);
-                    const int sb = owner_seg(sm, gb + half, gb + G, p);
-                    bt = beats<TAKE_NEW>(eval_seg(sm, L, i, sb, p), eval_seg(sm, L, i, sa, p));
-                }
-                const uint32_t w = __ballot_sync(0xffffffffu, bt);
-                uint32_t* bal = reinterpret_cast<uint32_t*>(smem + a.R * a.row_smem_words);
-                if (lane == 0) bal[threadIdx.x >> 5] = w;
-                __syncthreads();
-                if (live) {
-                    int qs = -1;
-                    for (int t = 0; t < nw; ++t) {
-                        const uint32_t bw = bal[w0 + t];
-                        if (bw) { qs = 32 * t + __ffs(bw) - 1; break; }
-                    }
-                    if (qs >= 0) {
-                        const int nlo = qs > 0 ? lo + (int)(((int64_t)n * qs) / (G + 1)) + 1 : lo;
-                        hi = lo + (int)(((int64_t)n * (qs + 1)) / (G + 1));
-                        lo = nlo;
-                    } else {
-                        lo = lo + (int)(((int64_t)n * G) / (G + 1)) + 1;
-                    }
-                }
-                if (!__syncthreads_or(active && hi > lo)) break;
-            }
+        if (active && s == gb) xs[gb] = cx.takeover(gb, gb + half, gb + G);
+        if (G <= 32) __syncwarp(); else __syncthreads();
+        if (active) {
+            const int x = xs[gb];
+            cut[s] = (s - gb) >= half ? max(cut[s], x) : min(cut[s], x);
         }
-        // x = lo: A keeps [.., x), B takes [x, ..)
-        if (active) sm.cut[s] = inB ? max(sm.cut[s], lo) : min(sm.cut[s], lo);
-        __syncthreads();
+        if (G <= 32) __syncwarp(); else __syncthreads();
     }
+    __syncthreads();
 
     // ---- 3. fill this thread's columns ----
     if (!active) return;
     const int c0 = s * L, c1 = min(c0 + L, W);
     if (c0 >= W) return;
-    int sg = owner_seg(sm, 0, T, c0);
-    int seg_end = sg + 1 < T ? sm.cut[sg + 1] : W;
-    int n = sm.cnt[sg];
-    const uint32_t* st = sm.stk + sg * (L + 1);
-    int e = 0;
-    auto locate = [&](int j) {
-        int lo = 0, hi = n - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if ((int)(st[mid] >> 16) <= j) lo = mid; else hi = mid - 1;
-        }
-        e = lo;
-    };
-    if (n > 0) locate(c0);
+    int sg = cx.owner(0, T, c0);
+    int seg_end = sg + 1 < T ? cut[sg + 1] : W;
+    int n = cnt[sg];
+    int e = n > 0 ? cx.entry(sg, n, c0) : 0;
     uint32_t k = 0, rr = kNoRow, gk = kInfU;
     int next_start = W;
     auto load_entry = [&]() {
         if (n == 0) { k = 0; rr = kNoRow; gk = kInfU; next_start = W; return; }
-        const uint32_t ent = st[e];
+        const uint32_t ent = stk[sg * LY::stk_stride + e];
         k = ent & 0xffffu;
-        rr = sm.nrs[nidx((int)k, L)];
+        rr = nrs[LY::nidx((int)k)];
         const uint32_t av = i > rr ? i - rr : rr - i;
         gk = av * av;
-        next_start = e + 1 < n ? (int)(st[e + 1] >> 16) : W;
+        next_start = e + 1 < n ? (int)(stk[sg * LY::stk_stride + e + 1] >> 16) : W;
     };
     load_entry();
 
@@ -280,11 +293,10 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
 
     auto cell = [&](int j, int32_t& d, int32_t& lab, int32_t& col) {
         if (j >= seg_end) {
-            while (sg + 1 < T && sm.cut[sg + 1] <= j) ++sg;
-            seg_end = sg + 1 < T ? sm.cut[sg + 1] : W;
-            n = sm.cnt[sg];
-            st = sm.stk + sg * (L + 1);
-            if (n > 0) locate(j);
+            while (sg + 1 < T && cut[sg + 1] <= j) ++sg;
+            seg_end = sg + 1 < T ? cut[sg + 1] : W;
+            n = cnt[sg];
+            e = n > 0 ? cx.entry(sg, n, j) : 0;
             load_entry();
         }
         while (j >= next_start) {
@@ -329,7 +341,20 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     }
 }
 
-template __global__ void k_rows<false>(RowArgs);
-template __global__ void k_rows<true>(RowArgs);
+// Row-pass words of shared memory per row for a given (T, L).
+inline int row_words(int T, int L) { return (T * (L + 2)) / 2 + T * (L + 1) + 3 * T; }
+
+// Host-side dispatch over the compile-time segment length.
+template <bool TAKE_NEW>
+inline const void* rows_kernel_ptr(int L) {
+    switch (L) {
+        case 4: return (const void*)k_rows<4, TAKE_NEW>;
+        case 8: return (const void*)k_rows<8, TAKE_NEW>;
+        case 16: return (const void*)k_rows<16, TAKE_NEW>;
+        case 32: return (const void*)k_rows<32, TAKE_NEW>;
+        case 64: return (const void*)k_rows<64, TAKE_NEW>;
+        default: return (const void*)k_rows<128, TAKE_NEW>;
+    }
+}
 
 }  // namespace dfc

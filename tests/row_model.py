@@ -1,0 +1,165 @@
+"""Pure-Python model of the k_rows algorithm (segment stacks + leader-walk merges
++ fill), statement for statement, for CPU testing of the merge logic.
+Test infrastructure only."""
+INF = None
+
+
+def floor_div(a, b):
+    return a // b
+
+
+def build_segment(g, c0, c1, W, take_new):
+    """Stack of (k, start) for columns [c0, c1) over the domain [0, W)."""
+    st = []
+    for m in range(c0, c1):
+        if g[m] is None:
+            continue
+        num = den = None
+        while st:
+            tk, ts = st[-1]
+            num = g[m] - g[tk] + m * m - tk * tk
+            den = 2 * (m - tk)
+            lim = ts * den
+            pop = num <= lim if take_new else num < lim
+            if not pop:
+                break
+            st.pop()
+        start = 0
+        if st:
+            lim = (W - 1) * den
+            if (num > lim) if take_new else (num >= lim):
+                continue
+            q = num // den
+            start = (q + (1 if num != q * den else 0)) if take_new else q + 1
+        st.append((m, start))
+    return st
+
+
+class Row:
+    def __init__(self, g, T, L, take_new):
+        self.g, self.T, self.L, self.W, self.tn = g, T, L, len(g), take_new
+        self.stk = [build_segment(g, s * L, min(s * L + L, self.W), self.W, take_new) for s in range(T)]
+        self.cut = [0] * T
+
+    def owner(self, s0, s1, j):
+        lo, hi = s0, s1 - 1
+        while lo < hi:
+            mid = (lo + hi + 1) >> 1
+            if self.cut[mid] <= j:
+                lo = mid
+            else:
+                hi = mid - 1
+        return lo
+
+    def entry(self, s, j):
+        st = self.stk[s]
+        lo, hi = 0, len(st) - 1
+        while lo < hi:
+            mid = (lo + hi + 1) >> 1
+            if st[mid][1] <= j:
+                lo = mid
+            else:
+                hi = mid - 1
+        return lo
+
+    def make_piece(self, s, e, s1):
+        st = self.stk[s]
+        k, start = st[e]
+        seg_hi = self.cut[s + 1] if s + 1 < s1 else self.W
+        lo = max(start, self.cut[s])
+        hi = min(st[e + 1][1] if e + 1 < len(st) else self.W, seg_hi)
+        return dict(s=s, e=e, k=k, g=self.g[k], lo=lo, hi=hi)
+
+    def piece_at(self, s0, s1, j):
+        s = self.owner(s0, s1, j)
+        if not self.stk[s]:
+            return None
+        return self.make_piece(s, self.entry(s, j), s1)
+
+    def takeover(self, s0, sm, s1, max_steps=100000):
+        W, L, tn = self.W, self.L, self.tn
+        p0 = min(sm * L, W - 1)
+        b = self.piece_at(sm, s1, p0)
+        if b is None:
+            return W
+        a = self.piece_at(s0, sm, p0)
+        if a is None:
+            return 0
+        moved = 0  # -1 after a step left (pred true at the old lo), +1 after a step right
+        for _ in range(max_steps):
+            lo, hi = max(a["lo"], b["lo"]), min(a["hi"], b["hi"])
+            assert lo < hi, (a, b)
+            num = b["g"] - a["g"] + b["k"] ** 2 - a["k"] ** 2
+            den = 2 * (b["k"] - a["k"])
+            dlo, dhi = den * lo, den * (hi - 1)
+            if (num <= dlo) if tn else (num < dlo):
+                if lo == 0 or moved > 0:  # pred true at lo, false at lo-1
+                    return lo
+                moved = -1
+                j = lo - 1
+                if a["lo"] == lo:
+                    a = (self.make_piece(a["s"], a["e"] - 1, sm) if a["lo"] > self.cut[a["s"]]
+                         else self.piece_at(s0, sm, j))
+                if b["lo"] == lo:
+                    b = (self.make_piece(b["s"], b["e"] - 1, s1) if b["lo"] > self.cut[b["s"]]
+                         else self.piece_at(sm, s1, j))
+            elif (num > dhi) if tn else (num >= dhi):
+                if hi == W or moved < 0:  # pred false at hi-1, true at hi
+                    return hi
+                moved = 1
+                j = hi
+                if a["hi"] == hi:
+                    seg_hi = self.cut[a["s"] + 1] if a["s"] + 1 < sm else W
+                    a = self.make_piece(a["s"], a["e"] + 1, sm) if hi < seg_hi else self.piece_at(s0, sm, j)
+                if b["hi"] == hi:
+                    seg_hi = self.cut[b["s"] + 1] if b["s"] + 1 < s1 else W
+                    b = self.make_piece(b["s"], b["e"] + 1, s1) if hi < seg_hi else self.piece_at(sm, s1, j)
+            else:
+                q = num // den
+                return (q + (1 if num != q * den else 0)) if tn else q + 1
+        raise RuntimeError("walk did not terminate")
+
+    def merge_all(self):
+        T = self.T
+        G = 2
+        while G <= T:
+            half = G // 2
+            xs = {gb: self.takeover(gb, gb + half, gb + G) for gb in range(0, T, G)}
+            for s in range(T):
+                gb = s & ~(G - 1)
+                x = xs[gb]
+                self.cut[s] = max(self.cut[s], x) if (s - gb) >= half else min(self.cut[s], x)
+            G *= 2
+
+    def fill(self):
+        """(D, owner column) per j, None for an empty row."""
+        out = []
+        for j in range(self.W):
+            s = self.owner(0, self.T, j)
+            if not self.stk[s]:
+                out.append((None, None))
+                continue
+            k = self.stk[s][self.entry(s, j)][0]
+            out.append((self.g[k] + (j - k) ** 2, k))
+        return out
+
+
+def row_envelope(g, T, L, take_new=False):
+    r = Row(g, T, L, take_new)
+    r.merge_all()
+    return r.fill()
+
+
+def brute(g, take_new=False):
+    W = len(g)
+    out = []
+    for j in range(W):
+        best = None
+        for k in range(W):
+            if g[k] is None:
+                continue
+            d = g[k] + (j - k) ** 2
+            if best is None or d < best[0] or (take_new and d == best[0]):
+                best = (d, k)
+        out.append(best if best else (None, None))
+    return out
