@@ -252,16 +252,19 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, i, W};
 
     // ---- 2. merge adjacent segment groups, one leader per merge ----
+    // Levels with G <= 32 stay inside one warp (__syncwarp); a merge spanning
+    // warps first needs every warp's cuts of the previous level (__syncthreads).
     for (int G = 2; G <= T; G <<= 1) {
         const int gb = s & ~(G - 1);
         const int half = G >> 1;
+        if (G > 32) __syncthreads();
         if (active && s == gb) xs[gb] = cx.takeover(gb, gb + half, gb + G);
         if (G <= 32) __syncwarp(); else __syncthreads();
         if (active) {
             const int x = xs[gb];
             cut[s] = (s - gb) >= half ? max(cut[s], x) : min(cut[s], x);
         }
-        if (G <= 32) __syncwarp(); else __syncthreads();
+        __syncwarp();
     }
     __syncthreads();
 
