@@ -117,6 +117,13 @@ int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t
                        const int32_t* d_label, uint32_t* d_ordinal, dfc_stream_t stream);
 
 /*
+ * Float distances of a squared-distance map: (float)sqrt((double)D) for each
+ * of n int32 values (DFC_INF_I32 -> +inf) -- the row pass's own epilogue
+ * (grid.cpp:146 semantics), e.g. for a map from dfc_vertical_u8.
+ */
+int dfc_sqrt_i32(const int32_t* d_sqdist, float* d_dist, int64_t n, dfc_stream_t stream);
+
+/*
  * Measurement hook (bench.py): cudaEvent_t handles recorded on the call's
  * stream by the next dfc_edt_u8* calls on this thread -- ev_col_begin before
  * the column pass, ev_row_begin between column and row pass, ev_row_end

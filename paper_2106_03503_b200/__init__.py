@@ -48,11 +48,12 @@ _lib.dfc_version.restype = C.c_char_p
 _lib.dfc_last_launch_count.restype = C.c_int
 _lib.dfc_last_cuda_error.restype = C.c_int
 _lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
+_lib.dfc_sqrt_i32.argtypes = [_vp, _vp, _i64, _vp]
 
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
-    "dfc_version", "dfc_set_profile_events",
+    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32",
 )
 
 
@@ -192,6 +193,14 @@ def raster(img: torch.Tensor, cityblock: bool = True, chessboard: bool = True,
     _check(_lib.dfc_raster_u8(_ptr(img), h, w, pitch, _ptr(o.get("cityblock")),
                               _ptr(o.get("chessboard")), _ptr(o.get("chamfer34")), _stream(stream)))
     return o
+
+
+def sqrt_i32(sq: torch.Tensor, stream=None) -> torch.Tensor:
+    """float32 (float)sqrt((double)D) of an int32 squared map (INF_I32 -> +inf)."""
+    sq = sq.contiguous()
+    out = torch.empty(sq.shape, dtype=torch.float32, device=sq.device)
+    _check(_lib.dfc_sqrt_i32(_ptr(sq), _ptr(out), sq.numel(), _stream(stream)))
+    return out
 
 
 def label_ordinals(img: torch.Tensor, label: torch.Tensor, stream=None) -> torch.Tensor:

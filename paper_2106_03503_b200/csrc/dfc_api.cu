@@ -3,6 +3,7 @@
 // Plumbing only: argument validation, scratch from the stream-ordered memory
 // pool, launch geometry, status codes.  Never throws, never synchronises.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "dfc_kernels.cuh"
@@ -68,16 +69,29 @@ struct RowGeom {
 };
 
 // T threads per row (power of two, 32..1024), L = 2^k columns per thread.
+// Shared memory holds a whole row (~6 B/column), so the rows resident per SM
+// are fixed by W; long segments (L up to 128) keep the merge tree shallow.
+// DFC_ROW_L (env) overrides the target segment length for tuning.
 RowGeom row_geom(int W) {
+    static int target = [] {
+        const char* e = getenv("DFC_ROW_L");
+        const int v = e ? atoi(e) : 0;
+        return (v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128) ? v : 128;
+    }();
     RowGeom g;
     g.T = 32;
-    while (g.T < 1024 && (int64_t)g.T * 32 < W) g.T <<= 1;
+    while (g.T < 1024 && (int64_t)g.T * target < W) g.T <<= 1;
     const int per = (W + g.T - 1) / g.T;
     g.L = 4;
     while (g.L < per) g.L <<= 1;
     g.R = g.T >= 256 ? 1 : 256 / g.T;
     g.row_words = dfc::row_words(g.T, g.L);
     g.smem_bytes = g.R * g.row_words * 4;
+    // keep the CTA within the 227 KB opt-in limit: fewer rows per CTA
+    while (g.R > 1 && g.smem_bytes > 227 * 1024) {
+        g.R >>= 1;
+        g.smem_bytes = g.R * g.row_words * 4;
+    }
     return g;
 }
 
@@ -354,6 +368,17 @@ int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t
         d_label, n, (int)cols, nw, masks, wpre, rowbase, d_ordinal);
     g_launches += 3;
     e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_sqrt_i32(const int32_t* d_sqdist, float* d_dist, int64_t n, dfc_stream_t stream) {
+    if (!d_sqdist || !d_dist || n < 0) return DFC_ERR_ARG;
+    g_launches = 0;
+    if (n == 0) return DFC_OK;
+    k_sqrt_i32<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, (cudaStream_t)stream>>>(
+        d_sqdist, d_dist, n);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 

@@ -129,6 +129,13 @@ __global__ void __launch_bounds__(1024) k_raster(RasterArgs a) {
     }
 }
 
+// ---- float distances from a squared map (the row pass's epilogue, standalone) ----
+__global__ void k_sqrt_i32(const int32_t* __restrict__ d, float* __restrict__ out, int64_t n) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x)
+        out[p] = dist_f32((uint32_t)d[p]);
+}
+
 // ---- label ordinals (LabelMap ids, grid.cpp:29-36) ----
 // K4a: one warp per row: per-32-column word object masks and in-row prefix counts.
 __global__ void k_ord_rows(const uint8_t* __restrict__ img, int64_t pitch, int H, int W, int nw,

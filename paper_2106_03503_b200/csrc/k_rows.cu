@@ -114,8 +114,61 @@ struct RowCtx {
         make_piece(p, s, entry(s, n, j), n, s1);
     }
 
+    // First column at which segment s (its FULL stack, s >= sm) beats group
+    // A = [s0, sm), W if never.  B = [sm, s1) beats A at j iff some s in B
+    // does, so the group takeover is the minimum of this over s in B: every
+    // lane of B walks its own stack in parallel (SIMD), no leader serialises.
+    __device__ int cross_seg(int s0, int sm, int s) const {
+        const int n = cnt[s];
+        if (n == 0) return W;
+        const uint32_t* st = stk + s * RowLayout<L>::stk_stride;
+        const int p0 = min(s * L, W - 1);
+        int be = entry(s, n, p0);
+        auto bset = [&](Piece& b, int e) {
+            const uint32_t ent = st[e];
+            b.e = e;
+            b.k = (int)(ent & 0xffffu);
+            b.g = g_of(b.k);
+            b.lo = (int)(ent >> 16);
+            b.hi = e + 1 < n ? (int)(st[e + 1] >> 16) : W;
+        };
+        Piece a, b;
+        bset(b, be);
+        piece_at(a, s0, sm, p0);
+        if (a.k < 0) return 0;   // A empty: s owns everything
+        int moved = 0;
+        for (int guard = 0; guard < 2 * W + 2; ++guard) {
+            const int lo = max(a.lo, b.lo), hi = min(a.hi, b.hi);
+            const int64_t num = (int64_t)b.g - (int64_t)a.g + (int64_t)b.k * b.k - (int64_t)a.k * a.k;
+            const int64_t den = 2 * (int64_t)(b.k - a.k);
+            const int64_t dlo = den * lo, dhi = den * (hi - 1);
+            if (TAKE_NEW ? num <= dlo : num < dlo) {          // s beats A at lo: go left
+                if (lo == 0 || moved > 0) return lo;
+                moved = -1;
+                if (a.lo == lo) {
+                    if (a.lo > cut[a.s]) make_piece(a, a.s, a.e - 1, cnt[a.s], sm);
+                    else piece_at(a, s0, sm, lo - 1);
+                }
+                if (b.lo == lo) bset(b, b.e - 1);
+            } else if (TAKE_NEW ? num > dhi : num >= dhi) {   // A holds at hi-1: go right
+                if (hi == W || moved < 0) return hi;
+                moved = 1;
+                if (a.hi == hi) {
+                    if (hi < (a.s + 1 < sm ? cut[a.s + 1] : W)) make_piece(a, a.s, a.e + 1, cnt[a.s], sm);
+                    else piece_at(a, s0, sm, hi);
+                }
+                if (b.hi == hi) bset(b, b.e + 1);
+            } else {
+                const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
+                return TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
+            }
+        }
+        return W;
+    }
+
     // First column x at which group B = [sm, s1) beats group A = [s0, sm)
     // (W if never).  The predicate is monotone in j; see the file comment.
+    // (Single-leader variant, kept for reference/testing.)
     __device__ int takeover(int s0, int sm, int s1) const {
         const int p0 = min(sm * L, W - 1);
         Piece a, b;
@@ -205,43 +258,60 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
         int tk = 0, ts = 0;   // top entry: column, start
         int tg = 0;           // top entry: vertical value
         if (active) {
-            for (int m = c0; m < c1; ++m) {
-                const uint32_t r = nrs[LY::nidx(m)];
-                if (r == kNoRow) continue;  // sentinel vertex never enters (:212)
+            // One event per iteration -- pop the top, or consume column m
+            // (push or skip) -- instead of a nested pop loop: lanes of a warp
+            // reconverge every iteration.
+            int m = c0;
+            int gm = -1;  // vertical value of column m, -1 = no feature (:212)
+            auto load_m = [&]() {
+                const uint32_t r = m < c1 ? nrs[LY::nidx(m)] : kNoRow;
                 const int am = (int)(i > r ? i - r : r - i);
-                const int gm = am * am;
-                const int mm = m * m;
+                gm = r == kNoRow ? -1 : am * am;
+            };
+            load_m();
+            while (m < c1) {
+                bool consume = true;
                 int num = 0;
                 uint32_t den = 1;
-                while (n > 0) {
+                if (gm >= 0 && n > 0) {
                     // num = v_m - v_k - k^2 + m^2 fits int32 (|.| < 2^31); ts*den < 2^32
-                    num = gm - tg + (mm - tk * tk);
+                    num = gm - tg + (m * m - tk * tk);
                     den = 2u * (uint32_t)(m - tk);
                     const uint32_t lim = (uint32_t)ts * den;  // start <= js[idx]  (:214)
-                    const bool pop = num < 0 || (TAKE_NEW ? (uint32_t)num <= lim : (uint32_t)num < lim);
-                    if (!pop) break;
-                    if (--n > 0) {
-                        const uint32_t e = st[n - 1];
-                        tk = (int)(e & 0xffffu);
-                        ts = (int)(e >> 16);
-                        const uint32_t rk = nrs[LY::nidx(tk)];
-                        const int ak = (int)(i > rk ? i - rk : rk - i);
-                        tg = ak * ak;
+                    if (num < 0 || (TAKE_NEW ? (uint32_t)num <= lim : (uint32_t)num < lim)) {
+                        consume = false;  // pop
+                        if (--n > 0) {
+                            const uint32_t e = st[n - 1];
+                            tk = (int)(e & 0xffffu);
+                            ts = (int)(e >> 16);
+                            const uint32_t rk = nrs[LY::nidx(tk)];
+                            const int ak = (int)(i > rk ? i - rk : rk - i);
+                            tg = ak * ak;
+                        }
                     }
                 }
-                int start = 0;
-                if (n > 0) {
-                    // push iff start <= cols-1 (:218); here 0 <= num
-                    const uint32_t lim = (uint32_t)(W - 1) * den;
-                    if (TAKE_NEW ? (uint32_t)num > lim : (uint32_t)num >= lim) continue;
-                    const uint32_t q = small_udiv((uint32_t)num, den);
-                    // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
-                    start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * den)) : (int)q + 1;
+                if (consume) {
+                    if (gm >= 0) {
+                        int start = 0;
+                        bool push = true;
+                        if (n > 0) {
+                            // push iff start <= cols-1 (:218); here 0 <= num
+                            const uint32_t lim = (uint32_t)(W - 1) * den;
+                            push = TAKE_NEW ? (uint32_t)num <= lim : (uint32_t)num < lim;
+                            const uint32_t q = small_udiv((uint32_t)num, den);
+                            // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
+                            start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * den)) : (int)q + 1;
+                        }
+                        if (push) {
+                            st[n++] = (uint32_t)m | ((uint32_t)start << 16);
+                            tk = m;
+                            ts = start;
+                            tg = gm;
+                        }
+                    }
+                    ++m;
+                    load_m();
                 }
-                st[n++] = (uint32_t)m | ((uint32_t)start << 16);
-                tk = m;
-                ts = start;
-                tg = gm;
             }
         }
         cnt[s] = n;
@@ -252,18 +322,23 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, i, W};
 
     // ---- 2. merge adjacent segment groups, one leader per merge ----
-    // Levels with G <= 32 stay inside one warp (__syncwarp); a merge spanning
-    // warps first needs every warp's cuts of the previous level (__syncthreads).
+    // ---- 2. merge adjacent segment groups (lane-parallel, see cross_seg) ----
+    // Levels with G <= 32 stay inside one warp (shuffles + __syncwarp); a
+    // merge spanning warps first needs every warp's cuts (__syncthreads).
     for (int G = 2; G <= T; G <<= 1) {
         const int gb = s & ~(G - 1);
         const int half = G >> 1;
         if (G > 32) __syncthreads();
-        if (active && s == gb) xs[gb] = cx.takeover(gb, gb + half, gb + G);
-        if (G <= 32) __syncwarp(); else __syncthreads();
-        if (active) {
-            const int x = xs[gb];
-            cut[s] = (s - gb) >= half ? max(cut[s], x) : min(cut[s], x);
+        int x = (active && s - gb >= half) ? cx.cross_seg(gb, gb + half, s) : W;
+        const int gw = G < 32 ? G : 32;
+        for (int o = 1; o < gw; o <<= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+        if (G > 32) {
+            if ((s & 31) == 0) xs[s >> 5] = x;
+            __syncthreads();
+            x = W;
+            for (int w = gb >> 5; w < (gb + G) >> 5; ++w) x = min(x, xs[w]);
         }
+        if (active) cut[s] = (s - gb) >= half ? max(cut[s], x) : min(cut[s], x);
         __syncwarp();
     }
     __syncthreads();

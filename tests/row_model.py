@@ -119,12 +119,61 @@ class Row:
                 return (q + (1 if num != q * den else 0)) if tn else q + 1
         raise RuntimeError("walk did not terminate")
 
-    def merge_all(self):
+    def cross_seg(self, s0, sm, s, max_steps=100000):
+        """First column where segment s (full-domain stack, s >= sm) beats group
+        A = [s0, sm) -- the lane-parallel merge: x_AB = min over s in B."""
+        W, L, tn = self.W, self.L, self.tn
+        st = self.stk[s]
+        if not st:
+            return W
+        p0 = min(s * L, W - 1)
+
+        def bpiece(e):
+            k, start = st[e]
+            return dict(e=e, k=k, g=self.g[k], lo=start, hi=st[e + 1][1] if e + 1 < len(st) else W)
+
+        b = bpiece(self.entry(s, p0))
+        a = self.piece_at(s0, sm, p0)
+        if a is None:
+            return 0
+        moved = 0
+        for _ in range(max_steps):
+            lo, hi = max(a["lo"], b["lo"]), min(a["hi"], b["hi"])
+            num = b["g"] - a["g"] + b["k"] ** 2 - a["k"] ** 2
+            den = 2 * (b["k"] - a["k"])
+            if (num <= den * lo) if tn else (num < den * lo):
+                if lo == 0 or moved > 0:
+                    return lo
+                moved = -1
+                if a["lo"] == lo:
+                    a = (self.make_piece(a["s"], a["e"] - 1, sm) if a["lo"] > self.cut[a["s"]]
+                         else self.piece_at(s0, sm, lo - 1))
+                if b["lo"] == lo:
+                    b = bpiece(b["e"] - 1)
+            elif (num > den * (hi - 1)) if tn else (num >= den * (hi - 1)):
+                if hi == W or moved < 0:
+                    return hi
+                moved = 1
+                if a["hi"] == hi:
+                    seg_hi = self.cut[a["s"] + 1] if a["s"] + 1 < sm else W
+                    a = self.make_piece(a["s"], a["e"] + 1, sm) if hi < seg_hi else self.piece_at(s0, sm, hi)
+                if b["hi"] == hi:
+                    b = bpiece(b["e"] + 1)
+            else:
+                q = num // den
+                return (q + (1 if num != q * den else 0)) if tn else q + 1
+        raise RuntimeError("walk did not terminate")
+
+    def merge_all(self, lane_parallel=True):
         T = self.T
         G = 2
         while G <= T:
             half = G // 2
-            xs = {gb: self.takeover(gb, gb + half, gb + G) for gb in range(0, T, G)}
+            if lane_parallel:
+                xs = {gb: min(self.cross_seg(gb, gb + half, t) for t in range(gb + half, gb + G))
+                      for gb in range(0, T, G)}
+            else:
+                xs = {gb: self.takeover(gb, gb + half, gb + G) for gb in range(0, T, G)}
             for s in range(T):
                 gb = s & ~(G - 1)
                 x = xs[gb]
@@ -144,9 +193,9 @@ class Row:
         return out
 
 
-def row_envelope(g, T, L, take_new=False):
+def row_envelope(g, T, L, take_new=False, lane_parallel=True):
     r = Row(g, T, L, take_new)
-    r.merge_all()
+    r.merge_all(lane_parallel)
     return r.fill()
 
 

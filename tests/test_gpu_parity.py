@@ -194,3 +194,17 @@ def test_shape_errors(dfc):
         dfc.edt(torch.zeros((70000, 1), dtype=torch.uint8, device="cuda"))  # more rows than supported
     with pytest.raises(dfc.DfcError):
         dfc.edt(torch.zeros((2, 40000), dtype=torch.uint8, device="cuda"))  # row wider than supported
+
+
+def test_sqrt_epilogue_exact(dfc):
+    """dist_f32 == (float)sqrt((double)D) over the whole int32 range, incl. D >= 2^24."""
+    rng = np.random.default_rng(3)
+    vals = np.concatenate([np.arange(0, 1 << 16), rng.integers(0, 2**31 - 1, 2_000_000),
+                           (np.arange(1, 46341, dtype=np.int64) ** 2), (np.arange(1, 46341, dtype=np.int64) ** 2) - 1,
+                           (np.arange(1, 46340, dtype=np.int64) ** 2) + np.arange(1, 46340),
+                           np.array([2**24 - 1, 2**24, 2**24 + 1, 2147352578, 0x7FFFFFFE])]).astype(np.int32)
+    got = dfc.sqrt_i32(torch.from_numpy(vals).cuda()).cpu().numpy()
+    want = np.sqrt(vals.astype(np.float64)).astype(np.float32)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    inf = dfc.sqrt_i32(torch.tensor([0x7FFFFFFF], dtype=torch.int32, device="cuda")).cpu().numpy()
+    assert np.isinf(inf[0])

@@ -21,7 +21,9 @@ def test_row_model_matches_bruteforce(seed):
         H = rnd.randint(1, 300)
         g = [rnd.randint(0, H) ** 2 if rnd.random() < dens else None for _ in range(W)]
         for take_new in (False, True):
-            assert row_envelope(g, T, L, take_new) == brute(g, take_new), (W, T, L, take_new)
+            want = brute(g, take_new)
+            assert row_envelope(g, T, L, take_new, True) == want, (W, T, L, take_new)
+            assert row_envelope(g, T, L, take_new, False) == want, (W, T, L, take_new)
 
 
 def test_row_model_ties():
