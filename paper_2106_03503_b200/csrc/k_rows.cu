@@ -50,13 +50,6 @@ struct RowLayout {
     static constexpr int stk_stride = L + 1;  // odd word stride: conflict-free
 };
 
-struct Piece {
-    int s, e;      // segment, stack entry
-    int k;         // parabola column (-1: empty group)
-    uint32_t g;    // its vertical value
-    int lo, hi;    // columns it owns inside its group: [lo, hi)
-};
-
 template <int L, bool TAKE_NEW>
 struct RowCtx {
     const uint16_t* nrs;
@@ -93,130 +86,20 @@ struct RowCtx {
         }
         return lo;
     }
-    __device__ __forceinline__ void make_piece(Piece& p, int s, int e, int n, int s1) const {
-        const uint32_t ent = stk[s * RowLayout<L>::stk_stride + e];
-        p.s = s;
-        p.e = e;
-        p.k = (int)(ent & 0xffffu);
-        p.g = g_of(p.k);
-        const int seg_hi = s + 1 < s1 ? cut[s + 1] : W;
-        p.lo = max((int)(ent >> 16), cut[s]);
-        p.hi = min(e + 1 < n ? start(s, e + 1) : W, seg_hi);
-    }
-    // the piece of group [s0, s1) owning column j; k = -1 if the group is empty
-    __device__ __forceinline__ void piece_at(Piece& p, int s0, int s1, int j) const {
+    // Envelope of group [s0, s1) at column j (kInfU if the group is empty).
+    __device__ __forceinline__ uint32_t env(int s0, int s1, int j) const {
         const int s = owner(s0, s1, j);
         const int n = cnt[s];
-        if (n == 0) {
-            p.k = -1;
-            return;
-        }
-        make_piece(p, s, entry(s, n, j), n, s1);
+        if (n == 0) return kInfU;
+        const uint32_t ent = stk[s * RowLayout<L>::stk_stride + entry(s, n, j)];
+        const int k = (int)(ent & 0xffffu);
+        return g_of(k) + (uint32_t)((j - k) * (j - k));
     }
-
-    // First column at which segment s (its FULL stack, s >= sm) beats group
-    // A = [s0, sm), W if never.  B = [sm, s1) beats A at j iff some s in B
-    // does, so the group takeover is the minimum of this over s in B: every
-    // lane of B walks its own stack in parallel (SIMD), no leader serialises.
-    __device__ int cross_seg(int s0, int sm, int s) const {
-        const int n = cnt[s];
-        if (n == 0) return W;
-        const uint32_t* st = stk + s * RowLayout<L>::stk_stride;
-        const int p0 = min(s * L, W - 1);
-        int be = entry(s, n, p0);
-        auto bset = [&](Piece& b, int e) {
-            const uint32_t ent = st[e];
-            b.e = e;
-            b.k = (int)(ent & 0xffffu);
-            b.g = g_of(b.k);
-            b.lo = (int)(ent >> 16);
-            b.hi = e + 1 < n ? (int)(st[e + 1] >> 16) : W;
-        };
-        Piece a, b;
-        bset(b, be);
-        piece_at(a, s0, sm, p0);
-        if (a.k < 0) return 0;   // A empty: s owns everything
-        int moved = 0;
-        for (int guard = 0; guard < 2 * W + 2; ++guard) {
-            const int lo = max(a.lo, b.lo), hi = min(a.hi, b.hi);
-            const int64_t num = (int64_t)b.g - (int64_t)a.g + (int64_t)b.k * b.k - (int64_t)a.k * a.k;
-            const int64_t den = 2 * (int64_t)(b.k - a.k);
-            const int64_t dlo = den * lo, dhi = den * (hi - 1);
-            if (TAKE_NEW ? num <= dlo : num < dlo) {          // s beats A at lo: go left
-                if (lo == 0 || moved > 0) return lo;
-                moved = -1;
-                if (a.lo == lo) {
-                    if (a.lo > cut[a.s]) make_piece(a, a.s, a.e - 1, cnt[a.s], sm);
-                    else piece_at(a, s0, sm, lo - 1);
-                }
-                if (b.lo == lo) bset(b, b.e - 1);
-            } else if (TAKE_NEW ? num > dhi : num >= dhi) {   // A holds at hi-1: go right
-                if (hi == W || moved < 0) return hi;
-                moved = 1;
-                if (a.hi == hi) {
-                    if (hi < (a.s + 1 < sm ? cut[a.s + 1] : W)) make_piece(a, a.s, a.e + 1, cnt[a.s], sm);
-                    else piece_at(a, s0, sm, hi);
-                }
-                if (b.hi == hi) bset(b, b.e + 1);
-            } else {
-                const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
-                return TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
-            }
-        }
-        return W;
-    }
-
-    // First column x at which group B = [sm, s1) beats group A = [s0, sm)
-    // (W if never).  The predicate is monotone in j; see the file comment.
-    // (Single-leader variant, kept for reference/testing.)
-    __device__ int takeover(int s0, int sm, int s1) const {
-        const int p0 = min(sm * L, W - 1);
-        Piece a, b;
-        piece_at(b, sm, s1, p0);
-        if (b.k < 0) return W;   // B has no finite parabola: never beats
-        piece_at(a, s0, sm, p0);
-        if (a.k < 0) return 0;   // A empty: B owns everything
-        int moved = 0;           // -1 after a step left, +1 after a step right
-        // each step discards a piece, so 2*W+2 steps bound the walk (defensive)
-        for (int guard = 0; guard < 2 * W + 2; ++guard) {
-            const int lo = max(a.lo, b.lo), hi = min(a.hi, b.hi);
-            // b beats a from xab on, with
-            //   keep_old: xab = floor(num/den) + 1,  take_new: xab = ceil(num/den)
-            const int64_t num = (int64_t)b.g - (int64_t)a.g + (int64_t)b.k * b.k - (int64_t)a.k * a.k;
-            const int64_t den = 2 * (int64_t)(b.k - a.k);
-            const int64_t dlo = den * lo, dhi = den * (hi - 1);
-            if (TAKE_NEW ? num <= dlo : num < dlo) {          // xab <= lo: move left
-                if (lo == 0 || moved > 0) return lo;  // true at lo, false at lo-1
-                moved = -1;
-                const int j = lo - 1;
-                // the previous piece is the previous stack entry unless the segment starts at lo
-                if (a.lo == lo) {
-                    if (a.lo > cut[a.s]) make_piece(a, a.s, a.e - 1, cnt[a.s], sm);
-                    else piece_at(a, s0, sm, j);
-                }
-                if (b.lo == lo) {
-                    if (b.lo > cut[b.s]) make_piece(b, b.s, b.e - 1, cnt[b.s], s1);
-                    else piece_at(b, sm, s1, j);
-                }
-            } else if (TAKE_NEW ? num > dhi : num >= dhi) {   // xab >= hi: move right
-                if (hi == W || moved < 0) return hi;  // false at hi-1, true at hi
-                moved = 1;
-                const int j = hi;
-                // the next piece is the next stack entry unless the segment ends at hi
-                if (a.hi == hi) {
-                    if (hi < (a.s + 1 < sm ? cut[a.s + 1] : W)) make_piece(a, a.s, a.e + 1, cnt[a.s], sm);
-                    else piece_at(a, s0, sm, j);
-                }
-                if (b.hi == hi) {
-                    if (hi < (b.s + 1 < s1 ? cut[b.s + 1] : W)) make_piece(b, b.s, b.e + 1, cnt[b.s], s1);
-                    else piece_at(b, sm, s1, j);
-                }
-            } else {                                           // lo < xab < hi
-                const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
-                return TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
-            }
-        }
-        return W;
+    // Does group B = [sm, s1) beat group A = [s0, sm) at column j?  Monotone
+    // in j (false ... false true ... true), E_A - E_B strictly increasing.
+    __device__ __forceinline__ bool beats(int s0, int sm, int s1, int j) const {
+        const uint32_t eb = env(sm, s1, j), ea = env(s0, sm, j);
+        return TAKE_NEW ? (eb <= ea && eb != kInfU) : (eb < ea);
     }
 };
 
@@ -238,7 +121,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     uint32_t* stk = base + (T * (L + 2)) / 2;                     // [T*(L+1)]
     int* cut = reinterpret_cast<int*>(stk + T * LY::stk_stride);  // [T]
     int* cnt = cut + T;                                           // [T]
-    int* xs = cnt + T;                                            // [T] takeover per merge
+    int* xs = cnt + T;                                            // [T/32] takeover per merge
 
     // ---- 0. stage the row's nearest-row values (coalesced 4-byte loads) ----
     if (active) {
@@ -322,23 +205,52 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, i, W};
 
     // ---- 2. merge adjacent segment groups, one leader per merge ----
-    // ---- 2. merge adjacent segment groups (lane-parallel, see cross_seg) ----
-    // Levels with G <= 32 stay inside one warp (shuffles + __syncwarp); a
-    // merge spanning warps first needs every warp's cuts (__syncthreads).
+    // ---- 2. merge adjacent segment groups: P-ary probe search ----
+    // The P = min(G, 32) lanes of a merge evaluate "B beats A" at P columns
+    // per round.  Round 0 probes c-1 and c (c = B's first column, where dense
+    // rows take over) and spreads the rest over the row; later rounds split
+    // the remaining bracket [lo, hi] uniformly.  The outcome is reduced
+    // order-independently: hi = min column where B beats, lo = 1 + max column
+    // where it does not.  G <= 32: groups live inside a warp and search in
+    // lockstep; G > 32: the group's first warp searches, the others wait.
     for (int G = 2; G <= T; G <<= 1) {
         const int gb = s & ~(G - 1);
         const int half = G >> 1;
-        if (G > 32) __syncthreads();
-        int x = (active && s - gb >= half) ? cx.cross_seg(gb, gb + half, s) : W;
-        const int gw = G < 32 ? G : 32;
-        for (int o = 1; o < gw; o <<= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
-        if (G > 32) {
-            if ((s & 31) == 0) xs[s >> 5] = x;
-            __syncthreads();
-            x = W;
-            for (int w = gb >> 5; w < (gb + G) >> 5; ++w) x = min(x, xs[w]);
+        const int P = G < 32 ? G : 32;
+        const int q = s - gb;
+        if (G > 32) __syncthreads();  // every warp's cuts of the previous level
+        if (q < 32) {                 // warp-uniform: whole warps probe or not
+            const int c = min((gb + half) * L, W - 1);
+            const float rP1 = 1.0f / (float)(P + 1), rPm1 = P > 2 ? 1.0f / (float)(P - 1) : 0.f;
+            int lo = 0, hi = W;
+            bool first = true;
+            while (__any_sync(0xffffffffu, active && hi > lo)) {
+                const int n = hi - lo;
+                int p;
+                if (first) p = q < 2 ? c - 1 + q : lo + __float2int_rz((float)((q - 1) * n) * rPm1);
+                else p = lo + __float2int_rz((float)((q + 1) * n) * rP1);
+                p = min(max(p, lo), hi - 1);
+                const bool live = active && hi > lo;
+                const bool bt = live && cx.beats(gb, gb + half, gb + G, p);
+                int t = live && bt ? p : W;             // first column where B beats
+                int f = live && !bt ? p : -1;           // last column where it does not
+                for (int o = 1; o < P; o <<= 1) {
+                    t = min(t, __shfl_xor_sync(0xffffffffu, t, o));
+                    f = max(f, __shfl_xor_sync(0xffffffffu, f, o));
+                }
+                if (live) {
+                    hi = min(hi, t);
+                    lo = max(lo, f + 1);
+                }
+                first = false;
+            }
+            if (G > 32 && q == 0) xs[gb >> 5] = lo;
+            if (G <= 32 && active) cut[s] = q >= half ? max(cut[s], lo) : min(cut[s], lo);
         }
-        if (active) cut[s] = (s - gb) >= half ? max(cut[s], x) : min(cut[s], x);
+        if (G > 32) {
+            __syncthreads();
+            if (active) cut[s] = q >= half ? max(cut[s], xs[gb >> 5]) : min(cut[s], xs[gb >> 5]);
+        }
         __syncwarp();
     }
     __syncthreads();

@@ -40,6 +40,7 @@ class Row:
         self.g, self.T, self.L, self.W, self.tn = g, T, L, len(g), take_new
         self.stk = [build_segment(g, s * L, min(s * L + L, self.W), self.W, take_new) for s in range(T)]
         self.cut = [0] * T
+        self.stats = []
 
     def owner(self, s0, s1, j):
         lo, hi = s0, s1 - 1
@@ -164,12 +165,63 @@ class Row:
                 return (q + (1 if num != q * den else 0)) if tn else q + 1
         raise RuntimeError("walk did not terminate")
 
+    def E_group(self, s0, s1, j):
+        p = self.piece_at(s0, s1, j)
+        return None if p is None else p["g"] + (j - p["k"]) ** 2
+
+    def beats(self, s0, sm, s1, j):
+        eb, ea = self.E_group(sm, s1, j), self.E_group(s0, sm, j)
+        if eb is None:
+            return False
+        if ea is None:
+            return True
+        return eb <= ea if self.tn else eb < ea
+
+    def probe_merge(self, s0, sm, s1, P, stats=None):
+        """P-ary probe search for the takeover column (mirrors k_rows.cu).
+        Round 0 probes c-1 and c (c = B's first column: dense rows end here)
+        and spreads the other P-2 probes uniformly; later rounds split the
+        remaining bracket uniformly."""
+        W, L = self.W, self.L
+        lo, hi = 0, W            # x in [lo, hi]; pred(hi) true or hi == W
+        c = min(sm * L, W - 1)
+        rounds = 0
+        while hi > lo:
+            n = hi - lo
+            if rounds == 0:
+                ps = []
+                for q in range(P):
+                    if q < 2:
+                        p = c - 1 + q
+                    else:
+                        p = lo + ((q - 1) * n) // (P - 1)
+                    ps.append(p)
+                ps.sort()
+            else:
+                ps = [lo + ((q + 1) * n) // (P + 1) for q in range(P)]
+            ps = [min(max(p, lo), hi - 1) for p in ps]
+            rounds += 1
+            bits = [self.beats(s0, sm, s1, p) for p in ps]
+            f = next((q for q in range(P) if bits[q]), None)
+            if f is None:
+                lo = ps[-1] + 1
+            else:
+                hi = ps[f]
+                if f > 0:
+                    lo = ps[f - 1] + 1
+        if stats is not None:
+            stats.append(rounds)
+        return lo
+
     def merge_all(self, lane_parallel=True):
         T = self.T
         G = 2
         while G <= T:
             half = G // 2
-            if lane_parallel:
+            if lane_parallel == "probe":
+                P = min(G, 32)
+                xs = {gb: self.probe_merge(gb, gb + half, gb + G, P, self.stats) for gb in range(0, T, G)}
+            elif lane_parallel:
                 xs = {gb: min(self.cross_seg(gb, gb + half, t) for t in range(gb + half, gb + G))
                       for gb in range(0, T, G)}
             else:

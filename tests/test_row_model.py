@@ -24,6 +24,7 @@ def test_row_model_matches_bruteforce(seed):
             want = brute(g, take_new)
             assert row_envelope(g, T, L, take_new, True) == want, (W, T, L, take_new)
             assert row_envelope(g, T, L, take_new, False) == want, (W, T, L, take_new)
+            assert row_envelope(g, T, L, take_new, "probe") == want, (W, T, L, take_new)
 
 
 def test_row_model_ties():
