@@ -40,6 +40,10 @@
 
 namespace dfc {
 
+// Rows whose segment stacks hold at most this many candidates in total are
+// merged by one lane instead of the merge tree (C3-like sparse rows).
+constexpr int kCompact = 64;
+
 template <int L>
 struct RowLayout {
     static constexpr int kLog = L == 4 ? 2 : L == 8 ? 3 : L == 16 ? 4 : L == 32 ? 5 : L == 64 ? 6 : 7;
@@ -122,6 +126,8 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     int* cut = reinterpret_cast<int*>(stk + T * LY::stk_stride);  // [T]
     int* cnt = cut + T;                                           // [T]
     int* xs = cnt + T;                                            // [T/32] takeover per merge
+    int* nzw = xs + T;                                            // [T/32] warp has candidates
+    uint32_t* cmp = reinterpret_cast<uint32_t*>(nzw + T);         // [kCompact+1] compact envelope
 
     // ---- 0. stage the row's nearest-row values (coalesced 4-byte loads) ----
     if (active) {
@@ -204,7 +210,70 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
 
     RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, i, W};
 
-    // ---- 2. merge adjacent segment groups, one leader per merge ----
+    // ---- 1b. row census: candidates per row, which warps have any ----
+    const int lane = threadIdx.x & 31;
+    const int my_cnt = active ? cnt[s] : 0;
+    const uint32_t nzmask = __ballot_sync(0xffffffffu, my_cnt > 0);
+    int tot = my_cnt;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (T > 32) {
+        if (lane == 0) {
+            xs[s >> 5] = tot;
+            nzw[s >> 5] = nzmask != 0;
+        }
+        __syncthreads();
+        tot = 0;
+        for (int w = 0; w < (T >> 5); ++w) tot += xs[w];
+    }
+
+    // (CTA-uniform choice: rows sharing a CTA must run the same barriers)
+    if (__syncthreads_and(tot <= kCompact)) {
+        // ---- 2'. sparse row: one lane runs the reference stack algorithm
+        // (exact_edt.cpp:208-223) over the surviving candidates of all
+        // segments, in column order; the result becomes a single segment.
+        if (s == 0 && active) {
+            int n = 0, tk = 0, ts = 0, tg = 0;
+            for (int sg = 0; sg < T; ++sg) {
+                const int cn = cnt[sg];
+                for (int e = 0; e < cn; ++e) {
+                    const int m = (int)(stk[sg * LY::stk_stride + e] & 0xffffu);
+                    const int gm = (int)cx.g_of(m);
+                    int start = 0;
+                    bool push = true;
+                    while (n > 0) {
+                        const int num = gm - tg + (m * m - tk * tk);
+                        const uint32_t den = 2u * (uint32_t)(m - tk);
+                        const uint32_t lim = (uint32_t)ts * den;
+                        if (num < 0 || (TAKE_NEW ? (uint32_t)num <= lim : (uint32_t)num < lim)) {
+                            if (--n > 0) {
+                                const uint32_t ent = cmp[n - 1];
+                                tk = (int)(ent & 0xffffu);
+                                ts = (int)(ent >> 16);
+                                tg = (int)cx.g_of(tk);
+                            }
+                            continue;
+                        }
+                        const uint32_t lim2 = (uint32_t)(W - 1) * den;
+                        push = TAKE_NEW ? (uint32_t)num <= lim2 : (uint32_t)num < lim2;
+                        const uint32_t qd = small_udiv((uint32_t)num, den);
+                        start = TAKE_NEW ? (int)(qd + ((uint32_t)num != qd * den)) : (int)qd + 1;
+                        break;
+                    }
+                    if (push) {
+                        cmp[n++] = (uint32_t)m | ((uint32_t)start << 16);
+                        tk = m;
+                        ts = start;
+                        tg = gm;
+                    }
+                }
+            }
+            for (int e = 0; e < n; ++e) stk[e] = cmp[e];  // all segment stacks already consumed
+            cnt[0] = n;
+        }
+        if (T > 32) __syncthreads(); else __syncwarp();
+        if (active && s > 0) cut[s] = W;   // segment 0 owns the whole row
+        __syncthreads();
+    } else {
     // ---- 2. merge adjacent segment groups: P-ary probe search ----
     // The P = min(G, 32) lanes of a merge evaluate "B beats A" at P columns
     // per round.  Round 0 probes c-1 and c (c = B's first column, where dense
@@ -223,6 +292,19 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
             const int c = min((gb + half) * L, W - 1);
             const float rP1 = 1.0f / (float)(P + 1), rPm1 = P > 2 ? 1.0f / (float)(P - 1) : 0.f;
             int lo = 0, hi = W;
+            // a side without any finite parabola decides the merge at once
+            bool hasA, hasB;
+            if (G <= 32) {
+                const uint32_t hm = half == 32 ? 0xffffffffu : ((1u << half) - 1u);
+                hasA = ((nzmask >> (gb & 31)) & hm) != 0;
+                hasB = ((nzmask >> ((gb & 31) + half)) & hm) != 0;
+            } else {
+                hasA = hasB = false;
+                for (int w = gb >> 5; w < (gb + half) >> 5; ++w) hasA |= nzw[w] != 0;
+                for (int w = (gb + half) >> 5; w < (gb + G) >> 5; ++w) hasB |= nzw[w] != 0;
+            }
+            if (!hasB) lo = hi = W;
+            else if (!hasA) lo = hi = 0;
             bool first = true;
             while (__any_sync(0xffffffffu, active && hi > lo)) {
                 const int n = hi - lo;
@@ -254,6 +336,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
         __syncwarp();
     }
     __syncthreads();
+    }  // dense row
 
     // ---- 3. fill this thread's columns ----
     if (!active) return;
@@ -332,7 +415,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
 }
 
 // Row-pass words of shared memory per row for a given (T, L).
-inline int row_words(int T, int L) { return (T * (L + 2)) / 2 + T * (L + 1) + 3 * T; }
+inline int row_words(int T, int L) { return (T * (L + 2)) / 2 + T * (L + 1) + 4 * T + kCompact + 2; }
 
 // Host-side dispatch over the compile-time segment length.
 template <bool TAKE_NEW>
