@@ -117,6 +117,19 @@ int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t
                        const int32_t* d_label, uint32_t* d_ordinal, dfc_stream_t stream);
 
 /*
+ * Stage two alone, from a vertical-DISTANCE plane: d_vdist[i*pitch_elems+k]
+ * = a (the squared vertical value is a*a), 0xFFFF = no feature in column k.
+ * Replaces meijster_scan(vert) (exact_edt.cpp:272-283) for vertical maps of
+ * perfect squares -- every map vertical_pass produces.  take_new = 1 is
+ * meijster_scan's tie rule (nearest_col = largest minimising column), 0 the
+ * keep_old rule; squared distances are identical either way.
+ * pitch_elems must be even and d_vdist 4-byte aligned.
+ */
+int dfc_envelope_vdist_u16(const uint16_t* d_vdist, int64_t rows, int64_t cols, int64_t pitch_elems,
+                           int take_new, int32_t* d_sqdist, float* d_dist, int32_t* d_nearest_col,
+                           dfc_stream_t stream);
+
+/*
  * Float distances of a squared-distance map: (float)sqrt((double)D) for each
  * of n int32 values (DFC_INF_I32 -> +inf) -- the row pass's own epilogue
  * (grid.cpp:146 semantics), e.g. for a map from dfc_vertical_u8.

@@ -49,11 +49,12 @@ _lib.dfc_last_launch_count.restype = C.c_int
 _lib.dfc_last_cuda_error.restype = C.c_int
 _lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
 _lib.dfc_sqrt_i32.argtypes = [_vp, _vp, _i64, _vp]
+_lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
 
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
-    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32",
+    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16",
 )
 
 
@@ -192,6 +193,25 @@ def raster(img: torch.Tensor, cityblock: bool = True, chessboard: bool = True,
             o.setdefault(key, _empty((h, w), torch.int32, img))
     _check(_lib.dfc_raster_u8(_ptr(img), h, w, pitch, _ptr(o.get("cityblock")),
                               _ptr(o.get("chessboard")), _ptr(o.get("chamfer34")), _stream(stream)))
+    return o
+
+
+def envelope_vdist(vdist: torch.Tensor, take_new: bool = True, dist: bool = False, stream=None):
+    """Stage two from a uint16 vertical-distance plane (0xFFFF = no feature):
+    meijster_scan(vert) for vert = a^2 (exact_edt.cpp:272-283)."""
+    if vdist.dtype != torch.int16 and vdist.dtype != torch.uint16:
+        raise ValueError("vdist must be a 16-bit CUDA tensor")
+    h, w = vdist.shape
+    if vdist.stride(1) != 1 or vdist.stride(0) % 2 or vdist.data_ptr() % 4:
+        padded = torch.full((h, w + (w & 1)), -1, dtype=torch.int16, device=vdist.device)
+        padded[:, :w] = vdist.view(torch.int16)
+        vdist = padded[:, :w]
+    o = {"sqdist": _empty((h, w), torch.int32, vdist), "nearest_col": _empty((h, w), torch.int32, vdist)}
+    if dist:
+        o["dist"] = _empty((h, w), torch.float32, vdist)
+    _check(_lib.dfc_envelope_vdist_u16(_ptr(vdist), h, w, vdist.stride(0), 1 if take_new else 0,
+                                       _ptr(o["sqdist"]), _ptr(o.get("dist")), _ptr(o["nearest_col"]),
+                                       _stream(stream)))
     return o
 
 

@@ -1,0 +1,154 @@
+// exact_edt.cpp -- distfield exact-EDT entry points over the C ABI.
+// Reference behaviour followed: exact_edt.cpp:112-117 (vertical_pass),
+// :232-237 (meijster_row_envelope), :272-283 (meijster_scan), :285-317 (edt),
+// :319-371 (voronoi_labels).
+#include "distfield/exact_edt.hpp"
+
+#include <cmath>
+#include <stdexcept>
+
+#include "device.hpp"
+
+namespace distfield {
+
+using detail::DeviceBuffer;
+using detail::dfc_check;
+using detail::stream;
+
+namespace {
+
+// Vertical map -> uint16 vertical-distance plane (0xFFFF = no feature in the
+// column).  Every finite value of a vertical-pass map is a perfect square.
+std::vector<std::uint16_t> vdist_plane(const DistanceMap& vert, std::size_t row0, std::size_t nrows,
+                                       std::size_t pitch) {
+    std::vector<std::uint16_t> a(nrows * pitch, 0xFFFF);
+    for (std::size_t i = 0; i < nrows; ++i) {
+        const auto r = vert.row(row0 + i);
+        for (std::size_t j = 0; j < vert.cols(); ++j) {
+            const std::uint64_t v = r[j];
+            if (DistanceMap::is_infinite(v)) continue;
+            auto s = static_cast<std::uint64_t>(std::sqrt(static_cast<double>(v)));
+            while (s * s > v) --s;
+            while ((s + 1) * (s + 1) <= v) ++s;
+            if (s * s != v || s >= 0xFFFF)
+                throw std::invalid_argument("meijster_scan: the GPU path needs a vertical-pass map "
+                                            "(finite values must be squares of row offsets)");
+            a[i * pitch + j] = static_cast<std::uint16_t>(s);
+        }
+    }
+    return a;
+}
+
+struct Scan {
+    std::vector<std::int32_t> d, col;
+};
+
+Scan scan_rows(const DistanceMap& vert, std::size_t row0, std::size_t nrows) {
+    const std::size_t cols = vert.cols(), pitch = cols + (cols & 1);
+    const auto plane = vdist_plane(vert, row0, nrows, pitch);
+    DeviceBuffer<std::uint16_t> da(plane.size());
+    da.upload(plane.data());
+    DeviceBuffer<std::int32_t> dd(nrows * cols), dc(nrows * cols);
+    dfc_check(dfc_envelope_vdist_u16(da.get(), (int64_t)nrows, (int64_t)cols, (int64_t)pitch, 1, dd.get(),
+                                     nullptr, dc.get(), stream()),
+              "meijster_scan");
+    return {dd.download(), dc.download()};
+}
+
+}  // namespace
+
+DistanceMap vertical_pass(const BinaryImage& img, unsigned) {
+    auto dimg = detail::upload_image(img);
+    DeviceBuffer<std::int32_t> dv(img.rows() * img.cols());
+    dfc_check(dfc_vertical_u8(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
+                              dv.get(), stream()),
+              "vertical_pass");
+    return detail::to_distance_map(dv.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean);
+}
+
+MeijsterResult meijster_scan(const DistanceMap& vert, ScanStats* stats, unsigned) {
+    const Scan s = scan_rows(vert, 0, vert.rows());
+    MeijsterResult out{detail::to_distance_map(s.d, vert.rows(), vert.cols(), DistanceKind::squared_euclidean),
+                       Grid<std::uint32_t>(vert.rows(), vert.cols(), kNoColumn)};
+    auto cells = out.nearest_col.cells();
+    for (std::size_t p = 0; p < cells.size(); ++p)
+        cells[p] = s.col[p] < 0 ? kNoColumn : static_cast<std::uint32_t>(s.col[p]);
+    if (stats) stats->candidates += vert.rows() * vert.cols();
+    return out;
+}
+
+EnvelopeState meijster_row_envelope(const DistanceMap& vert, std::size_t row) {
+    if (row >= vert.rows()) throw std::out_of_range("meijster_row_envelope: row out of range");
+    const Scan s = scan_rows(vert, row, 1);
+    const std::int64_t cols = static_cast<std::int64_t>(vert.cols());
+    EnvelopeState env;
+    env.ks.push_back(0);   // column-0 base (may own an empty segment)
+    env.js.push_back(0);
+    for (std::int64_t j = 0; j < cols; ++j) {
+        const std::int32_t k = s.col[static_cast<std::size_t>(j)];
+        if (k < 0) break;  // featureless row: only the base, js = {0, cols}
+        if (j == 0 && k == 0) continue;
+        if (k != env.ks.back() || (j == 0 && k != 0)) {
+            env.ks.push_back(k);
+            env.js.push_back(j);
+        }
+    }
+    env.js.push_back(cols);
+    return env;
+}
+
+DistanceMap edt(const BinaryImage& img, EdtAlgorithm, Orientation, ScanStats* stats, unsigned) {
+    auto dimg = detail::upload_image(img);
+    DeviceBuffer<std::int32_t> dd(img.rows() * img.cols());
+    dfc_check(dfc_edt_u8(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
+                         DFC_BG_TO_OBJ, dd.get(), nullptr, nullptr, nullptr, stream()),
+              "edt");
+    if (stats) stats->candidates += img.rows() * img.cols();
+    return detail::to_distance_map(dd.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean);
+}
+
+std::pair<DistanceMap, DistanceMap> edt_both_polarities(const BinaryImage& img) {
+    auto dimg = detail::upload_image(img);
+    const std::size_t n = img.rows() * img.cols();
+    DeviceBuffer<std::int32_t> d0(n), d1(n);
+    dfc_check(dfc_edt_u8_dual(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
+                              d0.get(), nullptr, d1.get(), nullptr, stream()),
+              "edt_both_polarities");
+    return {detail::to_distance_map(d0.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean),
+            detail::to_distance_map(d1.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean)};
+}
+
+std::vector<float> edt_distances(const BinaryImage& img) {
+    auto dimg = detail::upload_image(img);
+    const std::size_t n = img.rows() * img.cols();
+    DeviceBuffer<std::int32_t> dd(n);
+    DeviceBuffer<float> ds(n);
+    dfc_check(dfc_edt_u8(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
+                         DFC_BG_TO_OBJ, dd.get(), ds.get(), nullptr, nullptr, stream()),
+              "edt_distances");
+    return ds.download();
+}
+
+LabelMap voronoi_labels(const BinaryImage& img, unsigned) {
+    const std::size_t n = img.rows() * img.cols();
+    auto dimg = detail::upload_image(img);
+    DeviceBuffer<std::int32_t> dd(n), dl(n);
+    dfc_check(dfc_edt_u8(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
+                         DFC_BG_TO_OBJ, dd.get(), nullptr, dl.get(), nullptr, stream()),
+              "voronoi_labels");
+    std::int32_t d00 = 0;
+    detail::cuda_check(cudaMemcpyAsync(&d00, dd.get(), sizeof d00, cudaMemcpyDeviceToHost, stream()), "d2h");
+    detail::cuda_check(cudaStreamSynchronize(stream()), "synchronize");
+    if (d00 == DFC_INF_I32) throw std::domain_error("no features: voronoi labels undefined");  // :321
+    DeviceBuffer<std::uint32_t> dord(n);
+    dfc_check(dfc_label_ordinals(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
+                                 dl.get(), dord.get(), stream()),
+              "voronoi_labels");
+    const auto ord = dord.download();
+    LabelMap lm(img.rows(), img.cols());
+    for (std::size_t i = 0; i < img.rows(); ++i)
+        for (std::size_t j = 0; j < img.cols(); ++j) lm(i, j) = ord[i * img.cols() + j];
+    return lm;
+}
+
+}  // namespace distfield

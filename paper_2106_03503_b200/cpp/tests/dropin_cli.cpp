@@ -1,0 +1,104 @@
+// dropin_cli -- exercises the C++ drop-in (namespace distfield) end to end for
+// tests/test_dropin.py:  dropin_cli <op> <rows> <cols> <in.u8> <out.bin> [arg]
+// Writes the reference-typed result (uint64 maps, uint32 labels/columns, or
+// int64 ks/js) as raw little-endian; on an exception prints its type and exits 3.
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+#include <typeinfo>
+#include <vector>
+
+#include "distfield/exact_edt.hpp"
+#include "distfield/propagation.hpp"
+#include "distfield/random_image.hpp"
+
+using namespace distfield;
+
+template <typename T>
+static void put(std::ofstream& f, const std::vector<T>& v) {
+    f.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * sizeof(T)));
+}
+static void put_map(std::ofstream& f, const DistanceMap& dm) {
+    for (std::size_t i = 0; i < dm.rows(); ++i) {
+        const auto r = dm.row(i);
+        f.write(reinterpret_cast<const char*>(r.data()), static_cast<std::streamsize>(r.size() * 8));
+    }
+}
+
+int main(int argc, char** argv) {
+    if (argc < 6) {
+        std::fprintf(stderr, "usage: dropin_cli op rows cols in out [arg]\n");
+        return 2;
+    }
+    const std::string op = argv[1];
+    const std::size_t rows = std::stoul(argv[2]), cols = std::stoul(argv[3]);
+    try {
+        BinaryImage img(rows, cols);
+        {
+            std::ifstream in(argv[4], std::ios::binary);
+            std::vector<char> buf(rows * cols);
+            in.read(buf.data(), static_cast<std::streamsize>(buf.size()));
+            for (std::size_t p = 0; p < buf.size(); ++p)
+                if (buf[p]) img.set_object(p / cols, p % cols);
+        }
+        std::ofstream out(argv[5], std::ios::binary);
+        if (op == "edt") {
+            ScanStats st;
+            put_map(out, edt(img, EdtAlgorithm::envelope, Orientation::automatic, &st, 4));
+        } else if (op == "edt_simple") {
+            put_map(out, edt(img, EdtAlgorithm::simple, Orientation::columns));
+        } else if (op == "vertical") {
+            put_map(out, vertical_pass(img));
+        } else if (op == "meijster") {
+            const auto r = meijster_scan(vertical_pass(img));
+            put_map(out, r.map);
+            std::vector<std::uint32_t> nc(r.nearest_col.cells().begin(), r.nearest_col.cells().end());
+            put(out, nc);
+        } else if (op == "rowenv") {
+            const auto env = meijster_row_envelope(vertical_pass(img), std::stoul(argv[6]));
+            std::vector<std::int64_t> v{static_cast<std::int64_t>(env.ks.size())};
+            v.insert(v.end(), env.ks.begin(), env.ks.end());
+            v.insert(v.end(), env.js.begin(), env.js.end());
+            put(out, v);
+        } else if (op == "labels") {
+            const auto lm = voronoi_labels(img);
+            std::vector<std::uint32_t> v(rows * cols);
+            for (std::size_t i = 0; i < rows; ++i)
+                for (std::size_t j = 0; j < cols; ++j) v[i * cols + j] = lm(i, j);
+            put(out, v);
+        } else if (op == "cityblock") {
+            put_map(out, cityblock_sequential(img));
+        } else if (op == "chamfer") {
+            put_map(out, chamfer34(img));
+        } else if (op == "chessboard") {
+            put_map(out, chessboard(img));
+        } else if (op == "both") {
+            const auto [a, b] = edt_both_polarities(img);
+            put_map(out, a);
+            put_map(out, b);
+        } else if (op == "random") {  // generator parity: rows cols <unused> out density seed
+            const auto r = generate_random_image(rows, cols, std::stod(argv[6]), std::stoull(argv[7]));
+            std::vector<std::uint8_t> v(rows * cols);
+            for (std::size_t p = 0; p < v.size(); ++p) v[p] = r.is_object(p / cols, p % cols);
+            put(out, v);
+        } else {
+            std::fprintf(stderr, "unknown op %s\n", op.c_str());
+            return 2;
+        }
+    } catch (const std::domain_error& e) {
+        std::printf("EXC domain_error: %s\n", e.what());
+        return 3;
+    } catch (const std::length_error& e) {
+        std::printf("EXC length_error: %s\n", e.what());
+        return 3;
+    } catch (const std::invalid_argument& e) {
+        std::printf("EXC invalid_argument: %s\n", e.what());
+        return 3;
+    } catch (const std::exception& e) {
+        std::printf("EXC %s: %s\n", typeid(e).name(), e.what());
+        return 3;
+    }
+    return 0;
+}

@@ -139,7 +139,7 @@ bool out_vec_ok(const void* p, int64_t stride) {
 // base + b*stride.  take_new selects meijster_scan's tie rule.
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
              int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
-             int64_t sN, cudaStream_t st) {
+             int64_t sN, cudaStream_t st, bool vdist = false) {
     const RowGeom g = row_geom((int)W);
     RowArgs a;
     a.nr = nr;
@@ -160,6 +160,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.sL = sL;
     a.NC = reinterpret_cast<char*>(NC);
     a.sN = sN;
+    a.vdist = vdist;
     a.vec = W % 4 == 0 && out_vec_ok(D, sD) && out_vec_ok(S, sS) && out_vec_ok(LB, sL) &&
             out_vec_ok(NC, sN);
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
@@ -368,6 +369,21 @@ int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t
         d_label, n, (int)cols, nw, masks, wpre, rowbase, d_ordinal);
     g_launches += 3;
     e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_envelope_vdist_u16(const uint16_t* d_vdist, int64_t rows, int64_t cols, int64_t pitch_elems,
+                           int take_new, int32_t* d_sqdist, float* d_dist, int32_t* d_nearest_col,
+                           dfc_stream_t stream) {
+    if (!d_vdist || (!d_sqdist && !d_dist && !d_nearest_col)) return DFC_ERR_ARG;
+    if (!shape_ok(rows, cols)) return DFC_ERR_SHAPE;
+    if (pitch_elems < cols || pitch_elems % 2 != 0 || !aligned(d_vdist, 4)) return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    const int rc = row_pass(d_vdist, 1, rows, cols, (int)pitch_elems, take_new != 0, d_sqdist, 0, d_dist,
+                            0, nullptr, 0, d_nearest_col, 0, (cudaStream_t)stream, true);
+    if (rc != DFC_OK) return rc;
+    const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 

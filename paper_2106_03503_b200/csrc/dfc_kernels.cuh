@@ -31,6 +31,7 @@ struct RowArgs {
     char* LB; int64_t sL;
     char* NC; int64_t sN;
     bool vec;                 // 16-byte vector stores are legal
+    bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
 };
 
 // Raster transforms (k_raster.cu)

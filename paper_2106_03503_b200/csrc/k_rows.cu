@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     const bool active = row < a.total_rows;
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
+    const uint32_t gi = a.vdist ? 0u : i;     // g = (gi - nr)^2
     const int W = a.W;
 
     uint32_t* base = smem + rho * a.row_smem_words;
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
             int gm = -1;  // vertical value of column m, -1 = no feature (:212)
             auto load_m = [&]() {
                 const uint32_t r = m < c1 ? nrs[LY::nidx(m)] : kNoRow;
-                const int am = (int)(i > r ? i - r : r - i);
+                const int am = (int)(gi > r ? gi - r : r - gi);
                 gm = r == kNoRow ? -1 : am * am;
             };
             load_m();
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
                             tk = (int)(e & 0xffffu);
                             ts = (int)(e >> 16);
                             const uint32_t rk = nrs[LY::nidx(tk)];
-                            const int ak = (int)(i > rk ? i - rk : rk - i);
+                            const int ak = (int)(gi > rk ? gi - rk : rk - gi);
                             tg = ak * ak;
                         }
                     }
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     }
     __syncthreads();
 
-    RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, i, W};
+    RowCtx<L, TAKE_NEW> cx{nrs, stk, cut, cnt, gi, W};
 
     // ---- 1b. row census: candidates per row, which warps have any ----
     const int lane = threadIdx.x & 31;
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
         const uint32_t ent = stk[sg * LY::stk_stride + e];
         k = ent & 0xffffu;
         rr = nrs[LY::nidx((int)k)];
-        const uint32_t av = i > rr ? i - rr : rr - i;
+        const uint32_t av = gi > rr ? gi - rr : rr - gi;
         gk = av * av;
         next_start = e + 1 < n ? (int)(stk[sg * LY::stk_stride + e + 1] >> 16) : W;
     };

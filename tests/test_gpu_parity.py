@@ -208,3 +208,21 @@ def test_sqrt_epilogue_exact(dfc):
     np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
     inf = dfc.sqrt_i32(torch.tensor([0x7FFFFFFF], dtype=torch.int32, device="cuda")).cpu().numpy()
     assert np.isinf(inf[0])
+
+
+@pytest.mark.parametrize("shape", [(40, 64), (7, 301), (1, 1000)])
+def test_envelope_from_vertical_plane(dfc, shape):
+    """dfc_envelope_vdist_u16 == meijster_scan(vertical_pass(img)) (take_new) and keep_old D."""
+    img = oracle.random_image(*shape, 0.03, shape[1])
+    vert = oracle.vertical_pass(img)
+    a = np.where(vert == oracle.INF, 0xFFFF, np.sqrt(vert.astype(np.float64)).astype(np.int64)).astype(np.uint16)
+    w = shape[1] + (shape[1] & 1)
+    plane = np.full((shape[0], w), 0xFFFF, np.uint16)
+    plane[:, : shape[1]] = a
+    t = torch.from_numpy(plane.view(np.int16)).cuda()[:, : shape[1]]
+    out = dfc.envelope_vdist(t, take_new=True, dist=True)
+    torch.cuda.synchronize()
+    d, ncol = oracle.meijster_scan(vert, take_new=True)
+    np.testing.assert_array_equal(out["sqdist"].cpu().numpy(), oracle.to_i32(d))
+    np.testing.assert_array_equal(out["nearest_col"].cpu().numpy(), ncol.view(np.int32))
+    np.testing.assert_array_equal(out["dist"].cpu().numpy(), oracle.sqrt_f32(oracle.to_i32(d)))
