@@ -34,7 +34,11 @@ def test_six_point_goldens():
     img = np.zeros((g["rows"], g["cols"]), np.uint8)
     for a, b in g["points"]:
         img[a, b] = 1
-    ref = lambda k: np.where(np.array(g[k]) < 0, INF, np.array(g[k])).astype(np.uint64).ravel()
+    def ref(k):
+        arr = np.array(g[k], dtype=np.int64)
+        out = arr.astype(np.uint64)
+        out[arr < 0] = INF
+        return out.ravel()
     assert (run("edt", img) == ref("kSquaredEuclidean")).all()
     assert (run("edt_simple", img) == ref("kSquaredEuclidean")).all()
     assert (run("vertical", img) == ref("kVerticalFinal")).all()
@@ -53,11 +57,11 @@ def test_dropin_matches_oracle(shape, dens):
     img = oracle.random_image(*shape, dens, shape[0] * 7 + shape[1])
     np.testing.assert_array_equal(run("edt", img), oracle.edt(img).ravel())
     np.testing.assert_array_equal(run("vertical", img), oracle.vertical_pass(img).ravel())
-    m = run("meijster", img, dtype=np.uint64)
+    m = run("meijster", img, dtype=np.uint8)
     npx = img.size
     d, ncol = oracle.meijster_scan(oracle.vertical_pass(img), take_new=True)
-    np.testing.assert_array_equal(m[:npx], d.ravel())
-    np.testing.assert_array_equal(m[npx:].view(np.uint32)[: npx], ncol.ravel())
+    np.testing.assert_array_equal(m[: 8 * npx].view(np.uint64), d.ravel())
+    np.testing.assert_array_equal(m[8 * npx:].view(np.uint32), ncol.ravel())
     lab = run("labels", img, dtype=np.uint32)
     want = oracle.voronoi_labels(img)
     if want is None:
