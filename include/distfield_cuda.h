@@ -117,6 +117,29 @@ int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t
                        const int32_t* d_label, uint32_t* d_ordinal, dfc_stream_t stream);
 
 /*
+ * Stage one alone as a uint16 nearest-object-row plane (0xFFFF = no object in
+ * the column): d_nr[i*nr_pitch + j] = the row of the nearest object pixel in
+ * column j (upper one on ties, exact_edt.cpp:327-360).  The building block of
+ * the column-striped multi-GPU path (config 5).  nr_pitch % 4 == 0,
+ * nr_pitch >= cols rounded up to 4, d_nr 8-byte aligned.
+ */
+int dfc_column_nr_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes, int polarity,
+                     uint16_t* d_nr, int64_t nr_pitch, dfc_stream_t stream);
+
+/*
+ * Stage two alone from a nearest-row plane that may be split into column
+ * tiles: element (i, j) at d_nr[(j / tile_cols) * tile_stride_elems +
+ * i * tile_cols + j % tile_cols]; tile_cols >= cols means one row-major
+ * plane of row stride tile_cols.  Local row i is global row row0 + i (the
+ * values in d_nr are global rows).  Labels are global linear indices
+ * (row * cols + col).  This is the row-stripe half of the config-5 exchange:
+ * the N all-to-all blocks are read in place.  tile_cols even.
+ */
+int dfc_rows_from_nr_u16(const uint16_t* d_nr, int64_t rows, int64_t cols, int64_t row0, int64_t tile_cols,
+                         int64_t tile_stride_elems, int take_new, int32_t* d_sqdist, float* d_dist,
+                         int32_t* d_label, int32_t* d_nearest_col, dfc_stream_t stream);
+
+/*
  * Stage two alone, from a vertical-DISTANCE plane: d_vdist[i*pitch_elems+k]
  * = a (the squared vertical value is a*a), 0xFFFF = no feature in column k.
  * Replaces meijster_scan(vert) (exact_edt.cpp:272-283) for vertical maps of

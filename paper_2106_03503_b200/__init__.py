@@ -49,12 +49,14 @@ _lib.dfc_last_launch_count.restype = C.c_int
 _lib.dfc_last_cuda_error.restype = C.c_int
 _lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
 _lib.dfc_sqrt_i32.argtypes = [_vp, _vp, _i64, _vp]
+_lib.dfc_column_nr_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
+_lib.dfc_rows_from_nr_u16.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp]
 _lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
 
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
-    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16",
+    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16",
 )
 
 
@@ -193,6 +195,33 @@ def raster(img: torch.Tensor, cityblock: bool = True, chessboard: bool = True,
             o.setdefault(key, _empty((h, w), torch.int32, img))
     _check(_lib.dfc_raster_u8(_ptr(img), h, w, pitch, _ptr(o.get("cityblock")),
                               _ptr(o.get("chessboard")), _ptr(o.get("chamfer34")), _stream(stream)))
+    return o
+
+
+def column_nr(img: torch.Tensor, polarity: int = 0, out: torch.Tensor = None, stream=None) -> torch.Tensor:
+    """Stage one as an int16 tensor of nearest object rows (uint16 bits, -1 = none),
+    shape [rows, round_up(cols, 4)]."""
+    img, h, w, pitch = _img2d(img)
+    wp = (w + 3) // 4 * 4
+    if out is None:
+        out = torch.empty((h, wp), dtype=torch.int16, device=img.device)
+    _check(_lib.dfc_column_nr_u8(_ptr(img), h, w, pitch, polarity, _ptr(out), out.stride(0), _stream(stream)))
+    return out
+
+
+def rows_from_nr(nr: torch.Tensor, rows: int, cols: int, row0: int = 0, tile_cols: int = None,
+                 tile_stride: int = 0, dist: bool = False, label: bool = False, stream=None, out=None):
+    """Stage two from a (possibly column-tiled) int16 nearest-row buffer; see
+    dfc_rows_from_nr_u16.  Returns int32 sqdist (+ float dist, int32 label)."""
+    o = dict(out or {})
+    o.setdefault("sqdist", torch.empty((rows, cols), dtype=torch.int32, device=nr.device))
+    if dist:
+        o.setdefault("dist", torch.empty((rows, cols), dtype=torch.float32, device=nr.device))
+    if label:
+        o.setdefault("label", torch.empty((rows, cols), dtype=torch.int32, device=nr.device))
+    tc = tile_cols if tile_cols is not None else nr.stride(0)
+    _check(_lib.dfc_rows_from_nr_u16(_ptr(nr), rows, cols, row0, tc, tile_stride, 0, _ptr(o["sqdist"]),
+                                     _ptr(o.get("dist")), _ptr(o.get("label")), None, _stream(stream)))
     return o
 
 

@@ -139,12 +139,16 @@ bool out_vec_ok(const void* p, int64_t stride) {
 // base + b*stride.  take_new selects meijster_scan's tie rule.
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
              int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
-             int64_t sN, cudaStream_t st, bool vdist = false) {
+             int64_t sN, cudaStream_t st, bool vdist = false, int tile_cols = 0,
+             int64_t tile_stride = 0, int row0 = 0) {
     const RowGeom g = row_geom((int)W);
     RowArgs a;
     a.nr = nr;
     a.nr_img_stride = H * Wp;
     a.Wp = Wp;
+    a.tile_cols = tile_cols > 0 ? tile_cols : Wp;
+    a.tile_stride = tile_stride;
+    a.row0 = row0;
     a.H = (int)H;
     a.W = (int)W;
     a.total_rows = nimg * H;
@@ -369,6 +373,46 @@ int dfc_label_ordinals(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t
         d_label, n, (int)cols, nw, masks, wpre, rowbase, d_ordinal);
     g_launches += 3;
     e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_column_nr_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes, int polarity,
+                     uint16_t* d_nr, int64_t nr_pitch, dfc_stream_t stream) {
+    if (!d_img || !d_nr || (polarity != 0 && polarity != 1)) return DFC_ERR_ARG;
+    if (!shape_ok(rows, cols)) return DFC_ERR_SHAPE;
+    if (pitch_bytes < cols || nr_pitch < round_up(cols, 4) || nr_pitch % 4 != 0 || !aligned(d_nr, 8))
+        return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nb = (rows + kBand - 1) / kBand;
+    Scratch sc(st);
+    cudaError_t e = sc.alloc(2 * (size_t)nb * nr_pitch * sizeof(uint16_t));
+    if (e != cudaSuccess) return cuda_fail(e);
+    uint16_t* first = static_cast<uint16_t*>(sc.p);
+    uint16_t* last = first + nb * nr_pitch;
+    column_pass(d_img, 1, rows, cols, pitch_bytes, 0, polarity, 1, d_nr, first, last, (int)nr_pitch, st);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_rows_from_nr_u16(const uint16_t* d_nr, int64_t rows, int64_t cols, int64_t row0, int64_t tile_cols,
+                         int64_t tile_stride_elems, int take_new, int32_t* d_sqdist, float* d_dist,
+                         int32_t* d_label, int32_t* d_nearest_col, dfc_stream_t stream) {
+    if (!d_nr || (!d_sqdist && !d_dist && !d_label && !d_nearest_col)) return DFC_ERR_ARG;
+    if (rows < 1 || cols < 1 || cols > kMaxRowCols || row0 < 0 || row0 + rows > 65535) return DFC_ERR_SHAPE;
+    const int64_t hi = row0 + rows - 1;
+    if (hi * hi + (cols - 1) * (cols - 1) > DFC_MAX_SQDIST) return DFC_ERR_SHAPE;
+    if (tile_cols < 2 || tile_cols % 2 != 0 || !aligned(d_nr, 4) || tile_stride_elems % 2 != 0) return DFC_ERR_ARG;
+    if (tile_cols < cols && tile_stride_elems < rows * tile_cols) return DFC_ERR_ARG;
+    if (take_new && d_label) return DFC_ERR_ARG;  // labels follow the keep_old rule
+    init_pool_once();
+    g_launches = 0;
+    const int rc = row_pass(d_nr, 1, rows, cols, (int)std::min<int64_t>(tile_cols, 1 << 30), take_new != 0,
+                            d_sqdist, 0, d_dist, 0, d_label, 0, d_nearest_col, 0, (cudaStream_t)stream, false,
+                            (int)std::min<int64_t>(tile_cols, 1 << 30), tile_stride_elems, (int)row0);
+    if (rc != DFC_OK) return rc;
+    const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 

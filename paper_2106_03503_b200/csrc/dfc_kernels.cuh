@@ -20,7 +20,10 @@ struct ColArgs {
 struct RowArgs {
     const uint16_t* nr;       // nearest object row per (row, column), kNoRow = none
     int64_t nr_img_stride;    // elements between images/slots
-    int Wp;                   // elements between rows of nr
+    int Wp;                   // elements between rows of nr (inside one column tile)
+    int tile_cols;            // columns per tile of the nr plane (>= W: one tile)
+    int64_t tile_stride;      // elements between consecutive column tiles
+    int row0;                 // global row of local row 0 (row-striped shards)
     int H, W;
     int64_t total_rows;       // n_img * H
     int T, L, R;              // threads per row, columns per thread, rows per CTA

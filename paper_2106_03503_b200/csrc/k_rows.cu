@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
     const bool active = row < a.total_rows;
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
-    const uint32_t gi = a.vdist ? 0u : i;     // g = (gi - nr)^2
+    const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // g = (gi - nr)^2, global row
     const int W = a.W;
 
     uint32_t* base = smem + rho * a.row_smem_words;
@@ -132,11 +132,21 @@ __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
 
     // ---- 0. stage the row's nearest-row values (coalesced 4-byte loads) ----
     if (active) {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(a.nr + img * a.nr_img_stride +
-                                                                (int64_t)i * a.Wp);
+        const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
         const int npairs = (W + 1) >> 1;
-        for (int q = s; q < npairs; q += T)
-            *reinterpret_cast<uint32_t*>(nrs + LY::nidx(2 * q)) = __ldg(src + q);
+        if (a.tile_cols >= W) {  // one tile: the row is contiguous
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(rowp);
+            for (int q = s; q < npairs; q += T)
+                *reinterpret_cast<uint32_t*>(nrs + LY::nidx(2 * q)) = __ldg(src + q);
+        } else {                 // row striped over column tiles (received all-to-all blocks)
+            int t = (2 * s) / a.tile_cols;  // tile of column 2q, advanced incrementally
+            for (int q = s; q < npairs; q += T) {
+                const int j = 2 * q;
+                while (j >= (t + 1) * a.tile_cols) ++t;
+                const uint16_t* p = rowp + t * a.tile_stride + (j - t * a.tile_cols);
+                *reinterpret_cast<uint32_t*>(nrs + LY::nidx(j)) = __ldg(reinterpret_cast<const uint32_t*>(p));
+            }
+        }
     }
     __syncthreads();
 
