@@ -134,7 +134,18 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg = args.config
-    img_np, seed = make_input(cfg, rank)
+    sharded_mode = world > 1 and cfg in ("c3", "c5")
+    img_np, seed = make_input(cfg, 0 if sharded_mode else rank)
+    job_px = img_np.size if sharded_mode else img_np.size * world   # pixels the whole job does per step
+    if sharded_mode and cfg == "c3":      # per-image shards, no collective
+        from paper_2106_03503_b200.sharded import shard_range
+        lo, hi = shard_range(img_np.shape[0], rank, world)
+        img_np = np.ascontiguousarray(img_np[lo:hi])
+    H5 = W5 = None
+    if sharded_mode and cfg == "c5":      # column stripes -> NCCL all-to-all -> row stripes
+        H5, W5 = img_np.shape
+        Ws = W5 // world
+        img_np = np.ascontiguousarray(img_np[:, rank * Ws:(rank + 1) * Ws])
     img = torch.from_numpy(img_np).to(dev)
     npx = img_np.size
     stream = torch.cuda.current_stream()
@@ -146,6 +157,10 @@ def run_ours(args, rank, world, local_rank):
                for k, dt in (("sqdist_bg", torch.int32), ("dist_bg", torch.float32),
                              ("sqdist_obj", torch.int32), ("dist_obj", torch.float32))}
         step = lambda: dfc.edt_dual(img, out=out)
+    elif sharded_mode and cfg == "c5":
+        from paper_2106_03503_b200 import sharded
+        out = {}
+        step = lambda: sharded.edt_column_striped(img, H5, W5, rank, world)
     elif cfg == "c1" or cfg == "c5":
         out = {"sqdist": torch.empty(img_np.shape, dtype=torch.int32, device=dev)}
         if cfg == "c1":
@@ -199,16 +214,24 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, row_ms = float(t[0]), float(t[1])
     ms_per_step = total_ms / args.steps
-    value = world * npx * args.steps / (total_ms * 1e-3) / 1e6
+    value = job_px * args.steps / (total_ms * 1e-3) / 1e6
 
     # ---- e2e through the public API with HOST buffers (pinned), copies timed ----
     host_in = torch.from_numpy(img_np).pin_memory()
     host_out = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in out.items()}
     dev_in = torch.empty_like(img)
 
+    e2e_host_out = {}
+
     def e2e_step():
         dev_in.copy_(host_in, non_blocking=True)
         nonlocal_img = dev_in
+        if sharded_mode and cfg == "c5":
+            _, _, sq = sharded.edt_column_striped(nonlocal_img, H5, W5, rank, world)
+            if "sq" not in e2e_host_out:
+                e2e_host_out["sq"] = torch.empty(sq.shape, dtype=sq.dtype).pin_memory()
+            e2e_host_out["sq"].copy_(sq, non_blocking=True)
+            return
         if cfg == "c2":
             dfc.edt_dual(nonlocal_img, out=out)
         elif cfg in ("c1", "c5"):
@@ -238,15 +261,16 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t[0])
     h2d = int(host_in.numel() * host_in.element_size())
-    d2h = int(sum(v.numel() * v.element_size() for v in host_out.values()))
+    d2h = int(sum(v.numel() * v.element_size() for v in host_out.values())) + \
+        int(sum(v.numel() * v.element_size() for v in e2e_host_out.values()))
 
     if rank != 0:
         return None
     peak, peak_src = peaks()
     c = CONFIGS[cfg]
-    kernel_bytes = c["bytes_kernel"] * npx
+    kernel_bytes = c["bytes_kernel"] * (npx if not (sharded_mode and cfg == "c5") else H5 * W5 // world)
     achieved = kernel_bytes / (row_ms * 1e-3) / 1e9
-    step_achieved = c["bytes_alg"] * npx / (ms_per_step * 1e-3) / 1e9
+    step_achieved = c["bytes_alg"] * job_px / world / (ms_per_step * 1e-3) / 1e9
     line = {
         "metric": "exact squared-EDT Mpixel/s (bit-exact)" if cfg != "c4" else "raster DT Mpixel/s (bit-exact)",
         "value": round(value, 1),
@@ -256,12 +280,15 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 5),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded_mode else "weak",
         "vs_baseline": None,
         "dtype": "u8->int32" + ("+f32" if cfg in ("c1", "c2") else ""),
         "data": "synthetic (seeded stand-in, SURVEY.md 8(d))",
         "config": {"workload": c["desc"], "seed": seed, "pixels_per_gpu_step": npx,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"replicas x{world}" if not sharded_mode else
+                                   f"per-image shards x{world}" if cfg == "c3" else
+                                   f"column stripes -> NCCL all-to-all -> row stripes x{world}"),
                    "l2": "256 MiB flush between timed steps (outside the events)"},
         "roofline": {
             "bound": "hbm", "kernel": "k_rows (row envelope)" if cfg != "c4" else "k_band_* + k_raster (whole step)",
@@ -271,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
             "step": {"bytes_alg_per_px": c["bytes_alg"], "achieved": round(step_achieved, 1),
                      "frac": round(step_achieved / peak, 4)},
         },
-        "e2e": {"value": round(world * npx / (e2e_ms * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
+        "e2e": {"value": round(job_px / (e2e_ms * 1e-3) / 1e6, 1), "unit": "Mpixel/s",
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,

@@ -408,10 +408,12 @@ int dfc_rows_from_nr_u16(const uint16_t* d_nr, int64_t rows, int64_t cols, int64
     if (take_new && d_label) return DFC_ERR_ARG;  // labels follow the keep_old rule
     init_pool_once();
     g_launches = 0;
+    prof(1, (cudaStream_t)stream);
     const int rc = row_pass(d_nr, 1, rows, cols, (int)std::min<int64_t>(tile_cols, 1 << 30), take_new != 0,
                             d_sqdist, 0, d_dist, 0, d_label, 0, d_nearest_col, 0, (cudaStream_t)stream, false,
                             (int)std::min<int64_t>(tile_cols, 1 << 30), tile_stride_elems, (int)row0);
     if (rc != DFC_OK) return rc;
+    prof(2, (cudaStream_t)stream);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
