@@ -3,5 +3,6 @@
 // code), so kernel host stubs, templates and registrations live in one unit.
 #include "k_columns.cu"
 #include "k_rows.cu"
+#include "k_rows_stream.cu"
 #include "k_raster.cu"
 #include "dfc_api.cu"

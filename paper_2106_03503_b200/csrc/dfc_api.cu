@@ -167,14 +167,51 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.vdist = vdist;
     a.vec = W % 4 == 0 && out_vec_ok(D, sD) && out_vec_ok(S, sS) && out_vec_ok(LB, sL) &&
             out_vec_ok(NC, sN);
+    a.row_list = nullptr;
+    a.row_count = nullptr;
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e);
-    void* args[] = {&a};
-    e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
-    if (e != cudaSuccess) return cuda_fail(e);
+
+    // Streaming kernel (one lane = one row) when the nr plane allows coalesced
+    // 16-byte tile loads; rows whose live stack overflows go to k_rows.
+    static const bool force_segment = [] {
+        const char* v = getenv("DFC_ROWS");
+        return v && strcmp(v, "segment") == 0;
+    }();
+    const bool stream_ok = !force_segment && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
+                           a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
+    if (stream_ok) {
+        Scratch fl(st);
+        e = fl.alloc((size_t)(a.total_rows + 1) * sizeof(int));
+        if (e != cudaSuccess) return cuda_fail(e);
+        int* fail_count = static_cast<int*>(fl.p);
+        int* fail_rows = fail_count + 1;
+        e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        const void* sfn = take_new ? stream_kernel_ptr<true>() : stream_kernel_ptr<false>();
+        const int ssm = stream_smem_bytes();
+        e = cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
+        if (e != cudaSuccess) return cuda_fail(e);
+        const int64_t sblocks = (a.total_rows + 32 * kSWarps - 1) / (32 * kSWarps);
+        void* sargs[] = {&a, &fail_rows, &fail_count};
+        e = cudaLaunchKernel(sfn, dim3((unsigned)sblocks), dim3(32 * kSWarps), sargs, (size_t)ssm, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        ++g_launches;
+        RowArgs fb = a;  // fallback: the segment kernel over the overflowed rows
+        fb.row_list = fail_rows;
+        fb.row_count = fail_count;
+        void* fargs[] = {&fb};
+        const int64_t fblocks = std::min<int64_t>(blocks, 148 * 4);
+        e = cudaLaunchKernel(fn, dim3((unsigned)fblocks), dim3(g.R * g.T), fargs, (size_t)g.smem_bytes, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+    } else {
+        void* args[] = {&a};
+        e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
     ++g_launches;
     return DFC_OK;
 }

@@ -35,6 +35,8 @@ struct RowArgs {
     char* NC; int64_t sN;
     bool vec;                 // 16-byte vector stores are legal
     bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
+    const int* row_list;      // fallback mode: process only these rows (nullptr: all)
+    const int* row_count;     // number of entries in row_list (device)
 };
 
 // Raster transforms (k_raster.cu)

@@ -108,14 +108,36 @@ struct RowCtx {
 };
 
 template <int L, bool TAKE_NEW>
+__device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp);
+
+template <int L, bool TAKE_NEW>
 __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
+    if (a.row_list == nullptr) {
+        rows_group<L, TAKE_NEW>(a, blockIdx.x);
+        return;
+    }
+    // fallback mode (rows the streaming kernel could not hold): grid-stride
+    // over the listed rows; the trip count is uniform per CTA
+    const int64_t n = *a.row_count;
+    for (int64_t grp = blockIdx.x; grp * a.R < n; grp += gridDim.x) {
+        rows_group<L, TAKE_NEW>(a, grp);
+        __syncthreads();
+    }
+}
+
+template <int L, bool TAKE_NEW>
+__device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     using LY = RowLayout<L>;
     extern __shared__ uint32_t smem[];
     const int T = a.T;
     const int rho = threadIdx.x / T;          // row within the CTA
     const int s = threadIdx.x - rho * T;      // segment (thread) within the row
-    const int64_t row = (int64_t)blockIdx.x * a.R + rho;
-    const bool active = row < a.total_rows;
+    int64_t row = grp * a.R + rho;
+    bool active = row < a.total_rows;
+    if (a.row_list) {
+        active = row < *a.row_count;
+        row = active ? a.row_list[row] : 0;
+    }
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // g = (gi - nr)^2, global row
