@@ -167,6 +167,14 @@ int dfc_sqrt_i32(const int32_t* d_sqdist, float* d_dist, int64_t n, dfc_stream_t
  */
 int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_end);
 
+/*
+ * Stage-2 kernel selection for the calls of this thread: 0 = library
+ * default, 1 = segment/merge kernel (k_rows), 2 = streaming lane-per-row
+ * kernel (k_rows_stream, with k_rows as its overflow fallback).  Results are
+ * identical; this is a performance/testing knob.
+ */
+int dfc_set_row_kernel(int mode);
+
 /* Number of kernels the last successful call on this thread enqueued. */
 int dfc_last_launch_count(void);
 /* Human-readable status; never NULL. */

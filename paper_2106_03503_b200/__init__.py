@@ -49,6 +49,7 @@ _lib.dfc_last_launch_count.restype = C.c_int
 _lib.dfc_last_cuda_error.restype = C.c_int
 _lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
 _lib.dfc_sqrt_i32.argtypes = [_vp, _vp, _i64, _vp]
+_lib.dfc_set_row_kernel.argtypes = [C.c_int]
 _lib.dfc_column_nr_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
 _lib.dfc_rows_from_nr_u16.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp]
 _lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
@@ -56,7 +57,7 @@ _lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
-    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16",
+    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel",
 )
 
 
@@ -83,6 +84,11 @@ def set_profile_events(col_begin=None, row_begin=None, row_end=None) -> None:
     edt* calls on this thread (measurement hook for bench.py); None disables."""
     h = lambda e: None if e is None else C.c_void_p(e.cuda_event)
     _check(_lib.dfc_set_profile_events(h(col_begin), h(row_begin), h(row_end)))
+
+
+def set_row_kernel(mode: str) -> None:
+    """Stage-2 kernel for this thread's calls: "default", "segment" or "stream"."""
+    _check(_lib.dfc_set_row_kernel({"default": 0, "segment": 1, "stream": 2}[mode]))
 
 
 def last_launch_count() -> int:

@@ -17,6 +17,17 @@ namespace {
 thread_local int g_last_cuda = 0;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming kernel
+
+// DFC_ROWS=segment|stream overrides the default stage-2 kernel (tuning/A-B).
+int env_row_mode() {
+    static const int m = [] {
+        const char* v = getenv("DFC_ROWS");
+        if (v && strcmp(v, "stream") == 0) return 2;
+        return 1;  // default: the segment/merge kernel
+    }();
+    return m;
+}
 
 void prof(int k, cudaStream_t st) {
     if (g_ev[k]) cudaEventRecord(g_ev[k], st);
@@ -177,11 +188,8 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
 
     // Streaming kernel (one lane = one row) when the nr plane allows coalesced
     // 16-byte tile loads; rows whose live stack overflows go to k_rows.
-    static const bool force_segment = [] {
-        const char* v = getenv("DFC_ROWS");
-        return v && strcmp(v, "segment") == 0;
-    }();
-    const bool stream_ok = !force_segment && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
+    const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
+    const bool stream_ok = mode == 2 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
                            a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
     if (stream_ok) {
         Scratch fl(st);
@@ -191,7 +199,8 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         int* fail_rows = fail_count + 1;
         e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
         if (e != cudaSuccess) return cuda_fail(e);
-        const void* sfn = take_new ? stream_kernel_ptr<true>() : stream_kernel_ptr<false>();
+        const int outs = (D ? kOutD : 0) | (S ? kOutS : 0) | (LB ? kOutL : 0) | (NC ? kOutN : 0);
+        const void* sfn = take_new ? stream_kernel_ptr<true>(outs) : stream_kernel_ptr<false>(outs);
         const int ssm = stream_smem_bytes();
         e = cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
         if (e != cudaSuccess) return cuda_fail(e);
@@ -485,6 +494,12 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
     g_ev[0] = static_cast<cudaEvent_t>(ev_col_begin);
     g_ev[1] = static_cast<cudaEvent_t>(ev_row_begin);
     g_ev[2] = static_cast<cudaEvent_t>(ev_row_end);
+    return DFC_OK;
+}
+
+int dfc_set_row_kernel(int mode) {
+    if (mode < 0 || mode > 2) return DFC_ERR_ARG;
+    g_row_mode = mode;
     return DFC_OK;
 }
 

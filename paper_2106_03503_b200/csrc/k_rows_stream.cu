@@ -4,37 +4,45 @@
 // voronoi label assembly, exact_edt.cpp:190-283, :362-369) with a different
 // parallel decomposition: a warp owns 32 rows, every lane runs the reference's
 // stack algorithm (exact_edt.cpp:208-223) over ITS row, left to right, in
-// lockstep over columns -- so all 32 lanes do the same work, no merges exist.
-// Columns are emitted as soon as they are final:
+// lockstep over columns -- all 32 lanes do the same work and no merges exist.
+// Columns are final as soon as no later parabola can change their owner:
 //
 //     every parabola of a later column p >= m+1 has D_p(F) >= (m+1-F)^2, so
 //     keep_old : D(F) <= (m+1-F)^2 => final   (a later column must be strictly smaller)
 //     take_new : D(F) <  (m+1-F)^2 => final   (a later column wins ties)
 //
-// and entries owning only final columns leave the stack.  The live stack is
-// tiny in practice (<= ~50 entries on the five configs; tests/stream_model.py
-// is the statement-level model, fuzzed against brute force), so it lives in a
-// per-lane ring of kCap entries in shared memory ([entry][lane]: every access
-// hits the lane's own bank).  A row that would overflow its ring is appended to
-// a fallback list and recomputed by k_rows (the segment/merge kernel).
+// and stack entries owning only final columns leave the stack, so the live
+// stack stays tiny in practice (<= ~50 entries on the five configs).  It lives
+// in a per-lane ring in shared memory ([entry][lane]: each lane hits its own
+// bank); a row that overflows its ring goes to a fallback list recomputed by
+// k_rows.  tests/stream_model.py is the statement-level model (fuzzed against
+// brute force for both tie rules).
 //
-// Input nearest-row values are staged 32 rows x 64 columns at a time through
-// shared memory with coalesced 16-byte loads, prefetched one tile ahead.
+// Data movement: nearest-row values are staged 32 rows x 32 columns at a time
+// with coalesced 16-byte loads (prefetched one tile ahead).  A lane records the
+// owner (column | nearest row << 16) of each final column in a 2 x 32-column
+// staging slot; completed 32-column blocks are flushed by the whole warp --
+// lane c computes column c of the block's row -- so D, sqrt(D), labels and
+// nearest columns all leave with coalesced 128-byte stores.
 #include "dfc_kernels.cuh"
 
 namespace dfc {
 
-constexpr int kSCap = 64;          // live-stack ring entries per lane
-constexpr int kSTile = 64;         // columns per staged input tile
-constexpr int kSTileStride = 66;   // halfwords per staged row (33 words: conflict-free)
+constexpr int kSCap = 32;          // live-stack ring entries per lane
+constexpr int kSTile = 32;         // columns per staged input tile
+constexpr int kSTileStride = 34;   // halfwords per staged row (17 words: conflict-free)
 constexpr int kSWarps = 4;         // warps (bands of 32 rows) per CTA
+constexpr uint32_t kEmpty = 0xFFFF0000u;  // staged owner of a featureless row
+
+enum : int { kOutD = 1, kOutS = 2, kOutL = 4, kOutN = 8 };
 
 struct StreamSmem {
-    uint16_t tile[32 * kSTileStride];   // current input tile [row][col]
+    uint16_t tile[32 * kSTileStride];   // input tile [row][col]
     uint2 stk[kSCap * 32];              // [entry][lane]: x = k | start << 16, y = nr_k
+    uint32_t stage[2][32][33];          // [slot][lane][col]: owner k | nr_k << 16
 };
 
-template <bool TAKE_NEW>
+template <bool TAKE_NEW, int OUTS>
 __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fail_rows, int* fail_count) {
     extern __shared__ uint4 smem_raw[];
     StreamSmem& sm = reinterpret_cast<StreamSmem*>(smem_raw)[threadIdx.x >> 5];
@@ -46,80 +54,40 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
-    const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
+    const uint16_t* rowp = active ? a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp : nullptr;
 
-    // ---- cooperative, coalesced staging of 32 rows x 64 columns ----
-    // lane q loads 16-byte chunk (q & 7) of rows (q >> 3) + 4t, t = 0..7
-    uint4 pre[8];
-    auto row_ptr = [&](int rl) -> const uint16_t* {
-        const int64_t r = band * 32 + rl;
-        if (r >= a.total_rows) return nullptr;
-        const int im = (int)(r / a.H);
-        return a.nr + im * a.nr_img_stride + (r - (int64_t)im * a.H) * a.Wp;
-    };
+    // ---- staging: lane q loads 16-byte chunk (q & 3) of rows (q >> 2) + 8t ----
+    uint4 pre[4];
     auto prefetch = [&](int c0) {
+        const int j = c0 + 8 * (lane & 3);
+        const int tt = j / a.tile_cols;  // column tile (all-to-all blocks); 8 | tile_cols
+        const int64_t off = tt * a.tile_stride + (j - tt * a.tile_cols);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int rl = (lane >> 3) + 4 * t;
-            const int j = c0 + 8 * (lane & 7);
-            const uint16_t* p = row_ptr(rl);
+        for (int t = 0; t < 4; ++t) {
+            const int rl = (lane >> 2) + 8 * t;
+            const uint16_t* p = (const uint16_t*)__shfl_sync(0xffffffffu, (unsigned long long)rowp, rl);
             uint4 v = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-            if (p && j < W) {
-                const int tt = j / a.tile_cols;  // column tile (all-to-all blocks); 8 | tile_cols
-                v = __ldg(reinterpret_cast<const uint4*>(p + tt * a.tile_stride + (j - tt * a.tile_cols)));
-            }
+            if (p && j < W) v = __ldg(reinterpret_cast<const uint4*>(p + off));
             pre[t] = v;
         }
     };
     auto commit = [&]() {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int rl = (lane >> 3) + 4 * t;
-            uint32_t* d = reinterpret_cast<uint32_t*>(sm.tile + rl * kSTileStride + 8 * (lane & 7));
+        for (int t = 0; t < 4; ++t) {
+            const int rl = (lane >> 2) + 8 * t;
+            uint32_t* d = reinterpret_cast<uint32_t*>(sm.tile + rl * kSTileStride + 8 * (lane & 3));
             d[0] = pre[t].x; d[1] = pre[t].y; d[2] = pre[t].z; d[3] = pre[t].w;
         }
     };
 
-    int32_t* Drow = a.D ? reinterpret_cast<int32_t*>(a.D + img * a.sD) + (int64_t)i * W : nullptr;
-    float* Srow = a.S ? reinterpret_cast<float*>(a.S + img * a.sS) + (int64_t)i * W : nullptr;
-    int32_t* Lrow = a.LB ? reinterpret_cast<int32_t*>(a.LB + img * a.sL) + (int64_t)i * W : nullptr;
-    int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + img * a.sN) + (int64_t)i * W : nullptr;
-
-    // ---- per-lane stack ring + registers for its two ends ----
-    int head = 0, cnt = 0;                 // ring: entries head .. head+cnt-1
-    int tk = 0, ts = 0; uint32_t tg = 0;   // top entry
+    // ---- per-lane live stack + its two ends in registers ----
+    int head = 0, cnt = 0;                  // ring entries head .. head+cnt-1
+    int tk = 0, ts = 0; uint32_t tg = 0;    // top entry
     int bk = 0; uint32_t bnr = kNoRow, bg = 0; int bend = W;  // bottom entry, end of its range
-    int F = 0;                             // first non-final column
-    bool dead = !active;                   // overflowed (or no row): recomputed elsewhere
+    int F = 0;                              // first non-final column
+    uint32_t pend = 0;                      // staging slots holding a completed block
+    bool dead = !active;                    // overflowed (or no row): recomputed elsewhere
 
-    // 4-column output staging in registers (shift in, store when aligned)
-    int32_t od0 = 0, od1 = 0, od2 = 0, od3 = 0;
-    int32_t ol0 = 0, ol1 = 0, ol2 = 0, ol3 = 0;
-    int32_t on0 = 0, on1 = 0, on2 = 0, on3 = 0;
-    auto emit = [&](int j, uint32_t d, uint32_t k, uint32_t nrk, bool inf) {
-        const int32_t dv = inf ? DFC_INF_I32 : (int32_t)d;
-        const int32_t lv = inf ? -1 : (int32_t)(nrk * (uint32_t)W + k);
-        const int32_t nv = inf ? -1 : (int32_t)k;
-        if (a.vec) {
-            od0 = od1; od1 = od2; od2 = od3; od3 = dv;
-            ol0 = ol1; ol1 = ol2; ol2 = ol3; ol3 = lv;
-            on0 = on1; on1 = on2; on2 = on3; on3 = nv;
-            if ((j & 3) == 3) {
-                const int j0 = j - 3;
-                if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j0), make_int4(od0, od1, od2, od3));
-                if (Srow)
-                    __stcs(reinterpret_cast<float4*>(Srow + j0),
-                           make_float4(dist_f32(od0), dist_f32(od1), dist_f32(od2), dist_f32(od3)));
-                if (Lrow) __stcs(reinterpret_cast<int4*>(Lrow + j0), make_int4(ol0, ol1, ol2, ol3));
-                if (Nrow) __stcs(reinterpret_cast<int4*>(Nrow + j0), make_int4(on0, on1, on2, on3));
-            }
-        } else {
-            if (Drow) Drow[j] = dv;
-            if (Srow) Srow[j] = dist_f32((uint32_t)dv);
-            if (Lrow) Lrow[j] = lv;
-            if (Nrow) Nrow[j] = nv;
-        }
-    };
     auto ent = [&](int idx) -> uint2& { return sm.stk[((head + idx) & (kSCap - 1)) * 32 + lane]; };
     auto load_bottom = [&]() {
         const uint2 e = ent(0);
@@ -129,21 +97,80 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
         bg = av * av;
         bend = cnt >= 2 ? (int)(ent(1).x >> 16) : W;
     };
-    // finalise columns F.. while no later parabola (column >= m1) can beat them
+
+    // ---- warp-cooperative flush of completed 32-column blocks ----
+    char* Dbase = a.D ? a.D + img * a.sD + (int64_t)i * W * 4 : nullptr;
+    char* Sbase = a.S ? a.S + img * a.sS + (int64_t)i * W * 4 : nullptr;
+    char* Lbase = a.LB ? a.LB + img * a.sL + (int64_t)i * W * 4 : nullptr;
+    char* Nbase = a.NC ? a.NC + img * a.sN + (int64_t)i * W * 4 : nullptr;
+    auto flush = [&](bool tail) {
+        // tail: also write the partial block at the end of the row (F == W)
+        uint32_t want = pend;
+        if (tail && !dead && (W & 31) && F == W) want |= 1u << ((W >> 5) & 1);
+        uint32_t ready = __ballot_sync(0xffffffffu, want != 0);
+        while (ready) {
+            const int L = __ffs(ready) - 1;
+            ready &= ready - 1;
+            const uint32_t wL = __shfl_sync(0xffffffffu, want, L);
+            const int FL = __shfl_sync(0xffffffffu, F, L);
+            const uint32_t giL = __shfl_sync(0xffffffffu, gi, L);
+            char* Db = (char*)__shfl_sync(0xffffffffu, (unsigned long long)Dbase, L);
+            char* Sb = (char*)__shfl_sync(0xffffffffu, (unsigned long long)Sbase, L);
+            char* Lb = (char*)__shfl_sync(0xffffffffu, (unsigned long long)Lbase, L);
+            char* Nb = (char*)__shfl_sync(0xffffffffu, (unsigned long long)Nbase, L);
+            for (int s = 0; s < 2; ++s) {
+                if (!((wL >> s) & 1)) continue;
+                // the block of parity s that ends at or before FL (or holds FL-1 at the tail)
+                int b = (FL - 1) >> 5;
+                if ((b & 1) != s) --b;
+                const int j = 32 * b + lane;
+                if (j >= W) continue;
+                const uint32_t own = sm.stage[s][L][lane];
+                const uint32_t k = own & 0xffffu, nr = own >> 16;
+                const bool inf = nr == kNoRow;
+                const uint32_t av = giL > nr ? giL - nr : nr - giL;
+                const int dj = j - (int)k;
+                const uint32_t d = inf ? (uint32_t)DFC_INF_I32 : av * av + (uint32_t)(dj * dj);
+                if (OUTS & kOutD) __stcs(reinterpret_cast<int32_t*>(Db) + j, (int32_t)d);
+                if (OUTS & kOutS) __stcs(reinterpret_cast<float*>(Sb) + j, dist_f32(d));
+                if (OUTS & kOutL) __stcs(reinterpret_cast<int32_t*>(Lb) + j, inf ? -1 : (int32_t)(nr * (uint32_t)W + k));
+                if (OUTS & kOutN) __stcs(reinterpret_cast<int32_t*>(Nb) + j, inf ? -1 : (int32_t)k);
+            }
+        }
+        pend = 0;
+    };
+
+    // emit final columns F.. (bounded by m1 unless force); stops when the next
+    // staging slot still holds an unflushed block
     auto finalize = [&](int m1, bool force) {
-        while (F < W && cnt > 0 && (force || F < m1)) {
-            while (cnt >= 2 && bend <= F) {  // the bottom owns only final columns
-                head = (head + 1) & (kSCap - 1);
-                --cnt;
-                load_bottom();
+        for (;;) {
+            bool blocked = false;
+            while (!dead && F < W && (force || F < m1)) {
+                uint32_t own;
+                if (cnt == 0) {
+                    if (!force) break;  // no parabola yet: a later column will own these
+                    own = kEmpty;       // end of a featureless row
+                } else {
+                    while (cnt >= 2 && bend <= F) {  // the bottom owns only final columns
+                        head = (head + 1) & (kSCap - 1);
+                        --cnt;
+                        load_bottom();
+                    }
+                    if (!force) {
+                        const uint32_t d = bg + (uint32_t)((F - bk) * (F - bk));
+                        const uint32_t lim = (uint32_t)((m1 - F) * (m1 - F));
+                        if (TAKE_NEW ? d >= lim : d > lim) break;
+                    }
+                    own = (uint32_t)bk | (bnr << 16);
+                }
+                const int s = (F >> 5) & 1;
+                if ((pend >> s) & 1) { blocked = true; break; }
+                sm.stage[s][lane][F & 31] = own;
+                ++F;
+                if ((F & 31) == 0) pend |= 1u << s;
             }
-            const uint32_t d = bg + (uint32_t)((F - bk) * (F - bk));
-            if (!force) {
-                const uint32_t lim = (uint32_t)((m1 - F) * (m1 - F));
-                if (TAKE_NEW ? d >= lim : d > lim) break;
-            }
-            emit(F, d, (uint32_t)bk, bnr, false);
-            ++F;
+            if (__any_sync(0xffffffffu, pend != 0)) flush(false);
+            if (!__any_sync(0xffffffffu, blocked)) break;
         }
     };
 
@@ -155,9 +182,8 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
         if (c0 + kSTile < W) prefetch(c0 + kSTile);
         const int c1 = min(c0 + kSTile, W);
         for (int m = c0; m < c1; ++m) {
-            if (dead) continue;
             const uint32_t r = sm.tile[lane * kSTileStride + (m - c0)];
-            if (r != kNoRow) {
+            if (!dead && r != kNoRow) {
                 const uint32_t am = gi > r ? gi - r : r - gi;
                 const int gm = (int)(am * am);
                 int start = -2;  // -2: stack empty -> owns from F
@@ -186,37 +212,38 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
                     break;
                 }
                 if (start != -1) {
-                    if (start == -2 || start < F) start = F;
-                    if (cnt == kSCap) {  // ring full: hand the row to the fallback kernel
+                    if (start < F) start = F;  // (also the empty-stack case, -2)
+                    if (cnt == kSCap) {        // ring full: the fallback kernel redoes the row
                         dead = true;
                         fail_rows[atomicAdd(fail_count, 1)] = (int)row;
-                        continue;
+                    } else {
+                        ent(cnt) = make_uint2((uint32_t)m | ((uint32_t)start << 16), r);
+                        ++cnt;
+                        tk = m;
+                        ts = start;
+                        tg = (uint32_t)gm;
+                        if (cnt == 1) load_bottom();
+                        else if (cnt == 2) bend = start;
                     }
-                    ent(cnt) = make_uint2((uint32_t)m | ((uint32_t)start << 16), r);
-                    ++cnt;
-                    tk = m;
-                    ts = start;
-                    tg = (uint32_t)gm;
-                    if (cnt == 1) load_bottom();
-                    else if (cnt == 2) bend = start;
                 }
                 if (cnt == 1) bend = W;
             }
             finalize(m + 1, false);
         }
     }
-    if (!dead) {
-        if (cnt == 0) {  // featureless image: no finite parabola anywhere in the row
-            for (int j = 0; j < W; ++j) emit(j, 0u, 0u, 0u, true);
-        } else {
-            finalize(W, true);  // no later columns: everything left is final
-        }
-    }
+    finalize(W, true);  // no later columns: everything left is final
+    flush(true);
 }
 
 template <bool TAKE_NEW>
-inline const void* stream_kernel_ptr() {
-    return (const void*)k_rows_stream<TAKE_NEW>;
+inline const void* stream_kernel_ptr(int outs) {
+    switch (outs) {
+#define DFC_S(o) case o: return (const void*)k_rows_stream<TAKE_NEW, o>;
+        DFC_S(1) DFC_S(2) DFC_S(3) DFC_S(4) DFC_S(5) DFC_S(6) DFC_S(7) DFC_S(8)
+        DFC_S(9) DFC_S(10) DFC_S(11) DFC_S(12) DFC_S(13) DFC_S(14) DFC_S(15)
+#undef DFC_S
+        default: return nullptr;
+    }
 }
 
 inline int stream_smem_bytes() { return kSWarps * (int)sizeof(StreamSmem); }

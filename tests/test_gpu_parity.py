@@ -269,3 +269,44 @@ def test_sharded_driver_single_rank(dfc):
     torch.cuda.synchronize()
     assert (r0, r1) == (0, 64)
     np.testing.assert_array_equal(sq.cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+
+
+@pytest.fixture
+def stream_kernel(dfc):
+    dfc.set_row_kernel("stream")
+    yield dfc
+    dfc.set_row_kernel("default")
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (33, 97), (64, 64), (40, 1031), (70, 600), (3, 4100), (100, 33)])
+@pytest.mark.parametrize("density", [0.0, 0.002, 0.02, 0.3, 1.0])
+def test_streaming_row_kernel(stream_kernel, shape, density):
+    """The lane-per-row streaming stage 2 gives the same maps, labels, columns."""
+    img = oracle.random_image(shape[0], shape[1], density, 31 * shape[0] + shape[1] + int(density * 1000))
+    _check_edt(stream_kernel, img)
+
+
+def test_streaming_overflow_falls_back(stream_kernel):
+    """A horizontal object line far above equal-height parabolas keeps ~i entries
+    alive per row: rows beyond the ring capacity must be recomputed exactly."""
+    img = np.zeros((300, 257), np.uint8)
+    img[0, :] = 1
+    img[299, 100] = 1
+    _check_edt(stream_kernel, img)
+    img2 = np.zeros((200, 512), np.uint8)
+    img2[0, ::2] = 1
+    _check_edt(stream_kernel, img2)
+
+
+def test_streaming_batched_and_dual(stream_kernel):
+    from paper_2106_03503_b200 import workloads
+    imgs = workloads.points_batch(40, 96, 128, 30, 5)
+    out = stream_kernel.edt_batched(_dev(imgs), dist=True, label=True)
+    img = workloads.discs(256, 384, 10, 3)
+    dual = stream_kernel.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    for b in range(0, 40, 7):
+        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
+        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
+    np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+    np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
