@@ -87,7 +87,7 @@ RowGeom row_geom(int W) {
     static int target = [] {
         const char* e = getenv("DFC_ROW_L");
         const int v = e ? atoi(e) : 0;
-        return (v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128) ? v : 128;
+        return (v == 4 || v == 8 || v == 16 || v == 32 || v == 64 || v == 128) ? v : 32;
     }();
     RowGeom g;
     g.T = 32;
