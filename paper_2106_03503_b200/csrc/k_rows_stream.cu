@@ -28,10 +28,12 @@
 
 namespace dfc {
 
-constexpr int kSCap = 32;          // live-stack ring entries per lane
+constexpr int kSCap = 64;          // live-stack ring entries per lane
+constexpr int kSEmit = 4;          // columns a lane may emit per scanned column (bounds the
+                                   // lockstep cost of catch-up bursts; the backlog drains)
 constexpr int kSTile = 32;         // columns per staged input tile
 constexpr int kSTileStride = 34;   // halfwords per staged row (17 words: conflict-free)
-constexpr int kSWarps = 4;         // warps (bands of 32 rows) per CTA
+constexpr int kSWarps = 2;         // warps (bands of 32 rows) per CTA
 constexpr uint32_t kEmpty = 0xFFFF0000u;  // staged owner of a featureless row
 
 enum : int { kOutD = 1, kOutS = 2, kOutL = 4, kOutN = 8 };
@@ -145,7 +147,8 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
     auto finalize = [&](int m1, bool force) {
         for (;;) {
             bool blocked = false;
-            while (!dead && F < W && (force || F < m1)) {
+            int budget = force ? W : kSEmit;
+            while (!dead && F < W && (force || F < m1) && budget-- > 0) {
                 uint32_t own;
                 if (cnt == 0) {
                     if (!force) break;  // no parabola yet: a later column will own these

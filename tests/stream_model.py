@@ -14,7 +14,7 @@ Test infrastructure only: mirrors paper_2106_03503_b200/csrc/k_rows_stream.cu.
 """
 
 
-def stream_row(g, take_new=False, cap=None):
+def stream_row(g, take_new=False, cap=None, emit_cap=None):
     """g: list of squared vertical values or None.  Returns (runs, max_live) where
     runs = [(start_col, k)] ; k = None for a featureless row.  Raises
     OverflowError if the live stack would exceed cap."""
@@ -30,7 +30,9 @@ def stream_row(g, take_new=False, cap=None):
 
     def finalize(m):
         nonlocal F
-        while F <= m and st:
+        budget = emit_cap if emit_cap is not None else 1 << 30
+        while F <= m and st and budget > 0:
+            budget -= 1
             # drop entries whose range ended at or before F
             while len(st) > 1 and st[1][1] <= F:
                 st.pop(0)

@@ -17,9 +17,11 @@ def test_stream_model_matches_bruteforce(seed):
         H = rnd.randint(1, 300)
         g = [rnd.randint(0, H) ** 2 if rnd.random() < dens else None for _ in range(W)]
         for tn in (False, True):
-            runs, live = stream_row(g, tn)
-            worst = max(worst, live)
-            assert expand(runs, g, W) == brute(g, tn), (W, tn, g)
+            want = brute(g, tn)
+            for cap in (None, 4, 1):
+                runs, live = stream_row(g, tn, emit_cap=cap)
+                worst = max(worst, live)
+                assert expand(runs, g, W) == want, (W, tn, cap, g)
 
 
 def test_stream_model_ties():
