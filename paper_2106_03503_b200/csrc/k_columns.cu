@@ -86,48 +86,47 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
     }
 }
 
-// K1b: one thread per (column, slot*image); in place: last[b] becomes the
-// nearest object row ABOVE band b, first[b] the nearest object row BELOW it.
-__global__ void k_band_scan(int W, int Wp, int nb, int64_t n_planes, uint16_t* __restrict__ first,
-                            uint16_t* __restrict__ last) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// K1b: per column, in place: last[b] becomes the nearest object row ABOVE band
+// b (exclusive prefix-max over bands: rows grow with the band index, kNoRow =
+// absent), first[b] the nearest object row BELOW it (exclusive suffix-min).
+// CTA = 32 columns x nc band chunks (nc <= 32); a thread scans its chunk
+// twice (aggregate, then carry-in + write) -- coalesced across the columns,
+// and parallel over the chunks instead of a serial walk over all bands.
+__global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64_t n_planes,
+                                                    uint16_t* __restrict__ first, uint16_t* __restrict__ last) {
+    __shared__ int agg_last[32][33];
+    __shared__ int agg_first[32][33];
+    const int cx = threadIdx.x & 31, ch = threadIdx.x >> 5, nc = blockDim.x >> 5;
+    const int j = blockIdx.x * 32 + cx;
     const int64_t plane = blockIdx.y;
-    if (j >= W || plane >= n_planes) return;
+    const int per = (nb + nc - 1) / nc;
+    const int b0 = ch * per, b1 = min(b0 + per, nb);
     uint16_t* F = first + plane * nb * (int64_t)Wp + j;
     uint16_t* Lp = last + plane * nb * (int64_t)Wp + j;
-    uint16_t run = kNoRow;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {  // 4 independent loads in flight
-        uint16_t t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t[u] = Lp[(int64_t)(b + u) * Wp];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            Lp[(int64_t)(b + u) * Wp] = run;
-            if (t[u] != kNoRow) run = t[u];
+    const bool ok = j < W && plane < n_planes;
+    int mx = -1, mn = 0x10000;
+    if (ok)
+        for (int b = b0; b < b1; ++b) {
+            const int l = Lp[(int64_t)b * Wp], f = F[(int64_t)b * Wp];
+            if (l != kNoRow) mx = l;                 // rows increase with b: latest = max
+            if (f != kNoRow && mn == 0x10000) mn = f;  // earliest in the chunk = min
         }
+    agg_last[ch][cx] = mx;
+    agg_first[ch][cx] = mn;
+    __syncthreads();
+    if (!ok) return;
+    int above = -1, below = 0x10000;
+    for (int c = 0; c < ch; ++c) above = max(above, agg_last[c][cx]);
+    for (int c = nc - 1; c > ch; --c) below = min(below, agg_first[c][cx]);
+    for (int b = b0; b < b1; ++b) {  // exclusive prefix max
+        const int l = Lp[(int64_t)b * Wp];
+        Lp[(int64_t)b * Wp] = above < 0 ? kNoRow : (uint16_t)above;
+        if (l != kNoRow) above = l;
     }
-    for (; b < nb; ++b) {
-        const uint16_t t = Lp[(int64_t)b * Wp];
-        Lp[(int64_t)b * Wp] = run;
-        if (t != kNoRow) run = t;
-    }
-    run = kNoRow;
-    b = nb - 1;
-    for (; b - 3 >= 0; b -= 4) {
-        uint16_t t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t[u] = F[(int64_t)(b - u) * Wp];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            F[(int64_t)(b - u) * Wp] = run;
-            if (t[u] != kNoRow) run = t[u];
-        }
-    }
-    for (; b >= 0; --b) {
-        const uint16_t t = F[(int64_t)b * Wp];
-        F[(int64_t)b * Wp] = run;
-        if (t != kNoRow) run = t;
+    for (int b = b1 - 1; b >= b0; --b) {  // exclusive suffix min
+        const int f = F[(int64_t)b * Wp];
+        F[(int64_t)b * Wp] = below == 0x10000 ? kNoRow : (uint16_t)below;
+        if (f != kNoRow) below = f;
     }
 }
 
@@ -156,7 +155,7 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
         uint32_t mk[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) mk[c] = pol_mask(m[c], pol, valid);
-        for (int r = 0; r < nrows; ++r) {
+        auto row_out = [&](int r) {
             const uint32_t i = r0 + r;
             uint32_t out[4];
 #pragma unroll
@@ -182,6 +181,12 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
                     row[j0 + c] = (int32_t)d;
                 }
             }
+        };
+        if (nrows == kBand) {  // full band: fully unrolled (masks, shifts constant-folded)
+#pragma unroll
+            for (int r = 0; r < kBand; ++r) row_out(r);
+        } else {
+            for (int r = 0; r < nrows; ++r) row_out(r);
         }
     }
 }
