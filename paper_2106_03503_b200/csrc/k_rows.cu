@@ -323,7 +323,8 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         if (G > 32) __syncthreads();  // every warp's cuts of the previous level
         if (q < 32) {                 // warp-uniform: whole warps probe or not
             const int c = min((gb + half) * L, W - 1);
-            const float rP1 = 1.0f / (float)(P + 1), rPm1 = P > 2 ? 1.0f / (float)(P - 1) : 0.f;
+            const float rP1 = 1.0f / (float)(P + 1);
+            const float rPm1 = P >= 4 ? 1.0f / (float)(P - 3) : P > 2 ? 1.0f / (float)(P - 1) : 0.f;
             int lo = 0, hi = W;
             // a side without any finite parabola decides the merge at once
             bool hasA, hasB;
@@ -342,7 +343,14 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
             while (__any_sync(0xffffffffu, active && hi > lo)) {
                 const int n = hi - lo;
                 int p;
-                if (first) p = q < 2 ? c - 1 + q : lo + __float2int_rz((float)((q - 1) * n) * rPm1);
+                if (first) {
+                    // c-1, c (dense rows take over at B's first column), both ends
+                    // (sparse rows: one side often owns everything), uniform rest
+                    if (q < 2) p = c - 1 + q;
+                    else if (P >= 4 && q == 2) p = 0;
+                    else if (P >= 4 && q == P - 1) p = W - 1;
+                    else p = lo + __float2int_rz((float)((q - (P >= 4 ? 2 : 1)) * n) * rPm1);
+                }
                 else p = lo + __float2int_rz((float)((q + 1) * n) * rP1);
                 p = min(max(p, lo), hi - 1);
                 const bool live = active && hi > lo;

@@ -193,8 +193,12 @@ class Row:
                 for q in range(P):
                     if q < 2:
                         p = c - 1 + q
+                    elif P >= 4 and q == 2:
+                        p = 0
+                    elif P >= 4 and q == P - 1:
+                        p = W - 1
                     else:
-                        p = lo + ((q - 1) * n) // (P - 1)
+                        p = lo + ((q - (2 if P >= 4 else 1)) * n) // (P - 3 if P >= 4 else P - 1)
                     ps.append(p)
                 ps.sort()
             else:
