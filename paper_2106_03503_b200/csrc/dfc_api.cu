@@ -125,9 +125,14 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
     k_band_summary<<<grid, tpb, 0, st>>>(c, first, last);
-    const int nc = std::max(1, std::min(32, c.nb / 4));  // band chunks (>= 4 bands) per column
-    dim3 gs((unsigned)((W + 31) / 32), (unsigned)(npol * n));
-    k_band_scan<<<gs, 32 * nc, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
+    if (c.nb <= 64) {  // short columns: serial over bands, one thread per column
+        dim3 gs((unsigned)((W + 255) / 256), (unsigned)(npol * n));
+        k_band_scan_serial<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
+    } else {           // tall columns: chunks of bands scanned in parallel
+        const int nc = std::min(32, c.nb / 4);
+        dim3 gs((unsigned)((W + 31) / 32), (unsigned)(npol * n));
+        k_band_scan<<<gs, 32 * nc, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
+    }
     if (vsq)
         k_band_fill<true><<<grid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
     else

@@ -86,6 +86,52 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
     }
 }
 
+// K1b (short columns, <= 64 bands): one thread per (column, plane), serial
+// over the bands with 4 independent loads in flight; same in-place result as
+// the chunked scan below.
+__global__ void k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint16_t* __restrict__ first,
+                                   uint16_t* __restrict__ last) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t plane = blockIdx.y;
+    if (j >= W || plane >= n_planes) return;
+    uint16_t* F = first + plane * nb * (int64_t)Wp + j;
+    uint16_t* Lp = last + plane * nb * (int64_t)Wp + j;
+    uint16_t run = kNoRow;
+    int b = 0;
+    for (; b + 4 <= nb; b += 4) {
+        uint16_t t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = Lp[(int64_t)(b + u) * Wp];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            Lp[(int64_t)(b + u) * Wp] = run;
+            if (t[u] != kNoRow) run = t[u];
+        }
+    }
+    for (; b < nb; ++b) {
+        const uint16_t t = Lp[(int64_t)b * Wp];
+        Lp[(int64_t)b * Wp] = run;
+        if (t != kNoRow) run = t;
+    }
+    run = kNoRow;
+    b = nb - 1;
+    for (; b - 3 >= 0; b -= 4) {
+        uint16_t t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = F[(int64_t)(b - u) * Wp];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            F[(int64_t)(b - u) * Wp] = run;
+            if (t[u] != kNoRow) run = t[u];
+        }
+    }
+    for (; b >= 0; --b) {
+        const uint16_t t = F[(int64_t)b * Wp];
+        F[(int64_t)b * Wp] = run;
+        if (t != kNoRow) run = t;
+    }
+}
+
 // K1b: per column, in place: last[b] becomes the nearest object row ABOVE band
 // b (exclusive prefix-max over bands: rows grow with the band index, kNoRow =
 // absent), first[b] the nearest object row BELOW it (exclusive suffix-min).
