@@ -192,6 +192,16 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
             };
             load_m();
             while (m < c1) {
+                if (gm == 0 && n > 0 && tg == 0 && tk == m - 1) {
+                    // run of object pixels: the new zero parabola starts exactly at m
+                    // and pops nothing (num = 2m-1 > 2*ts, start = m, push since m < W)
+                    st[n++] = (uint32_t)m | ((uint32_t)m << 16);
+                    tk = m;
+                    ts = m;
+                    ++m;
+                    load_m();
+                    continue;
+                }
                 bool consume = true;
                 int num = 0;
                 uint32_t den = 1;
@@ -405,7 +415,7 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     int32_t* Lrow = a.LB ? reinterpret_cast<int32_t*>(a.LB + img * a.sL) + (int64_t)i * W : nullptr;
     int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + img * a.sN) + (int64_t)i * W : nullptr;
 
-    auto cell = [&](int j, int32_t& d, int32_t& lab, int32_t& col) {
+    auto cell = [&](int j, int32_t& d, uint32_t& kk, uint32_t& rk) {
         if (j >= seg_end) {
             while (sg + 1 < T && cut[sg + 1] <= j) ++sg;
             seg_end = sg + 1 < T ? cut[sg + 1] : W;
@@ -417,40 +427,50 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
             ++e;
             load_entry();
         }
+        kk = k;
+        rk = rr;
         if (gk == kInfU) {
-            d = DFC_INF_I32; lab = -1; col = -1;
+            d = DFC_INF_I32;
         } else {
             const int dj = j - (int)k;
             d = (int32_t)(gk + (uint32_t)(dj * dj));
-            lab = (int32_t)(rr * (uint32_t)W + k);
-            col = (int32_t)k;
         }
     };
+    auto lab_of = [&](int32_t d, uint32_t kk, uint32_t rk) -> int32_t {
+        return d == DFC_INF_I32 ? -1 : (int32_t)(rk * (uint32_t)W + kk);
+    };
+    auto col_of = [&](int32_t d, uint32_t kk) -> int32_t { return d == DFC_INF_I32 ? -1 : (int32_t)kk; };
 
     if (a.vec) {
         for (int j = c0; j < c1; j += 4) {
-            int4 d4, l4, n4;
-            cell(j + 0, d4.x, l4.x, n4.x);
-            cell(j + 1, d4.y, l4.y, n4.y);
-            cell(j + 2, d4.z, l4.z, n4.z);
-            cell(j + 3, d4.w, l4.w, n4.w);
+            int4 d4;
+            uint32_t k0, k1, k2, k3, r0, r1, r2, r3;
+            cell(j + 0, d4.x, k0, r0);
+            cell(j + 1, d4.y, k1, r1);
+            cell(j + 2, d4.z, k2, r2);
+            cell(j + 3, d4.w, k3, r3);
             if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), d4);
             if (Srow) {
                 const float4 f4 = make_float4(dist_f32(d4.x), dist_f32(d4.y), dist_f32(d4.z),
                                               dist_f32(d4.w));
                 __stcs(reinterpret_cast<float4*>(Srow + j), f4);
             }
-            if (Lrow) __stcs(reinterpret_cast<int4*>(Lrow + j), l4);
-            if (Nrow) __stcs(reinterpret_cast<int4*>(Nrow + j), n4);
+            if (Lrow)
+                __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab_of(d4.x, k0, r0), lab_of(d4.y, k1, r1),
+                                                                   lab_of(d4.z, k2, r2), lab_of(d4.w, k3, r3)));
+            if (Nrow)
+                __stcs(reinterpret_cast<int4*>(Nrow + j),
+                       make_int4(col_of(d4.x, k0), col_of(d4.y, k1), col_of(d4.z, k2), col_of(d4.w, k3)));
         }
     } else {
         for (int j = c0; j < c1; ++j) {
-            int32_t d, lab, col;
-            cell(j, d, lab, col);
+            int32_t d;
+            uint32_t kk, rk;
+            cell(j, d, kk, rk);
             if (Drow) Drow[j] = d;
             if (Srow) Srow[j] = dist_f32((uint32_t)d);
-            if (Lrow) Lrow[j] = lab;
-            if (Nrow) Nrow[j] = col;
+            if (Lrow) Lrow[j] = lab_of(d, kk, rk);
+            if (Nrow) Nrow[j] = col_of(d, kk);
         }
     }
 }
