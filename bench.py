@@ -55,6 +55,16 @@ CONFIGS = {
 }
 
 
+def traffic_for(cfg):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(cfg)
+        return (t["dram_bytes_per_launch"], t["source"]) if t else (None, None)
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -293,7 +303,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {
             "bound": "hbm", "kernel": "k_rows (row envelope)" if cfg != "c4" else "k_band_* + k_raster (whole step)",
             "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
+            "frac": round(achieved / peak, 4), "traffic": traffic_for(cfg)[0],
+            "traffic_source": traffic_for(cfg)[1], "algorithmic_bytes_per_launch": kernel_bytes,
             "bytes_per_px": c["bytes_kernel"], "kernel_ms": round(row_ms, 5),
             "step": {"bytes_alg_per_px": c["bytes_alg"], "achieved": round(step_achieved, 1),
                      "frac": round(step_achieved / peak, 4)},
