@@ -25,7 +25,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdfc.so")
+LIB_PATH = os.environ.get("DFC_LIB") or os.path.join(HERE, "lib", "libdfc.so")  # DFC_LIB: A/B builds
 INF_I32 = 0x7FFFFFFF
 
 if not os.path.exists(LIB_PATH):

@@ -186,10 +186,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             out_vec_ok(NC, sN);
     a.row_list = nullptr;
     a.row_count = nullptr;
-    // rows per slot processed in sequence (merge probes start at the previous
-    // row's takeover columns); keep >= ~600 CTAs for the 148 SMs
-    a.n_seq = (int)std::max<int64_t>(1, std::min<int64_t>(16, a.total_rows / ((int64_t)g.R * 600)));
-    const int64_t blocks = (a.total_rows + (int64_t)g.R * a.n_seq - 1) / ((int64_t)g.R * a.n_seq);
+    const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
@@ -222,7 +219,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         fb.row_list = fail_rows;
         fb.row_count = fail_count;
         void* fargs[] = {&fb};
-        const int64_t fblocks = std::min<int64_t>((a.total_rows + g.R - 1) / g.R, 148 * 4);
+        const int64_t fblocks = std::min<int64_t>(blocks, 148 * 4);
         e = cudaLaunchKernel(fn, dim3((unsigned)fblocks), dim3(g.R * g.T), fargs, (size_t)g.smem_bytes, st);
         if (e != cudaSuccess) return cuda_fail(e);
     } else {

@@ -27,7 +27,6 @@ struct RowArgs {
     int H, W;
     int64_t total_rows;       // n_img * H
     int T, L, R;              // threads per row, columns per thread, rows per CTA
-    int n_seq;                // consecutive rows each row slot processes (k_rows)
     int row_smem_words;       // 32-bit words of shared memory per row
     // outputs (nullable); image b's plane at base + b * stride (bytes)
     char* D;  int64_t sD;

@@ -108,47 +108,36 @@ struct RowCtx {
 };
 
 template <int L, bool TAKE_NEW>
-__device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool active, bool use_prev);
+__device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp);
 
 template <int L, bool TAKE_NEW>
 __global__ void __launch_bounds__(1024) k_rows(RowArgs a) {
-    const int rho = threadIdx.x / a.T;
     if (a.row_list == nullptr) {
-        // Each row slot of the CTA processes n_seq CONSECUTIVE rows: the merge
-        // takeover columns of adjacent rows are close (median |dx| <= 1 on
-        // config 2), so round 0 of every merge probes around the previous
-        // row's answer.
-        const int64_t first = ((int64_t)blockIdx.x * a.R + rho) * a.n_seq;
-        bool prev_dense = false;
-        for (int t = 0; t < a.n_seq; ++t) {
-            const int64_t row = first + t;
-            const bool active = row < a.total_rows;
-            const bool same_img = t > 0 && active && row / a.H == (row - 1) / a.H;
-            prev_dense = rows_group<L, TAKE_NEW>(a, row, active, prev_dense && same_img);
-            __syncthreads();
-        }
+        rows_group<L, TAKE_NEW>(a, blockIdx.x);
         return;
     }
     // fallback mode (rows the streaming kernel could not hold): grid-stride
     // over the listed rows; the trip count is uniform per CTA
     const int64_t n = *a.row_count;
     for (int64_t grp = blockIdx.x; grp * a.R < n; grp += gridDim.x) {
-        const int64_t r = grp * a.R + rho;
-        const bool active = r < n;
-        rows_group<L, TAKE_NEW>(a, active ? a.row_list[r] : 0, active, false);
+        rows_group<L, TAKE_NEW>(a, grp);
         __syncthreads();
     }
 }
 
-// One row per slot of the CTA.  Returns whether the dense (merge tree) path ran
-// (CTA-uniform), i.e. whether this row's takeover columns are in xprev.
 template <int L, bool TAKE_NEW>
-__device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool active, bool use_prev) {
+__device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     using LY = RowLayout<L>;
     extern __shared__ uint32_t smem[];
     const int T = a.T;
-    const int rho = threadIdx.x / T;          // row slot within the CTA
+    const int rho = threadIdx.x / T;          // row within the CTA
     const int s = threadIdx.x - rho * T;      // segment (thread) within the row
+    int64_t row = grp * a.R + rho;
+    bool active = row < a.total_rows;
+    if (a.row_list) {
+        active = row < *a.row_count;
+        row = active ? a.row_list[row] : 0;
+    }
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // g = (gi - nr)^2, global row
@@ -162,7 +151,6 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
     int* xs = cnt + T;                                            // [T/32] per warp: takeover / census
     int* nzw = xs + (T >> 5);                                     // [T/32] warp has candidates
     uint32_t* cmp = reinterpret_cast<uint32_t*>(nzw + (T >> 5));  // [kCompact+2] compact envelope
-    int* xprev = reinterpret_cast<int*>(cmp + kCompact + 2);      // [T] previous row's takeovers (heap)
 
     // ---- 0. stage the row's nearest-row values (coalesced 4-byte loads) ----
     if (active) {
@@ -282,7 +270,6 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
     }
 
     // (CTA-uniform choice: rows sharing a CTA must run the same barriers)
-    bool dense = true;
     if (__syncthreads_and(tot <= kCompact)) {
         // ---- 2'. sparse row: one lane runs the reference stack algorithm
         // (exact_edt.cpp:208-223) over the surviving candidates of all
@@ -329,7 +316,6 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
         if (T > 32) __syncthreads(); else __syncwarp();
         if (active && s > 0) cut[s] = W;   // segment 0 owns the whole row
         __syncthreads();
-        dense = false;
     } else {
     // ---- 2. merge adjacent segment groups: P-ary probe search ----
     // The P = min(G, 32) lanes of a merge evaluate "B beats A" at P columns
@@ -364,18 +350,10 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
             if (!hasB) lo = hi = W;
             else if (!hasA) lo = hi = 0;
             bool first = true;
-            const int hp = T / G - 1 + gb / G;  // heap slot of this merge
-            const int xp = use_prev ? xprev[hp] : 0;
             while (__any_sync(0xffffffffu, active && hi > lo)) {
                 const int n = hi - lo;
                 int p;
-                if (first && use_prev) {
-                    // exponentially spaced around the previous row's takeover:
-                    // ..., -4, -2, -1, 0, +1, +3, +7, ...
-                    const int h = P >> 1;
-                    p = q == h - 1 ? xp - 1 : q == h ? xp
-                        : q > h ? xp + (1 << (q - h)) - 1 : xp - (1 << (h - 1 - q));
-                } else if (first) {
+                if (first) {
                     // c-1, c (dense rows take over at B's first column), both ends
                     // (sparse rows: one side often owns everything), uniform rest
                     if (q < 2) p = c - 1 + q;
@@ -400,7 +378,6 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
                 first = false;
             }
             if (G > 32 && q == 0) xs[gb >> 5] = lo;
-            if (q == 0 && active) xprev[hp] = lo;
             if (G <= 32 && active) cut[s] = q >= half ? max(cut[s], lo) : min(cut[s], lo);
         }
         if (G > 32) {
@@ -413,9 +390,9 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
     }  // dense row
 
     // ---- 3. fill this thread's columns ----
-    if (!active) return dense;
+    if (!active) return;
     const int c0 = s * L, c1 = min(c0 + L, W);
-    if (c0 >= W) return dense;
+    if (c0 >= W) return;
     int sg = cx.owner(0, T, c0);
     int seg_end = sg + 1 < T ? cut[sg + 1] : W;
     int n = cnt[sg];
@@ -496,12 +473,11 @@ __device__ __forceinline__ bool rows_group(const RowArgs& a, int64_t row, bool a
             if (Nrow) Nrow[j] = col_of(d, kk);
         }
     }
-    return dense;
 }
 
 // Row-pass words of shared memory per row for a given (T, L).
 inline int row_words(int T, int L) {
-    return (T * (L + 2)) / 2 + T * (L + 1) + 3 * T + 2 * (T >> 5) + kCompact + 2;  // ... cut, cnt, xprev
+    return (T * (L + 2)) / 2 + T * (L + 1) + 2 * T + 2 * (T >> 5) + kCompact + 2;  // nrs, stacks, cut, cnt, ...
 }
 
 // Host-side dispatch over the compile-time segment length.
