@@ -188,7 +188,6 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.row_list = nullptr;
     a.row_count = nullptr;
     a.dens = dens;
-    a.zs_skip_dense = false;
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
@@ -215,15 +214,9 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         e = cudaFuncSetAttribute(zfn, cudaFuncAttributeMaxDynamicSharedMemorySize, zsm);
         if (e != cudaSuccess) return cuda_fail(e);
         void* zargs[] = {&a, &fail_rows, &fail_count};
-        const int64_t zblocks = std::min<int64_t>(a.total_rows, 148 * 8);
-        e = cudaLaunchKernel(zfn, dim3((unsigned)zblocks), dim3(kZsThreads), zargs, (size_t)zsm, st);
+        e = cudaLaunchKernel(zfn, dim3((unsigned)a.total_rows), dim3(kZsThreads), zargs, (size_t)zsm, st);
         if (e != cudaSuccess) return cuda_fail(e);
-        RowArgs sp = a;  // the sparse planes, full launch (dense rows skipped)
-        sp.zs_skip_dense = true;
-        void* sargs[] = {&sp};
-        e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), sargs, (size_t)g.smem_bytes, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        g_launches += 2;
+        ++g_launches;
         RowArgs fb = a;
         fb.row_list = fail_rows;
         fb.row_count = fail_count;

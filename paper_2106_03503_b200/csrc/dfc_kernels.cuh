@@ -37,7 +37,6 @@ struct RowArgs {
     bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
     const int* row_list;      // fallback mode: process only these rows (nullptr: all)
     const uint32_t* dens;     // object pixels per plane (stage 1), nullptr: unknown
-    bool zs_skip_dense;       // k_rows: leave rows of dense planes to k_rows_zs
     const int* row_count;     // number of entries in row_list (device)
 };
 

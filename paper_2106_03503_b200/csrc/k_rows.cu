@@ -138,11 +138,6 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         active = row < *a.row_count;
         row = active ? a.row_list[row] : 0;
     }
-    // rows of dense planes belong to the zero-split kernel (k_rows_zs.cu) when
-    // it runs; in fallback mode we are given exactly the rows it handed back
-    if (active && a.zs_skip_dense && a.row_list == nullptr &&
-        (uint64_t)a.dens[row / a.H] * 2 > (uint64_t)a.H * (uint64_t)a.W)
-        active = false;
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // g = (gi - nr)^2, global row

@@ -25,34 +25,19 @@ namespace dfc {
 constexpr int kZsThreads = 256;
 constexpr int kZsGap = 256;   // longest gap (columns strictly between zeros) handled here
 
-// Dense plane: more than half of its pixels are objects of the polarity.
-__device__ __forceinline__ bool zs_dense_plane(const RowArgs& a, int img) {
-    return a.dens != nullptr && (uint64_t)a.dens[img] * 2 > (uint64_t)a.H * (uint64_t)a.W;
-}
-
-template <bool TAKE_NEW>
-__device__ __forceinline__ void zs_row(const RowArgs& a, int64_t row, int* fail_rows, int* fail_count);
-
 template <bool TAKE_NEW>
 __global__ void __launch_bounds__(kZsThreads) k_rows_zs(RowArgs a, int* fail_rows, int* fail_count) {
-    // grid-stride over the rows of DENSE planes; sparse planes are left to the
-    // segment kernel's own launch (it skips the dense ones)
-    for (int64_t row = blockIdx.x; row < a.total_rows; row += gridDim.x) {
-        const int img = (int)(row / a.H);
-        if (!zs_dense_plane(a, img)) {
-            row = ((int64_t)img + 1) * a.H - 1 - ((((int64_t)img + 1) * a.H - 1 - row) % gridDim.x);
-            continue;  // jump to this CTA's last row of the plane
-        }
-        zs_row<TAKE_NEW>(a, row, fail_rows, fail_count);
-        __syncthreads();
-    }
-}
-
-template <bool TAKE_NEW>
-__device__ __forceinline__ void zs_row(const RowArgs& a, int64_t row, int* fail_rows, int* fail_count) {
     extern __shared__ uint32_t zsm[];
     const int W = a.W;
+    const int64_t row = blockIdx.x;
+    if (row >= a.total_rows) return;
     const int img = (int)(row / a.H);
+    // sparse plane (objects of this polarity <= half the pixels): gaps are long,
+    // hand the row straight to the segment kernel
+    if ((uint64_t)a.dens[img] * 2 <= (uint64_t)a.H * (uint64_t)a.W) {
+        if (threadIdx.x == 0) fail_rows[atomicAdd(fail_count, 1)] = (int)row;
+        return;
+    }
     const uint32_t i = (uint32_t)(row - (int64_t)img * a.H);
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // zero column <=> nr == gi
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
