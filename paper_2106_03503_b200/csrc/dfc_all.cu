@@ -4,6 +4,5 @@
 #include "k_columns.cu"
 #include "k_rows.cu"
 #include "k_rows_stream.cu"
-#include "k_rows_zs.cu"
 #include "k_raster.cu"
 #include "dfc_api.cu"

@@ -109,7 +109,7 @@ RowGeom row_geom(int W) {
 // Stage 1 into a uint16 nearest-row plane [npol][n][H][Wp].
 int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
-                cudaStream_t st, int32_t* vsq = nullptr, uint32_t* dens = nullptr) {
+                cudaStream_t st, int32_t* vsq = nullptr) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -124,8 +124,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.vec = aligned(img, 4) && pitch % 4 == 0 && istride % 4 == 0;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
-    if (dens) cudaMemsetAsync(dens, 0, sizeof(uint32_t) * npol * n, st);
-    k_band_summary<<<grid, tpb, 0, st>>>(c, first, last, dens);
+    k_band_summary<<<grid, tpb, 0, st>>>(c, first, last);
     if (c.nb <= 64) {  // short columns: serial over bands, one thread per column
         dim3 gs((unsigned)((W + 255) / 256), (unsigned)(npol * n));
         k_band_scan_serial<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
@@ -158,7 +157,7 @@ bool out_vec_ok(const void* p, int64_t stride) {
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
              int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
              int64_t sN, cudaStream_t st, bool vdist = false, int tile_cols = 0,
-             int64_t tile_stride = 0, int row0 = 0, const uint32_t* dens = nullptr) {
+             int64_t tile_stride = 0, int row0 = 0) {
     const RowGeom g = row_geom((int)W);
     RowArgs a;
     a.nr = nr;
@@ -187,7 +186,6 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             out_vec_ok(NC, sN);
     a.row_list = nullptr;
     a.row_count = nullptr;
-    a.dens = dens;
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
@@ -197,36 +195,6 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     // Streaming kernel (one lane = one row) when the nr plane allows coalesced
     // 16-byte tile loads; rows whose live stack overflows go to k_rows.
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
-    // dense-row fast path (zero-split gaps) with the segment kernel for the
-    // rows it hands back; needs the per-plane object counts of stage 1
-    const bool zs_ok = mode == 1 && dens != nullptr && !vdist && W <= 8192 && aligned(nr, 4) &&
-                       a.tile_cols >= W && a.total_rows <= 0x7fffffff;
-    if (zs_ok) {
-        Scratch fl(st);
-        e = fl.alloc((size_t)(a.total_rows + 1) * sizeof(int));
-        if (e != cudaSuccess) return cuda_fail(e);
-        int* fail_count = static_cast<int*>(fl.p);
-        int* fail_rows = fail_count + 1;
-        e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        const void* zfn = take_new ? zs_kernel_ptr<true>() : zs_kernel_ptr<false>();
-        const int zsm = zs_smem_bytes((int)W);
-        e = cudaFuncSetAttribute(zfn, cudaFuncAttributeMaxDynamicSharedMemorySize, zsm);
-        if (e != cudaSuccess) return cuda_fail(e);
-        void* zargs[] = {&a, &fail_rows, &fail_count};
-        e = cudaLaunchKernel(zfn, dim3((unsigned)a.total_rows), dim3(kZsThreads), zargs, (size_t)zsm, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        ++g_launches;
-        RowArgs fb = a;
-        fb.row_list = fail_rows;
-        fb.row_count = fail_count;
-        void* fargs[] = {&fb};
-        const int64_t fblocks = std::min<int64_t>(blocks, 148 * 4);
-        e = cudaLaunchKernel(fn, dim3((unsigned)fblocks), dim3(g.R * g.T), fargs, (size_t)g.smem_bytes, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        ++g_launches;
-        return DFC_OK;
-    }
     const bool stream_ok = mode == 2 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
                            a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
     if (stream_ok) {
@@ -281,14 +249,13 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     const size_t carry_elems = (size_t)(planes * nb * Wp);
     const size_t nr_elems = (size_t)(planes * H * Wp);
     Scratch sc(st);
-    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 256 + planes * 4 + 16);
+    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 256);
     if (e != cudaSuccess) return cuda_fail(e);
     uint16_t* first = static_cast<uint16_t*>(sc.p);
     uint16_t* last = first + carry_elems;
     uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry_elems), 16));
-    uint32_t* dens = reinterpret_cast<uint32_t*>(round_up(reinterpret_cast<uintptr_t>(nr + nr_elems), 16));
     prof(0, st);
-    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, dens);
+    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -310,23 +277,21 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
         if (want_keep) {
             rc = row_pass(nr, nimg, H, W, Wp, false, o.D[0], stride_of(o.D[0], o.D[1]), o.S[0],
                           o.S[0] ? stride_of(o.S[0], o.S[1]) : 0, o.LB[0],
-                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st, false, 0, 0, 0, dens);
+                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st);
             if (rc != DFC_OK) return rc;
         }
         if (o.NC[0]) {
             rc = row_pass(nr, nimg, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[0],
-                          stride_of(o.NC[0], o.NC[1]), st, false, 0, 0, 0, dens);
+                          stride_of(o.NC[0], o.NC[1]), st);
             if (rc != DFC_OK) return rc;
         }
     } else {
         for (int s = 0; s < npol; ++s) {
             const uint16_t* pl = nr + (int64_t)s * H * Wp;
-            rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st, false, 0, 0,
-                          0, dens + s);
+            rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st);
             if (rc != DFC_OK) return rc;
             if (o.NC[s]) {
-                rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st, false, 0,
-                              0, 0, dens + s);
+                rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st);
                 if (rc != DFC_OK) return rc;
             }
         }

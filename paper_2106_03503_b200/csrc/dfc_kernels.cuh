@@ -36,7 +36,6 @@ struct RowArgs {
     bool vec;                 // 16-byte vector stores are legal
     bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
     const int* row_list;      // fallback mode: process only these rows (nullptr: all)
-    const uint32_t* dens;     // object pixels per plane (stage 1), nullptr: unknown
     const int* row_count;     // number of entries in row_list (device)
 };
 

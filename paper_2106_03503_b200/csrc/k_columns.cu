@@ -59,28 +59,18 @@ __device__ __forceinline__ uint32_t pol_mask(uint32_t m, int pol, uint32_t valid
 
 
 // K1a: grid (ceil(W/4)/blockDim, nb, n_img)
-__global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t* __restrict__ last,
-                               uint32_t* __restrict__ dens) {
+__global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t* __restrict__ last) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int j0 = 4 * g;
+    if (j0 >= a.W) return;
     const int b = blockIdx.y, im = blockIdx.z;
     const int r0 = b * kBand;
     const int nrows = min(kBand, a.H - r0);
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
-    uint32_t m[4] = {0u, 0u, 0u, 0u};
-    if (j0 < a.W)
-        band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    uint32_t m[4];
+    band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
-        if (dens) {  // object pixels of this polarity, per plane (warp-aggregated)
-            uint32_t cntp = 0;
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (j0 + c < a.W) cntp += __popc(pol_mask(m[c], pol, valid));
-            for (int o = 16; o > 0; o >>= 1) cntp += __shfl_xor_sync(0xffffffffu, cntp, o);
-            if ((threadIdx.x & 31) == 0 && cntp) atomicAdd(dens + s * a.n_img + im, cntp);
-        }
-        if (j0 >= a.W) continue;
         uint16_t f[4], l[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
