@@ -310,3 +310,32 @@ def test_streaming_batched_and_dual(stream_kernel):
         np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
     np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
     np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
+
+
+@pytest.mark.parametrize("gap", [1, 2, 17, 255, 256, 257, 600])
+def test_dense_rows_zero_split(dfc, gap):
+    """Dense planes (most pixels are objects) with gaps of many lengths, next to
+    objects at various vertical distances (non-trivial envelopes in the gaps)."""
+    rng = np.random.default_rng(gap)
+    H, W = 48, 1024
+    img = np.ones((H, W), np.uint8)
+    for i in range(H):
+        j0 = int(rng.integers(0, W - gap))
+        img[i, j0:j0 + gap] = 0
+        if i % 3 == 0:
+            img[max(0, i - 5):i + 5, j0 + gap // 3: j0 + gap // 2 + 1] = 0
+    img[:, :2] = 1
+    _check_edt(dfc, img)            # background -> object (dense objects)
+    _check_edt(dfc, (img == 0).astype(np.uint8), polarity=1)  # same plane via the inverted polarity
+
+
+def test_dense_rows_border_gaps_and_ties(dfc):
+    img = np.ones((40, 300), np.uint8)
+    img[:, :37] = 0        # gap at the left border
+    img[:, 250:] = 0       # gap at the right border
+    img[10:30, 100:140] = 0
+    img[::4, 120] = 1      # vertical ties inside the gap
+    _check_edt(dfc, img)
+    small = np.ones((6, 200), np.uint8)
+    small[2] = 0           # a full-width gap row (no zero at all in the row)
+    _check_edt(dfc, small)
