@@ -170,8 +170,10 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 /*
  * Stage-2 kernel selection for the calls of this thread: 0 = library
  * default, 1 = segment/merge kernel (k_rows), 2 = streaming lane-per-row
- * kernel (k_rows_stream, with k_rows as its overflow fallback).  Results are
- * identical; this is a performance/testing knob.
+ * kernel (k_rows_stream, with k_rows as its overflow fallback), 3 = window
+ * kernel (k_rows_win: per-segment stacks + bounded outward search, rows up to
+ * 16384 columns; wider rows use k_rows).  Results are identical; this is a
+ * performance/testing knob.
  */
 int dfc_set_row_kernel(int mode);
 

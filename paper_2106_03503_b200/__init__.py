@@ -87,8 +87,9 @@ def set_profile_events(col_begin=None, row_begin=None, row_end=None) -> None:
 
 
 def set_row_kernel(mode: str) -> None:
-    """Stage-2 kernel for this thread's calls: "default", "segment" or "stream"."""
-    _check(_lib.dfc_set_row_kernel({"default": 0, "segment": 1, "stream": 2}[mode]))
+    """Stage-2 kernel for this thread's calls: "default", "segment", "stream" or
+    "window" (k_rows_win.cu, rows up to 16384 columns)."""
+    _check(_lib.dfc_set_row_kernel({"default": 0, "segment": 1, "stream": 2, "window": 3}[mode]))
 
 
 def last_launch_count() -> int:

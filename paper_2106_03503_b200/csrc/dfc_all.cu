@@ -4,5 +4,6 @@
 #include "k_columns.cu"
 #include "k_rows.cu"
 #include "k_rows_stream.cu"
+#include "k_rows_win.cu"
 #include "k_raster.cu"
 #include "dfc_api.cu"

@@ -17,13 +17,14 @@ namespace {
 thread_local int g_last_cuda = 0;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
-thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming kernel
+thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming, 3: window
 
 // DFC_ROWS=segment|stream overrides the default stage-2 kernel (tuning/A-B).
 int env_row_mode() {
     static const int m = [] {
         const char* v = getenv("DFC_ROWS");
         if (v && strcmp(v, "stream") == 0) return 2;
+        if (v && strcmp(v, "win") == 0) return 3;
         return 1;  // default: the segment/merge kernel
     }();
     return m;
@@ -152,6 +153,42 @@ bool out_vec_ok(const void* p, int64_t stride) {
     return p == nullptr || (aligned(p, 16) && stride % 16 == 0);
 }
 
+// Window kernel (k_rows_win.cu): 32-column segments, a power-of-two count per
+// row; 256 threads per CTA, each row's segments spread over the CTA.
+int row_pass_win(RowArgs a, bool take_new, cudaStream_t st) {
+    constexpr int Lw = 32;
+    const int W = a.W;
+    WinLayout wl;
+    wl.nseg = 1;
+    while (wl.nseg * Lw < W) wl.nseg <<= 1;
+    wl.spt = 1;
+    wl.lg = 0;
+    while ((1 << wl.lg) < wl.nseg) ++wl.lg;
+    a.L = Lw;
+    a.R = std::max(1, 256 / wl.nseg);
+    a.T = std::min(wl.nseg, 256);
+    a.row_smem_words = win_row_words(wl.nseg, Lw);
+    a.vec_nr = aligned(a.nr, 16) && a.Wp % 8 == 0 && a.nr_img_stride % 8 == 0 &&
+               (a.tile_cols >= W || (a.tile_cols % Lw == 0 && a.tile_stride % 8 == 0));
+    int smem = a.R * a.row_smem_words * 4;
+    while (a.R > 1 && smem > 227 * 1024) {
+        a.R >>= 1;
+        smem = a.R * a.row_smem_words * 4;
+    }
+    if (smem > 227 * 1024) return DFC_ERR_SHAPE;
+    const int threads = std::min(256, std::max(32, a.R * wl.nseg));
+    const void* fn = take_new ? win_kernel_ptr<true>() : win_kernel_ptr<false>();
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int64_t blocks = (a.total_rows + a.R - 1) / a.R;
+    if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
+    void* args[] = {&a, &wl};
+    e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, (size_t)smem, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    ++g_launches;
+    return DFC_OK;
+}
+
 // Stage 2 over `nimg` planes of H rows.  Plane b writes its outputs at
 // base + b*stride.  take_new selects meijster_scan's tie rule.
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
@@ -186,6 +223,9 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             out_vec_ok(NC, sN);
     a.row_list = nullptr;
     a.row_count = nullptr;
+    a.vec_nr = false;
+    const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
+    if (mode == 3 && W <= 16384) return row_pass_win(a, take_new, st);
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
@@ -194,7 +234,6 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
 
     // Streaming kernel (one lane = one row) when the nr plane allows coalesced
     // 16-byte tile loads; rows whose live stack overflows go to k_rows.
-    const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
     const bool stream_ok = mode == 2 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
                            a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
     if (stream_ok) {
@@ -504,7 +543,7 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 }
 
 int dfc_set_row_kernel(int mode) {
-    if (mode < 0 || mode > 2) return DFC_ERR_ARG;
+    if (mode < 0 || mode > 3) return DFC_ERR_ARG;
     g_row_mode = mode;
     return DFC_OK;
 }

@@ -34,6 +34,7 @@ struct RowArgs {
     char* LB; int64_t sL;
     char* NC; int64_t sN;
     bool vec;                 // 16-byte vector stores are legal
+    bool vec_nr;              // 16-byte nr loads of a whole segment are legal (window kernel)
     bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
     const int* row_list;      // fallback mode: process only these rows (nullptr: all)
     const int* row_count;     // number of entries in row_list (device)

@@ -13,15 +13,18 @@
 //             whole domain [0, cols), as a stack of (column, start) entries;
 //  2. merge   log2(T) levels of pairwise merges of adjacent segment groups
 //             A < B.  E_A - E_B is strictly increasing in j (all columns of A
-//             are left of B's), so B takes over from A at ONE column x.  One
-//             leader thread per merge finds x by walking envelope "pieces"
-//             (a parabola together with the columns it owns in its group)
-//             outward from B's first column: inside the overlap of the
-//             current A piece and B piece the takeover column of the two
-//             parabolas is a closed-form integer expression, so each step
-//             either lands on x or discards one piece.  Dense rows finish in
-//             O(1) steps, sparse rows have few pieces.  Every segment keeps a
-//             "cut", the first column it may own inside its current group.
+//             are left of B's), so B takes over from A at ONE column x; every
+//             segment keeps a "cut", the first column it may own inside its
+//             current group.  The P = min(G, 32) lanes of a merge find x by a
+//             P-ary probe search: each round evaluates "B beats A" at P
+//             columns of the bracket [lo, hi] (the group envelope at a column
+//             is a binary search over cuts, then over that segment's stack).
+//             The bracket starts at (zl(A), zf(B)] -- A's last and B's first
+//             column with an object pixel on this row own themselves -- so on
+//             dense rows most merges need no probe; round 0 also probes c-1, c
+//             (c = B's first column) and both row ends.  Rows with at most
+//             kCompact candidates left skip the tree: one lane re-runs the
+//             stack algorithm over all segment stacks.
 //  3. fill    each thread walks its own columns along cuts and stacks (the
 //             owner column is monotone in j) and writes D, sqrt(D), the
 //             label and/or the nearest column.
@@ -151,6 +154,8 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     int* xs = cnt + T;                                            // [T/32] per warp: takeover / census
     int* nzw = xs + (T >> 5);                                     // [T/32] warp has candidates
     uint32_t* cmp = reinterpret_cast<uint32_t*>(nzw + (T >> 5));  // [kCompact+2] compact envelope
+    int* wzf = reinterpret_cast<int*>(cmp + kCompact + 2);        // [T/32] first zero column of a warp's group
+    int* wzl = wzf + (T >> 5);                                    // [T/32] last zero column of a warp's group
 
     // ---- 0. stage the row's nearest-row values (coalesced 4-byte loads) ----
     if (active) {
@@ -173,6 +178,7 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     __syncthreads();
 
     // ---- 1. per-segment envelope (exact_edt.cpp:208-223) ----
+    int zf = W, zl = -1;  // first / last column with an object pixel ON this row (g = 0)
     {
         const int c0 = s * L, c1 = min(c0 + L, W);
         uint32_t* st = stk + s * LY::stk_stride;
@@ -192,6 +198,10 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
             };
             load_m();
             while (m < c1) {
+                if (gm == 0) {
+                    zf = min(zf, m);
+                    zl = m;
+                }
                 if (gm == 0 && n > 0 && tg == 0 && tk == m - 1) {
                     // run of object pixels: the new zero parabola starts exactly at m
                     // and pops nothing (num = 2m-1 > 2*ts, start = m, push since m < W)
@@ -331,6 +341,20 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         const int P = G < 32 ? G : 32;
         const int q = s - gb;
         if (G > 32) __syncthreads();  // every warp's cuts of the previous level
+        // zero columns of both halves: zf/zl hold my (G/2)-group's first/last
+        int zfA, zlA, zfB, zlB;
+        if (G <= 32) {  // (rows narrower than a warp share it: lane - s is the row's first lane)
+            const int la = (lane - s + gb) & 31, lb = (lane - s + gb + half) & 31;
+            zfA = __shfl_sync(0xffffffffu, zf, la);
+            zlA = __shfl_sync(0xffffffffu, zl, la);
+            zfB = __shfl_sync(0xffffffffu, zf, lb);
+            zlB = __shfl_sync(0xffffffffu, zl, lb);
+        } else {
+            zfA = wzf[gb >> 5];
+            zlA = wzl[gb >> 5];
+            zfB = wzf[(gb + half) >> 5];
+            zlB = wzl[(gb + half) >> 5];
+        }
         if (q < 32) {                 // warp-uniform: whole warps probe or not
             const int c = min((gb + half) * L, W - 1);
             const float rP1 = 1.0f / (float)(P + 1);
@@ -349,6 +373,13 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
             }
             if (!hasB) lo = hi = W;
             else if (!hasA) lo = hi = 0;
+            else {
+                // A owns its last zero column zl(A) (D = 0, unique), B its first
+                // zf(B): B takes over inside (zl(A), zf(B)] -- on dense rows an
+                // empty bracket, no probe round at all.
+                if (zlA >= 0) lo = zlA + 1;
+                if (zfB < W) hi = zfB;
+            }
             bool first = true;
             while (__any_sync(0xffffffffu, active && hi > lo)) {
                 const int n = hi - lo;
@@ -383,6 +414,12 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         if (G > 32) {
             __syncthreads();
             if (active) cut[s] = q >= half ? max(cut[s], xs[gb >> 5]) : min(cut[s], xs[gb >> 5]);
+        }
+        zf = min(zfA, zfB);  // the merged group's zero columns
+        zl = max(zlA, zlB);
+        if (G >= 32 && lane == 0) {  // read at the next level after its barrier
+            wzf[s >> 5] = zf;
+            wzl[s >> 5] = zl;
         }
         __syncwarp();
     }
@@ -477,7 +514,7 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
 
 // Row-pass words of shared memory per row for a given (T, L).
 inline int row_words(int T, int L) {
-    return (T * (L + 2)) / 2 + T * (L + 1) + 2 * T + 2 * (T >> 5) + kCompact + 2;  // nrs, stacks, cut, cnt, ...
+    return (T * (L + 2)) / 2 + T * (L + 1) + 2 * T + 4 * (T >> 5) + kCompact + 2;  // nrs, stacks, cut, cnt, ...
 }
 
 // Host-side dispatch over the compile-time segment length.

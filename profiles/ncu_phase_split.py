@@ -1,18 +1,19 @@
-"""Attribute an ncu source page to code regions of k_rows.cu by line ranges
-(found from marker comments).  Usage: python ncu_phase_split.py rep"""
+"""Attribute an ncu source page to code regions of a kernel file by line ranges
+(found from marker comments).  Usage: python ncu_phase_split.py rep [k_rows.cu]"""
 import csv
 import re
 import subprocess
 import sys
 
 rep = sys.argv[1]
-src = open("paper_2106_03503_b200/csrc/k_rows.cu").read().splitlines()
+srcname = sys.argv[2] if len(sys.argv) > 2 else "k_rows.cu"
+src = open("paper_2106_03503_b200/csrc/" + srcname).read().splitlines()
 marks = []
 for n, line in enumerate(src, 1):
     m = re.search(r"// ---- (\d\. [^-]+|[0-9]\.)", line)
     if "struct RowCtx" in line:
         marks.append((n, "RowCtx (merge lookups/walk)"))
-    if "__global__ void __launch_bounds__(1024) k_rows" in line:
+    if "__global__ void __launch_bounds__" in line:
         marks.append((n, "kernel prologue"))
     if m:
         marks.append((n, m.group(1).strip()))
@@ -31,7 +32,7 @@ for r in csv.reader(txt.splitlines()):
         v = lambda k: int(r[hdr.index(k)]) if r[hdr.index(k)].isdigit() else 0
         ln = int(r[0])
         key = "helpers:" + cur
-        if cur == "k_rows.cu":
+        if cur == srcname:
             key = "header"
             for n, name in marks:
                 if ln >= n:
