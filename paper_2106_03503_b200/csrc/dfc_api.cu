@@ -96,7 +96,12 @@ RowGeom row_geom(int W) {
     const int per = (W + g.T - 1) / g.T;
     g.L = 4;
     while (g.L < per) g.L <<= 1;
-    g.R = g.T >= 256 ? 1 : 256 / g.T;
+    static int cta = [] {  // threads per CTA target (DFC_ROW_CTA, tuning)
+        const char* e = getenv("DFC_ROW_CTA");
+        const int v = e ? atoi(e) : 0;
+        return (v == 32 || v == 64 || v == 128 || v == 256 || v == 512) ? v : 64;
+    }();
+    g.R = g.T >= cta ? 1 : cta / g.T;
     g.row_words = dfc::row_words(g.T, g.L);
     g.smem_bytes = g.R * g.row_words * 4;
     // keep the CTA within the 227 KB opt-in limit: fewer rows per CTA
