@@ -430,12 +430,13 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
     r.W = (int)cols;
     r.T = 32;
     while (r.T < 1024 && (int64_t)r.T * 32 < cols) r.T <<= 1;
-    r.L = (int)((cols + r.T - 1) / r.T);
+    r.L = 1;  // power of two: padded indices are a shift
+    while ((int64_t)r.L * r.T < cols) r.L <<= 1;
     r.city = d_cityblock;
     r.chess = d_chessboard;
     r.cham = d_chamfer34;
     const int padW = (int)(cols + cols / r.L + 1);
-    const int smem = (2 * padW + 2 * r.T) * 4;
+    const int smem = (2 * padW + 2 * r.T + 2) * 4;
     e = cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e);
     k_raster<<<(unsigned)rows, r.T, smem, st>>>(r);

@@ -21,20 +21,21 @@
 
 namespace dfc {
 
-constexpr int kBig = 0x3fffffff;  // "no object in this column" inside the scans
+constexpr int kBig = 0x1fffffff;  // "no object in this column"; 4 * kBig still fits int32
 
 
 // padded index: one pad word per L-column segment (segment-strided and
-// column-contiguous accesses are both bank-conflict free)
-__device__ __forceinline__ int pidx(int j, int L) { return j + j / L; }
+// column-contiguous accesses are both bank-conflict free); L = 2^lg
+__device__ __forceinline__ int pidx(int j, int lg) { return j + (j >> lg); }
 
 __global__ void __launch_bounds__(1024) k_raster(RasterArgs a) {
     extern __shared__ int rs[];
     const int T = a.T, L = a.L, W = a.W;
+    const int lg = 31 - __clz(L);
     const int s = threadIdx.x;
     const int i = blockIdx.x;
     const int padW = W + W / L + 1;
-    int* av = rs;               // [padW] vertical distance a_k (kBig = none)
+    int* av = rs + 2;           // [-2, padW) vertical distance a_k (kBig = none); pidx(-1), pidx(W): kBig
     int* l1 = av + padW;        // [padW] city-block row
     int* v = l1 + padW;         // [T] scan scratch
     int* w = v + T;             // [T]
@@ -44,8 +45,12 @@ __global__ void __launch_bounds__(1024) k_raster(RasterArgs a) {
     for (int j = s; j < W; j += T) {
         const uint32_t r = src[j];
         const int d = r == kNoRow ? kBig : (int)(i > (int)r ? i - (int)r : (int)r - i);
-        av[pidx(j, L)] = d;
+        av[pidx(j, lg)] = d;
         any |= d < kBig;
+    }
+    if (s == 0) {
+        av[pidx(-1, lg)] = kBig;
+        av[pidx(W, lg)] = kBig;
     }
     const bool row_has = __syncthreads_or(any);
     int32_t* crow = a.city ? a.city + (int64_t)i * W : nullptr;
@@ -65,10 +70,10 @@ __global__ void __launch_bounds__(1024) k_raster(RasterArgs a) {
     int fend = kBig, bbeg = kBig;
     {
         int f = kBig;
-        for (int j = c0; j < c1; ++j) f = min(av[pidx(j, L)], f + 1);
+        for (int j = c0; j < c1; ++j) f = min(av[pidx(j, lg)], f + 1);
         fend = f;
         int b = kBig;
-        for (int j = c1 - 1; j >= c0; --j) b = min(av[pidx(j, L)], b + 1);
+        for (int j = c1 - 1; j >= c0; --j) b = min(av[pidx(j, lg)], b + 1);
         bbeg = b;
     }
     // carries: fwd(c0-1) = min_{s'<s} (fend_s' - (s'+1)L) + sL
@@ -87,43 +92,32 @@ __global__ void __launch_bounds__(1024) k_raster(RasterArgs a) {
     if (c0 < W) {
         int f = s > 0 ? min(kBig, v[s - 1] + s * L) : kBig;   // fwd(c0 - 1)
         for (int j = c0; j < c1; ++j) {
-            f = min(av[pidx(j, L)], f + 1);
-            l1[pidx(j, L)] = f;
+            f = min(av[pidx(j, lg)], f + 1);
+            l1[pidx(j, lg)] = f;
         }
         int b = s + 1 < T ? min(kBig, w[s + 1] - (s + 1) * L) : kBig;  // bwd(c1)
         for (int j = c1 - 1; j >= c0; --j) {
-            b = min(av[pidx(j, L)], b + 1);
-            l1[pidx(j, L)] = min(l1[pidx(j, L)], b);
+            b = min(av[pidx(j, lg)], b + 1);
+            l1[pidx(j, lg)] = min(l1[pidx(j, lg)], b);
         }
     }
     __syncthreads();
 
     // ---- chessboard / chamfer-3-4: outward window search per cell ----
+    // bch >= 3 * binf throughout, so 3h >= bch ends both searches; columns
+    // outside the row read the kBig sentinels at pidx(-1) and pidx(W).
     for (int j = s; j < W; j += T) {
-        const int aj = av[pidx(j, L)];
-        int binf = aj, bch = aj < kBig ? 3 * aj : kBig;
-        for (int h = 1;; ++h) {
-            if (h >= binf && 3 * h >= bch) break;
-            const bool left = j - h >= 0, right = j + h < W;
-            if (!left && !right) break;
-            if (left) {
-                const int ak = av[pidx(j - h, L)];
-                if (ak < kBig) {
-                    const int mx = max(ak, h), mn = min(ak, h);
-                    binf = min(binf, mx);
-                    bch = min(bch, 3 * mx + mn);
-                }
-            }
-            if (right) {
-                const int ak = av[pidx(j + h, L)];
-                if (ak < kBig) {
-                    const int mx = max(ak, h), mn = min(ak, h);
-                    binf = min(binf, mx);
-                    bch = min(bch, 3 * mx + mn);
-                }
-            }
+        const int aj = av[pidx(j, lg)];
+        int binf = aj, bch = 3 * aj;
+        const int hmax = max(j, W - 1 - j);
+        for (int h = 1; 3 * h < bch && h <= hmax; ++h) {
+            const int al = av[pidx(max(j - h, -1), lg)];
+            const int ar = av[pidx(min(j + h, W), lg)];
+            const int ml = max(al, h), mr = max(ar, h);
+            binf = min(binf, min(ml, mr));
+            bch = min(bch, min(3 * ml + min(al, h), 3 * mr + min(ar, h)));
         }
-        if (crow) __stcs(crow + j, l1[pidx(j, L)]);
+        if (crow) __stcs(crow + j, l1[pidx(j, lg)]);
         if (brow) __stcs(brow + j, binf);
         if (mrow) __stcs(mrow + j, bch);
     }
