@@ -160,6 +160,43 @@ int dfc_envelope_vdist_u16(const uint16_t* d_vdist, int64_t rows, int64_t cols, 
 int dfc_sqrt_i32(const int32_t* d_sqdist, float* d_dist, int64_t n, dfc_stream_t stream);
 
 /*
+ * CLI / rendering epilogues (k_render.cu).  They replace host loops of the
+ * reference's I/O layer so the CLI path stays on the device:
+ *
+ * dfc_unpack_pbm: a P4 raster -- `rows` rows of `row_bytes` = ceil(cols/8)
+ * bytes, MSB first, bit 1 = object (read_netpbm, netpbm.cpp:81-95) -- into a
+ * uint8 0/1 image of pitch `pitch_bytes` (>= cols); invert != 0 flips it
+ * (BinaryImage::inverted, grid.cpp:38-44, the CLI's --polarity inside).
+ */
+int dfc_unpack_pbm(const uint8_t* d_bits, int64_t rows, int64_t cols, int64_t row_bytes, int invert,
+                   uint8_t* d_img, int64_t pitch_bytes, dfc_stream_t stream);
+
+/* uint8 image -> 0/1 (object = nonzero, grid.hpp:82), optionally inverted;
+ * d_dst may alias d_src when the pitches are equal. */
+int dfc_binarize_u8(const uint8_t* d_src, int64_t rows, int64_t cols, int64_t src_pitch, int invert,
+                    uint8_t* d_dst, int64_t dst_pitch, dfc_stream_t stream);
+
+/* Object pixels of an image (BinaryImage::object_count), ADDED to *d_count
+ * (a device uint64 the caller zeroes). */
+int dfc_count_objects_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                         uint64_t* d_count, dfc_stream_t stream);
+
+/*
+ * to_gray (grid.cpp:93-110) of n int32 values: round(255 * v / max) (mode 0,
+ * GrayMapping::linear) or round(255 * sqrt(v) / sqrt(max)) (mode 1,
+ * sqrt_linear), double arithmetic and lround as the reference; all zeros when
+ * max == 0.  *d_max (device int32) receives the max finite value, -1 if there
+ * is none -- the caller raises the reference's domain_error on -1 after its
+ * own synchronisation.  d_scratch: one device uint32.
+ */
+int dfc_gray_i32(const int32_t* d_map, int64_t n, int mode, uint8_t* d_gray, int32_t* d_max,
+                 uint32_t* d_scratch, dfc_stream_t stream);
+
+/* labels_to_gray (grid.cpp:112-121): round(255 * ordinal / feature_count). */
+int dfc_labels_gray(const uint32_t* d_ordinal, int64_t n, int64_t feature_count, uint8_t* d_gray,
+                    dfc_stream_t stream);
+
+/*
  * Measurement hook (bench.py): cudaEvent_t handles recorded on the call's
  * stream by the next dfc_edt_u8* calls on this thread -- ev_col_begin before
  * the column pass, ev_row_begin between column and row pass, ev_row_end

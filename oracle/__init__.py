@@ -88,6 +88,12 @@ def _bind_ref(lib):
     lib.dfref_edt_labels_batch.restype = C.c_int
     lib.dfref_edt_labels_batch.argtypes = [_u8p, _sz, _sz, _sz, C.c_uint, C.c_void_p, C.c_void_p, dp]
     lib.dfref_propagation.argtypes = [_u8p, _sz, _sz, C.c_int, C.c_uint, _u64p, dp]
+    szp = C.POINTER(_sz)
+    lib.dfref_read_netpbm.argtypes = [C.c_char_p, _sz, C.c_void_p, szp, szp, C.c_char_p, _sz]
+    lib.dfref_write_pbm.argtypes = [_u8p, _sz, _sz, C.c_int, C.c_char_p, _sz]
+    lib.dfref_transform_text.argtypes = [_u8p, _sz, _sz, C.c_int, C.c_int, C.c_char_p, _sz]
+    lib.dfref_transform_gray.argtypes = [_u8p, _sz, _sz, C.c_int, C.c_int, _u8p]
+    lib.dfref_labels_render.argtypes = [_u8p, _sz, _sz, _u8p, C.c_char_p, _sz, C.POINTER(C.c_int)]
     lib.dfref_kind_bound.restype = C.c_uint64
     lib.dfref_kind_bound.argtypes = [C.c_int, _sz, _sz]
     return lib
@@ -268,3 +274,51 @@ def ref_propagation(img, kind, threads=1, want_time=False):
     ns = C.c_double(0)
     ref.dfref_propagation(img, r, c, kind, threads, out, C.byref(ns))
     return (out, ns.value) if want_time else out
+
+
+# ---- the CLI's I/O layer, from the reference (checkers for tools/distfield_b200) ----
+
+def ref_read_netpbm(data: bytes):
+    """(image, None) or (None, error message) from the reference read_netpbm."""
+    r, c = _sz(0), _sz(0)
+    err = C.create_string_buffer(512)
+    if ref.dfref_read_netpbm(data, len(data), None, C.byref(r), C.byref(c), err, 512) != 0:
+        return None, err.value.decode()
+    out = np.empty((r.value, c.value), np.uint8)
+    ref.dfref_read_netpbm(data, len(data), out.ctypes.data, C.byref(r), C.byref(c), err, 512)
+    return out, None
+
+
+def ref_write_pbm(img, raw=True) -> bytes:
+    img, r, c = _img(img)
+    n = ref.dfref_write_pbm(img, r, c, int(raw), None, 0)
+    buf = C.create_string_buffer(n)
+    ref.dfref_write_pbm(img, r, c, int(raw), buf, n)
+    return buf.raw[:n]
+
+
+def ref_transform_text(img, metric, mode=0) -> str:
+    """metric 0 edt / 1 cityblock / 2 chamfer34; mode 0 plain, 1 sqrt, 2 normalized."""
+    img, r, c = _img(img)
+    n = ref.dfref_transform_text(img, r, c, metric, mode, None, 0)
+    buf = C.create_string_buffer(n + 1)
+    ref.dfref_transform_text(img, r, c, metric, mode, buf, n + 1)
+    return buf.value.decode()
+
+
+def ref_transform_gray(img, metric, sqrt_mode):
+    img, r, c = _img(img)
+    out = np.empty((r, c), np.uint8)
+    return None if ref.dfref_transform_gray(img, r, c, metric, int(sqrt_mode), out) else out
+
+
+def ref_labels_render(img):
+    """(labels_to_gray image, to_text(labels)) or None when the reference throws."""
+    img, r, c = _img(img)
+    gray = np.empty((r, c), np.uint8)
+    n = C.c_int(0)
+    if ref.dfref_labels_render(img, r, c, gray, None, 0, C.byref(n)):
+        return None
+    buf = C.create_string_buffer(n.value + 1)
+    ref.dfref_labels_render(img, r, c, gray, buf, n.value + 1, C.byref(n))
+    return gray, buf.value.decode()

@@ -2,7 +2,7 @@
 //
 // A flat extern "C" shim over the UNMODIFIED reference library, compiled by
 // oracle/Makefile directly from the reference sources where they lie
-// (/root/reference/proj/core/src/{grid,exact_edt,propagation,random_image}.cpp)
+// (/root/reference/proj/core/src/{grid,exact_edt,propagation,random_image,netpbm}.cpp)
 // into oracle/_ref/libdfref.so.  Used (a) to pin the C restatement
 // oracle/dt_oracle.c and (b) as bench.py's CPU baseline ("kind": "reference").
 // Each call copies the caller's uint8 buffer into a distfield::BinaryImage
@@ -12,9 +12,11 @@
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <string>
 
 #include "distfield/exact_edt.hpp"
 #include "distfield/grid.hpp"
+#include "distfield/netpbm.hpp"
 #include "distfield/propagation.hpp"
 #include "distfield/random_image.hpp"
 
@@ -146,6 +148,87 @@ int dfref_propagation(const std::uint8_t* img, std::size_t rows, std::size_t col
     if (ns) *ns = since(t0);
     copy_map(dm, out);
     return 0;
+}
+
+// ---- the CLI's I/O layer (checkers for tools/distfield_b200) ----
+
+static int put_text(const std::string& t, char* out, std::size_t cap) {
+    if (out && cap > t.size()) std::memcpy(out, t.c_str(), t.size() + 1);
+    return static_cast<int>(t.size());
+}
+
+// read_netpbm: 0 and the image (out may be NULL to query rows/cols), or 1 and
+// the NetpbmError message (with its byte offset) in err.
+int dfref_read_netpbm(const char* bytes, std::size_t n, std::uint8_t* out, std::size_t* rows, std::size_t* cols,
+                      char* err, std::size_t errcap) {
+    try {
+        const auto img = read_netpbm(std::string_view(bytes, n));
+        *rows = img.rows();
+        *cols = img.cols();
+        if (out)
+            for (std::size_t i = 0; i < img.rows(); ++i)
+                for (std::size_t j = 0; j < img.cols(); ++j) out[i * img.cols() + j] = img.is_object(i, j);
+        return 0;
+    } catch (const std::exception& e) {
+        put_text(e.what(), err, errcap);
+        return 1;
+    }
+}
+
+// write_netpbm(BinaryImage, variant 0 plain / 1 raw) -> bytes; returns size.
+int dfref_write_pbm(const std::uint8_t* img, std::size_t rows, std::size_t cols, int raw, char* out,
+                    std::size_t cap) {
+    const std::string t = write_netpbm(to_image(img, rows, cols), raw ? PbmVariant::raw : PbmVariant::plain);
+    if (out && cap >= t.size()) std::memcpy(out, t.data(), t.size());
+    return static_cast<int>(t.size());
+}
+
+static DistanceMap ref_transform(const BinaryImage& bi, int metric) {
+    return metric == 0   ? edt(bi, EdtAlgorithm::envelope)
+           : metric == 1 ? cityblock_sequential(bi)
+                         : chamfer34(bi);
+}
+
+// Text dump of a transform: metric 0 edt / 1 cityblock / 2 chamfer34;
+// mode 0 to_text, 1 to_text_sqrt, 2 to_text(chamfer_normalized).  Returns
+// the length (the text is written when cap > length).
+int dfref_transform_text(const std::uint8_t* img, std::size_t rows, std::size_t cols, int metric, int mode,
+                         char* out, std::size_t cap) {
+    const DistanceMap dm = ref_transform(to_image(img, rows, cols), metric);
+    return put_text(mode == 0 ? to_text(dm) : mode == 1 ? to_text_sqrt(dm) : to_text(chamfer_normalized(dm)), out,
+                    cap);
+}
+
+// to_gray of a transform (mode 0 linear / 1 sqrt_linear): 0, or 1 when the
+// reference throws (no finite value).
+int dfref_transform_gray(const std::uint8_t* img, std::size_t rows, std::size_t cols, int metric, int mode,
+                         std::uint8_t* out) {
+    try {
+        const auto g = to_gray(ref_transform(to_image(img, rows, cols), metric),
+                               mode ? GrayMapping::sqrt_linear : GrayMapping::linear);
+        for (std::size_t i = 0; i < rows; ++i)
+            for (std::size_t j = 0; j < cols; ++j) out[i * cols + j] = g(i, j);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+// labels_to_gray(voronoi_labels(img), object_count) and to_text(labels):
+// 0, or 1 when the reference throws (no features).
+int dfref_labels_render(const std::uint8_t* img, std::size_t rows, std::size_t cols, std::uint8_t* gray, char* text,
+                        std::size_t cap, int* text_len) {
+    try {
+        const auto bi = to_image(img, rows, cols);
+        const auto lab = voronoi_labels(bi);
+        const auto g = labels_to_gray(lab, bi.object_count());
+        for (std::size_t i = 0; i < rows; ++i)
+            for (std::size_t j = 0; j < cols; ++j) gray[i * cols + j] = g(i, j);
+        *text_len = put_text(to_text(lab), text, cap);
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
 }
 
 std::uint64_t dfref_kind_bound(int kind, std::size_t rows, std::size_t cols) {

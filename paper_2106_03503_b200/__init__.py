@@ -53,11 +53,17 @@ _lib.dfc_set_row_kernel.argtypes = [C.c_int]
 _lib.dfc_column_nr_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
 _lib.dfc_rows_from_nr_u16.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp]
 _lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
+_lib.dfc_unpack_pbm.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
+_lib.dfc_binarize_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
+_lib.dfc_count_objects_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp]
+_lib.dfc_gray_i32.argtypes = [_vp, _i64, C.c_int, _vp, _vp, _vp, _vp]
+_lib.dfc_labels_gray.argtypes = [_vp, _i64, _i64, _vp, _vp]
 
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
     "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel",
+    "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
 )
 
 
@@ -256,6 +262,54 @@ def sqrt_i32(sq: torch.Tensor, stream=None) -> torch.Tensor:
     sq = sq.contiguous()
     out = torch.empty(sq.shape, dtype=torch.float32, device=sq.device)
     _check(_lib.dfc_sqrt_i32(_ptr(sq), _ptr(out), sq.numel(), _stream(stream)))
+    return out
+
+
+def unpack_pbm(bits: torch.Tensor, rows: int, cols: int, invert: bool = False, stream=None) -> torch.Tensor:
+    """uint8 0/1 image [rows, cols] from a device P4 raster (uint8, rows * ceil(cols/8)
+    bytes, MSB first, bit 1 = object; netpbm.cpp:81-95), optionally inverted."""
+    bits = bits.contiguous()
+    rb = (cols + 7) // 8
+    if bits.numel() < rows * rb:
+        raise ValueError("P4 raster too short")
+    out = torch.empty((rows, cols), dtype=torch.uint8, device=bits.device)
+    _check(_lib.dfc_unpack_pbm(_ptr(bits), rows, cols, rb, int(invert), _ptr(out), cols, _stream(stream)))
+    return out
+
+
+def binarize(img: torch.Tensor, invert: bool = False, stream=None) -> torch.Tensor:
+    """0/1 uint8 copy of an image (object = nonzero), optionally inverted."""
+    img, h, w, pitch = _img2d(img)
+    out = torch.empty((h, w), dtype=torch.uint8, device=img.device)
+    _check(_lib.dfc_binarize_u8(_ptr(img), h, w, pitch, int(invert), _ptr(out), w, _stream(stream)))
+    return out
+
+
+def count_objects(img: torch.Tensor, stream=None) -> torch.Tensor:
+    """Device int64 scalar: object pixels of the image (BinaryImage::object_count)."""
+    img, h, w, pitch = _img2d(img)
+    cnt = torch.zeros((), dtype=torch.int64, device=img.device)
+    _check(_lib.dfc_count_objects_u8(_ptr(img), h, w, pitch, _ptr(cnt), _stream(stream)))
+    return cnt
+
+
+def gray(dmap: torch.Tensor, sqrt_mode: bool = False, stream=None):
+    """to_gray (grid.cpp:93-110) of an int32 map -> (uint8 map, device int32 max;
+    -1 = no finite value, where the reference throws domain_error)."""
+    dmap = dmap.contiguous()
+    out = torch.empty(dmap.shape, dtype=torch.uint8, device=dmap.device)
+    mx = torch.empty((), dtype=torch.int32, device=dmap.device)
+    scratch = torch.empty((), dtype=torch.int32, device=dmap.device)
+    _check(_lib.dfc_gray_i32(_ptr(dmap), dmap.numel(), int(sqrt_mode), _ptr(out), _ptr(mx), _ptr(scratch),
+                             _stream(stream)))
+    return out, mx
+
+
+def labels_gray(ordinal: torch.Tensor, feature_count: int, stream=None) -> torch.Tensor:
+    """labels_to_gray (grid.cpp:112-121) of uint32 ordinals (int32/int64 tensor)."""
+    o = ordinal.to(torch.int32).contiguous()
+    out = torch.empty(o.shape, dtype=torch.uint8, device=o.device)
+    _check(_lib.dfc_labels_gray(_ptr(o), o.numel(), int(feature_count), _ptr(out), _stream(stream)))
     return out
 
 

@@ -20,4 +20,8 @@ DistanceMap chamfer34(const BinaryImage& img);
 // (proj/tests/oracles.hpp:52-55).  kind() == DistanceKind::chessboard.
 DistanceMap chessboard(const BinaryImage& img);
 
+// (d / 3)^2 per cell of a chamfer-3-4 map (propagation.cpp:111-127);
+// std::invalid_argument for any other kind.
+Grid<double> chamfer_normalized(const DistanceMap& dm);
+
 }  // namespace distfield

@@ -541,6 +541,69 @@ int dfc_sqrt_i32(const int32_t* d_sqdist, float* d_dist, int64_t n, dfc_stream_t
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 
+static unsigned grid_for(int64_t n, int per_block = 256, int cap = 148 * 16) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + per_block - 1) / per_block, cap));
+}
+
+int dfc_unpack_pbm(const uint8_t* d_bits, int64_t rows, int64_t cols, int64_t row_bytes, int invert,
+                   uint8_t* d_img, int64_t pitch_bytes, dfc_stream_t stream) {
+    if (!d_bits || !d_img || rows < 1 || cols < 1 || row_bytes != (cols + 7) / 8 || pitch_bytes < cols)
+        return DFC_ERR_ARG;
+    g_launches = 0;
+    k_unpack_pbm<<<grid_for(rows * row_bytes), 256, 0, (cudaStream_t)stream>>>(d_bits, rows, cols, row_bytes,
+                                                                              invert, d_img, pitch_bytes);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_binarize_u8(const uint8_t* d_src, int64_t rows, int64_t cols, int64_t src_pitch, int invert,
+                    uint8_t* d_dst, int64_t dst_pitch, dfc_stream_t stream) {
+    if (!d_src || !d_dst || rows < 1 || cols < 1 || src_pitch < cols || dst_pitch < cols) return DFC_ERR_ARG;
+    g_launches = 0;
+    k_binarize<<<grid_for(rows * cols), 256, 0, (cudaStream_t)stream>>>(d_src, rows, cols, src_pitch, invert,
+                                                                       d_dst, dst_pitch);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_count_objects_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                         uint64_t* d_count, dfc_stream_t stream) {
+    if (!d_img || !d_count || rows < 1 || cols < 1 || pitch_bytes < cols) return DFC_ERR_ARG;
+    g_launches = 0;
+    k_count<<<grid_for(rows * cols), 256, 0, (cudaStream_t)stream>>>(
+        d_img, rows, cols, pitch_bytes, reinterpret_cast<unsigned long long*>(d_count));
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_gray_i32(const int32_t* d_map, int64_t n, int mode, uint8_t* d_gray, int32_t* d_max,
+                 uint32_t* d_scratch, dfc_stream_t stream) {
+    if (!d_map || !d_gray || !d_max || !d_scratch || n < 1 || (mode != 0 && mode != 1)) return DFC_ERR_ARG;
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(d_scratch, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    k_max_finite<<<grid_for(n), 256, 0, st>>>(d_map, n, d_scratch);
+    k_gray<<<grid_for(n), 256, 0, st>>>(d_map, n, mode, d_scratch, d_gray, d_max);
+    g_launches += 2;
+    e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_labels_gray(const uint32_t* d_ordinal, int64_t n, int64_t feature_count, uint8_t* d_gray,
+                    dfc_stream_t stream) {
+    if (!d_ordinal || !d_gray || n < 1) return DFC_ERR_ARG;
+    if (feature_count < 1) return DFC_ERR_NO_FEATURES;
+    g_launches = 0;
+    k_labels_gray<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(d_ordinal, n, (double)feature_count, d_gray);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
 int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_end) {
     g_ev[0] = static_cast<cudaEvent_t>(ev_col_begin);
     g_ev[1] = static_cast<cudaEvent_t>(ev_row_begin);
