@@ -17,7 +17,8 @@ namespace {
 thread_local int g_last_cuda = 0;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
-thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming, 3: window
+thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming, 3: window,
+                                  // 4: dense rows first, the rest by the segment kernel (default)
 
 // DFC_ROWS=segment|stream overrides the default stage-2 kernel (tuning/A-B).
 int env_row_mode() {
@@ -25,7 +26,8 @@ int env_row_mode() {
         const char* v = getenv("DFC_ROWS");
         if (v && strcmp(v, "stream") == 0) return 2;
         if (v && strcmp(v, "win") == 0) return 3;
-        return 1;  // default: the segment/merge kernel
+        if (v && strcmp(v, "segment") == 0) return 1;
+        return 4;  // default: dense-row kernel, then the segment/merge kernel for the other rows
     }();
     return m;
 }
@@ -115,7 +117,7 @@ RowGeom row_geom(int W) {
 // Stage 1 into a uint16 nearest-row plane [npol][n][H][Wp].
 int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
-                cudaStream_t st, int32_t* vsq = nullptr) {
+                cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -130,7 +132,11 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.vec = aligned(img, 4) && pitch % 4 == 0 && istride % 4 == 0;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
-    k_band_summary<<<grid, tpb, 0, st>>>(c, first, last);
+    if (counts) {
+        const cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)npol * n * sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    k_band_summary<<<grid, tpb, 0, st>>>(c, first, last, counts);
     if (c.nb <= 64) {  // short columns: serial over bands, one thread per column
         dim3 gs((unsigned)((W + 255) / 256), (unsigned)(npol * n));
         k_band_scan_serial<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
@@ -199,7 +205,7 @@ int row_pass_win(RowArgs a, bool take_new, cudaStream_t st) {
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
              int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
              int64_t sN, cudaStream_t st, bool vdist = false, int tile_cols = 0,
-             int64_t tile_stride = 0, int row0 = 0) {
+             int64_t tile_stride = 0, int row0 = 0, const unsigned long long* plane_counts = nullptr) {
     const RowGeom g = row_geom((int)W);
     RowArgs a;
     a.nr = nr;
@@ -229,6 +235,8 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.row_list = nullptr;
     a.row_count = nullptr;
     a.vec_nr = false;
+    a.row_done = nullptr;
+    a.plane_counts = plane_counts;
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
     if (mode == 3 && W <= 16384) return row_pass_win(a, take_new, st);
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
@@ -239,6 +247,29 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
 
     // Streaming kernel (one lane = one row) when the nr plane allows coalesced
     // 16-byte tile loads; rows whose live stack overflows go to k_rows.
+    if (mode == 4 && W <= kDenseMaxW) {
+        // dense rows (short runs between object pixels) by k_rows_dense, which
+        // flags them; the segment kernel then skips the flagged rows
+        Scratch fl(st);
+        e = fl.alloc((size_t)a.total_rows);
+        if (e != cudaSuccess) return cuda_fail(e);
+        a.row_done = static_cast<uint8_t*>(fl.p);
+        a.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0 && a.tile_cols >= W;
+        const void* dfn = take_new ? dense_kernel_ptr<true>() : dense_kernel_ptr<false>();
+        const int dsm = dense_smem_bytes((int)W);
+        e = cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+        if (e != cudaSuccess) return cuda_fail(e);
+        const int64_t dblocks = std::min<int64_t>((a.total_rows + kDenseWarps - 1) / kDenseWarps, 148 * 16);
+        void* dargs[] = {&a};
+        e = cudaLaunchKernel(dfn, dim3((unsigned)dblocks), dim3(32 * kDenseWarps), dargs, (size_t)dsm, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        ++g_launches;
+        void* args[] = {&a};
+        e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        ++g_launches;
+        return DFC_OK;
+    }
     const bool stream_ok = mode == 2 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
                            a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
     if (stream_ok) {
@@ -255,8 +286,18 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         e = cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
         if (e != cudaSuccess) return cuda_fail(e);
         const int64_t sblocks = (a.total_rows + 32 * kSWarps - 1) / (32 * kSWarps);
-        void* sargs[] = {&a, &fail_rows, &fail_count};
-        e = cudaLaunchKernel(sfn, dim3((unsigned)sblocks), dim3(32 * kSWarps), sargs, (size_t)ssm, st);
+        static const int chunk_env = [] {  // DFC_CHUNK (tuning): columns per warp chunk
+            const char* v = getenv("DFC_CHUNK");
+            const int c = v ? atoi(v) : 0;
+            return c >= 32 ? c & ~31 : 256;
+        }();
+        int chunk = (int)std::min<int64_t>(W, chunk_env);
+        chunk = (chunk + 31) & ~31;
+        const int nchunks = (int)((W + chunk - 1) / chunk);
+        if (sblocks > 0x7fffffff || nchunks > 65535) return DFC_ERR_SHAPE;
+        void* sargs[] = {&a, &fail_rows, &fail_count, &chunk};
+        e = cudaLaunchKernel(sfn, dim3((unsigned)sblocks, (unsigned)nchunks), dim3(32 * kSWarps), sargs,
+                             (size_t)ssm, st);
         if (e != cudaSuccess) return cuda_fail(e);
         ++g_launches;
         RowArgs fb = a;  // fallback: the segment kernel over the overflowed rows
@@ -293,13 +334,14 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     const size_t carry_elems = (size_t)(planes * nb * Wp);
     const size_t nr_elems = (size_t)(planes * H * Wp);
     Scratch sc(st);
-    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 256);
+    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 256 + (size_t)planes * 8);
     if (e != cudaSuccess) return cuda_fail(e);
     uint16_t* first = static_cast<uint16_t*>(sc.p);
     uint16_t* last = first + carry_elems;
     uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry_elems), 16));
+    auto* counts = reinterpret_cast<unsigned long long*>(round_up(reinterpret_cast<uintptr_t>(nr + nr_elems), 16));
     prof(0, st);
-    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st);
+    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -321,21 +363,23 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
         if (want_keep) {
             rc = row_pass(nr, nimg, H, W, Wp, false, o.D[0], stride_of(o.D[0], o.D[1]), o.S[0],
                           o.S[0] ? stride_of(o.S[0], o.S[1]) : 0, o.LB[0],
-                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st);
+                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st, false, 0, 0, 0, counts);
             if (rc != DFC_OK) return rc;
         }
         if (o.NC[0]) {
             rc = row_pass(nr, nimg, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[0],
-                          stride_of(o.NC[0], o.NC[1]), st);
+                          stride_of(o.NC[0], o.NC[1]), st, false, 0, 0, 0, counts);
             if (rc != DFC_OK) return rc;
         }
     } else {
         for (int s = 0; s < npol; ++s) {
             const uint16_t* pl = nr + (int64_t)s * H * Wp;
-            rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st);
+            rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st, false, 0, 0, 0,
+                          counts + s);
             if (rc != DFC_OK) return rc;
             if (o.NC[s]) {
-                rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st);
+                rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st, false, 0, 0,
+                              0, counts + s);
                 if (rc != DFC_OK) return rc;
             }
         }
@@ -612,7 +656,7 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 }
 
 int dfc_set_row_kernel(int mode) {
-    if (mode < 0 || mode > 3) return DFC_ERR_ARG;
+    if (mode < 0 || mode > 4) return DFC_ERR_ARG;
     g_row_mode = mode;
     return DFC_OK;
 }

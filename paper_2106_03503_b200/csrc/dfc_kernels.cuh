@@ -38,6 +38,8 @@ struct RowArgs {
     bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
     const int* row_list;      // fallback mode: process only these rows (nullptr: all)
     const int* row_count;     // number of entries in row_list (device)
+    uint8_t* row_done;        // per row: 1 = written by k_rows_dense (the segment kernel skips it)
+    const unsigned long long* plane_counts;  // object pixels per plane (dense gate), nullable
 };
 
 // Raster transforms (k_raster.cu)

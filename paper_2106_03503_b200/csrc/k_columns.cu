@@ -59,25 +59,35 @@ __device__ __forceinline__ uint32_t pol_mask(uint32_t m, int pol, uint32_t valid
 
 
 // K1a: grid (ceil(W/4)/blockDim, nb, n_img)
-__global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t* __restrict__ last) {
+// counts (nullable): object pixels per plane [slot][img], accumulated with one
+// atomic per warp (the row pass's dense-plane gate, k_rows_dense.cu).
+__global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t* __restrict__ last,
+                               unsigned long long* __restrict__ counts) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int j0 = 4 * g;
-    if (j0 >= a.W) return;
+    const bool live = j0 < a.W;  // no early exit: the count reduction needs the whole warp
     const int b = blockIdx.y, im = blockIdx.z;
     const int r0 = b * kBand;
     const int nrows = min(kBand, a.H - r0);
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
-    uint32_t m[4];
-    band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    if (live) band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
         uint16_t f[4], l[4];
+        uint32_t mk[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const uint32_t mk = (j0 + c < a.W) ? pol_mask(m[c], pol, valid) : 0u;
-            f[c] = mk ? (uint16_t)(r0 + __ffs(mk) - 1) : kNoRow;
-            l[c] = mk ? (uint16_t)(r0 + 31 - __clz(mk)) : kNoRow;
+            mk[c] = (live && j0 + c < a.W) ? pol_mask(m[c], pol, valid) : 0u;
+            f[c] = mk[c] ? (uint16_t)(r0 + __ffs(mk[c]) - 1) : kNoRow;
+            l[c] = mk[c] ? (uint16_t)(r0 + 31 - __clz(mk[c])) : kNoRow;
         }
+        if (counts) {
+            unsigned long long c = (unsigned)(__popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]));
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts + (int64_t)s * a.n_img + im, c);
+        }
+        if (!live) continue;
         const int64_t off = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
         *reinterpret_cast<uint2*>(first + off) =
             make_uint2(f[0] | ((uint32_t)f[1] << 16), f[2] | ((uint32_t)f[3] << 16));

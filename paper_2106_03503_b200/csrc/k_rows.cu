@@ -141,6 +141,10 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         active = row < *a.row_count;
         row = active ? a.row_list[row] : 0;
     }
+    if (a.row_done) {  // rows k_rows_dense already wrote
+        if (active && a.row_done[row]) active = false;
+        if (__syncthreads_and(!active)) return;  // CTA-uniform
+    }
     const int img = active ? (int)(row / a.H) : 0;
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // g = (gi - nr)^2, global row

@@ -1,4 +1,4 @@
-// k_rows_stream.cu -- stage 2 as a STREAMING scan: one lane = one row.
+// k_rows_stream.cu -- stage 2 as a STREAMING scan: one lane = one row (chunk).
 //
 // Same result as k_rows.cu (the reference's envelope_rows / meijster_scan /
 // voronoi label assembly, exact_edt.cpp:190-283, :362-369) with a different
@@ -17,6 +17,12 @@
 // bank); a row that overflows its ring goes to a fallback list recomputed by
 // k_rows.  tests/stream_model.py is the statement-level model (fuzzed against
 // brute force for both tie rules).
+//
+// Chunks: a warp owns columns [c0, c1) of its 32 rows (blockIdx.y), so a row
+// is scanned by W / chunk warps in parallel.  Each lane starts its scan at a
+// warm-up column s0 <= c0 chosen so that no candidate left of s0 can own a
+// column of the chunk (the bound is derived below), keeps the envelope over
+// [F, W) with F starting at c0, and scans past c1 until its chunk is final.
 //
 // Data movement: nearest-row values are staged 32 rows x 32 columns at a time
 // with coalesced 16-byte loads (prefetched one tile ahead).  A lane records the
@@ -45,7 +51,8 @@ struct StreamSmem {
 };
 
 template <bool TAKE_NEW, int OUTS>
-__global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fail_rows, int* fail_count) {
+__global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fail_rows, int* fail_count,
+                                                              int chunk) {
     extern __shared__ uint4 smem_raw[];
     StreamSmem& sm = reinterpret_cast<StreamSmem*>(smem_raw)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
@@ -57,6 +64,8 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
     const uint16_t* rowp = active ? a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp : nullptr;
+    // this warp's column chunk [c0, c1) (multiple of 32 wide)
+    const int c0 = (int)blockIdx.y * chunk, c1 = min(c0 + chunk, W);
 
     // ---- staging: lane q loads 16-byte chunk (q & 3) of rows (q >> 2) + 8t ----
     uint4 pre[4];
@@ -86,7 +95,7 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
     int head = 0, cnt = 0;                  // ring entries head .. head+cnt-1
     int tk = 0, ts = 0; uint32_t tg = 0;    // top entry
     int bk = 0; uint32_t bnr = kNoRow, bg = 0; int bend = W;  // bottom entry, end of its range
-    int F = 0;                              // first non-final column
+    int F = c0;                             // first non-final column (columns < c0: other warps)
     uint32_t pend = 0;                      // staging slots holding a completed block
     bool dead = !active;                    // overflowed (or no row): recomputed elsewhere
 
@@ -108,7 +117,7 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
     auto flush = [&](bool tail) {
         // tail: also write the partial block at the end of the row (F == W)
         uint32_t want = pend;
-        if (tail && !dead && (W & 31) && F == W) want |= 1u << ((W >> 5) & 1);
+        if (tail && !dead && (c1 & 31) && F == c1) want |= 1u << ((c1 >> 5) & 1);
         uint32_t ready = __ballot_sync(0xffffffffu, want != 0);
         while (ready) {
             const int L = __ffs(ready) - 1;
@@ -148,7 +157,7 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
         for (;;) {
             bool blocked = false;
             int budget = force ? W : kSEmit;
-            while (!dead && F < W && (force || F < m1) && budget-- > 0) {
+            while (!dead && F < c1 && (force || F < m1) && budget-- > 0) {
                 uint32_t own;
                 if (cnt == 0) {
                     if (!force) break;  // no parabola yet: a later column will own these
@@ -177,16 +186,48 @@ __global__ void __launch_bounds__(32 * kSWarps) k_rows_stream(RowArgs a, int* fa
         }
     };
 
-    prefetch(0);
-    for (int c0 = 0; c0 < W; c0 += kSTile) {
+    // ---- warm-up start s0: no candidate left of s0 can own a column of the
+    // chunk.  For a candidate F' >= c0 with vertical distance a', every F in
+    // [c0, c1) has sqrt(D(F)) <= a' + |F - F'| <= A + (F - c0), A = min_F'
+    // (a' + F' - c0); a column k <= s0 - 1 = c0 - A - 1 has (F - k)^2 >=
+    // (A + F - c0 + 1)^2 > D(F).  So scanning from s0 = c0 - A is exact
+    // (tests/stream_model.py::stream_chunk).  The pre-scan stops once F' - c0
+    // reaches A; s0 = 0 when no candidate lies right of c0.
+    int s0 = 0;
+    if (c0 > 0) {
+        int A = 0x3fffffff;
+        bool need = !dead;
+        for (int t0 = c0; t0 < W && __any_sync(0xffffffffu, need); t0 += kSTile) {
+            prefetch(t0);
+            __syncwarp();
+            commit();
+            __syncwarp();
+            if (need) {
+                for (int x = 0; x < kSTile && t0 + x < W && t0 + x - c0 < A; ++x) {
+                    const uint32_t r = sm.tile[lane * kSTileStride + x];
+                    if (r != kNoRow) {
+                        const int am = (int)(gi > r ? gi - r : r - gi);
+                        A = min(A, am + t0 + x - c0);
+                    }
+                }
+                need = t0 + kSTile - c0 < A;
+            }
+            __syncwarp();
+        }
+        s0 = A >= 0x3fffffff ? 0 : max(0, c0 - A);
+    }
+    const int S0 = __reduce_min_sync(0xffffffffu, dead ? W : s0) & ~(kSTile - 1);
+
+    if (S0 < W) prefetch(S0);
+    for (int t0 = S0; t0 < W && __any_sync(0xffffffffu, !dead && F < c1); t0 += kSTile) {
         __syncwarp();
         commit();
         __syncwarp();
-        if (c0 + kSTile < W) prefetch(c0 + kSTile);
-        const int c1 = min(c0 + kSTile, W);
-        for (int m = c0; m < c1; ++m) {
-            const uint32_t r = sm.tile[lane * kSTileStride + (m - c0)];
-            if (!dead && r != kNoRow) {
+        if (t0 + kSTile < W) prefetch(t0 + kSTile);
+        const int t1 = min(t0 + kSTile, W);
+        for (int m = t0; m < t1; ++m) {
+            const uint32_t r = sm.tile[lane * kSTileStride + (m - t0)];
+            if (!dead && r != kNoRow && m >= s0) {
                 const uint32_t am = gi > r ? gi - r : r - gi;
                 const int gm = (int)(am * am);
                 int start = -2;  // -2: stack empty -> owns from F
