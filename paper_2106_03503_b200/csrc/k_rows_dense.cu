@@ -22,7 +22,7 @@ namespace dfc {
 
 constexpr int kDenseRun = 1024;    // longest run allowed (the search per column stops at sqrt(D))
 constexpr int kDenseWarps = 4;     // rows (warps) per CTA
-constexpr int kDenseMaxW = 8192;   // staged row: 16 KB per warp
+constexpr int kDenseMaxW = 8192;
 
 // per-warp shared memory: the staged row (wp halfwords) + its zero mask, 16 B aligned
 __host__ __device__ __forceinline__ int dense_warp_bytes(int W) {
@@ -155,19 +155,20 @@ __global__ void __launch_bounds__(32 * kDenseWarps) k_rows_dense(RowArgs a) {
             const int hmax = max(j, W - 1 - j);
             for (int h = 0; h <= hmax && (uint32_t)(h * h) <= best; ++h) {
                 const uint32_t hh = (uint32_t)(h * h);
-#pragma unroll
-                for (int side = 0; side < 2; ++side) {
-                    const int k = side ? j + h : j - h;
-                    if ((side && h == 0) || k < 0 || k >= W) continue;
-                    const uint32_t r = nrs[k];
-                    if (r == kNoRow) continue;
-                    const uint32_t av = gi > r ? gi - r : r - gi;
+                // left j-h: the smallest column seen so far (wins keep_old ties);
+                // right j+h: the largest (wins take_new ties); off-row -> none
+                const int kl = j - h, kr = j + h;
+                const uint32_t rl = kl >= 0 ? nrs[kl] : kNoRow;
+                const uint32_t rr = (h > 0 && kr < W) ? nrs[kr] : kNoRow;
+                if (rl != kNoRow) {
+                    const uint32_t av = gi > rl ? gi - rl : rl - gi;
                     const uint32_t d = av * av + hh;
-                    if (d < best || (d == best && (TAKE_NEW ? (uint32_t)k > bk : (uint32_t)k < bk))) {
-                        best = d;
-                        bk = (uint32_t)k;
-                        br = r;
-                    }
+                    if (TAKE_NEW ? d < best : d <= best) { best = d; bk = (uint32_t)kl; br = rl; }
+                }
+                if (rr != kNoRow) {
+                    const uint32_t av = gi > rr ? gi - rr : rr - gi;
+                    const uint32_t d = av * av + hh;
+                    if (TAKE_NEW ? d <= best : d < best) { best = d; bk = (uint32_t)kr; br = rr; }
                 }
             }
             const bool inf = best == kInfU;
