@@ -150,6 +150,10 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;  // g = (gi - nr)^2, global row
     const int W = a.W;
 
+    // sparse plane (fewer object pixels than columns, e.g. C3): candidate
+    // columns are few, so the build visits them through per-segment bit masks
+    const bool sparse = L == 32 && active && a.plane_counts && a.tile_cols >= W &&
+                        a.plane_counts[img] < (unsigned long long)W;
     uint32_t* base = smem + rho * a.row_smem_words;
     uint16_t* nrs = reinterpret_cast<uint16_t*>(base);            // [T*(L+2)]
     uint32_t* stk = base + (T * (L + 2)) / 2;                     // [T*(L+1)]
@@ -165,7 +169,33 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     if (active) {
         const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
         const int npairs = (W + 1) >> 1;
-        if (a.tile_cols >= W) {  // one tile: the row is contiguous
+        if (sparse) {
+            // one tile, 32-column segments: the warp's 32 pairs are 2 segments;
+            // their candidate masks (bit x: column c0+x has an object in its
+            // column) come from two ballots, parked in cut[] until the build
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(rowp);
+            const int lane = threadIdx.x & 31;
+            for (int q0 = s - lane; q0 < npairs; q0 += T) {
+                const int q = q0 + lane;
+                uint32_t v = 0xffffffffu;
+                if (q < npairs) {
+                    v = __ldg(src + q);
+                    *reinterpret_cast<uint32_t*>(nrs + LY::nidx(2 * q)) = v;
+                }
+                const uint32_t b0 = __ballot_sync(0xffffffffu, (v & 0xffffu) != kNoRow && 2 * q < W);
+                const uint32_t b1 = __ballot_sync(0xffffffffu, (v >> 16) != kNoRow && 2 * q + 1 < W);
+                if ((lane & 15) == 0) {  // lanes 0 / 16: segment (2 q0 + 2 lane) / 32
+                    uint32_t e0 = (b0 >> lane) & 0xffffu, e1 = (b1 >> lane) & 0xffffu;
+                    // spread 16 bits to the even positions (pairs -> columns)
+                    e0 = (e0 | (e0 << 8)) & 0x00ff00ffu;  e1 = (e1 | (e1 << 8)) & 0x00ff00ffu;
+                    e0 = (e0 | (e0 << 4)) & 0x0f0f0f0fu;  e1 = (e1 | (e1 << 4)) & 0x0f0f0f0fu;
+                    e0 = (e0 | (e0 << 2)) & 0x33333333u;  e1 = (e1 | (e1 << 2)) & 0x33333333u;
+                    e0 = (e0 | (e0 << 1)) & 0x55555555u;  e1 = (e1 | (e1 << 1)) & 0x55555555u;
+                    const int sg = (2 * q0 + 2 * lane) >> 5;
+                    if (sg < T) cut[sg] = (int)(e0 | (e1 << 1));
+                }
+            }
+        } else if (a.tile_cols >= W) {  // one tile: the row is contiguous
             const uint32_t* src = reinterpret_cast<const uint32_t*>(rowp);
             for (int q = s; q < npairs; q += T)
                 *reinterpret_cast<uint32_t*>(nrs + LY::nidx(2 * q)) = __ldg(src + q);
@@ -192,15 +222,37 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         if (active) {
             // One event per iteration -- pop the top, or consume column m
             // (push or skip) -- instead of a nested pop loop: lanes of a warp
-            // reconverge every iteration.
+            // reconverge every iteration.  On sparse planes only the candidate
+            // columns are visited (bit mask from the staging).
+            const uint16_t* seg_nr = nrs + s * (L + 2);
+            uint32_t rem = sparse ? (uint32_t)cut[s] : 0u;
+            const bool by_mask = sparse;
             int m = c0;
             int gm = -1;  // vertical value of column m, -1 = no feature (:212)
             auto load_m = [&]() {
+                if (by_mask) {
+                    if (rem) {
+                        const int x = __ffs(rem) - 1;
+                        rem &= rem - 1;
+                        m = c0 + x;
+                        const uint32_t r = seg_nr[x];
+                        const int am = (int)(gi > r ? gi - r : r - gi);
+                        gm = am * am;
+                    } else {
+                        m = c1;
+                    }
+                    return;
+                }
                 const uint32_t r = m < c1 ? nrs[LY::nidx(m)] : kNoRow;
                 const int am = (int)(gi > r ? gi - r : r - gi);
                 gm = r == kNoRow ? -1 : am * am;
             };
-            load_m();
+            if (by_mask) load_m();
+            else {
+                const uint32_t r = m < c1 ? nrs[LY::nidx(m)] : kNoRow;
+                const int am = (int)(gi > r ? gi - r : r - gi);
+                gm = r == kNoRow ? -1 : am * am;
+            }
             while (m < c1) {
                 if (gm == 0) {
                     zf = min(zf, m);
@@ -212,7 +264,7 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
                     st[n++] = (uint32_t)m | ((uint32_t)m << 16);
                     tk = m;
                     ts = m;
-                    ++m;
+                    if (!by_mask) ++m;
                     load_m();
                     continue;
                 }
@@ -255,7 +307,7 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
                             tg = gm;
                         }
                     }
-                    ++m;
+                    if (!by_mask) ++m;
                     load_m();
                 }
             }
