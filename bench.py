@@ -301,7 +301,7 @@ def run_ours(args, rank, world, local_rank):
                                    f"column stripes -> NCCL all-to-all -> row stripes x{world}"),
                    "l2": "256 MiB flush between timed steps (outside the events)"},
         "roofline": {
-            "bound": "hbm", "kernel": "k_rows (row envelope)" if cfg != "c4" else "k_band_* + k_raster (whole step)",
+            "bound": "hbm", "kernel": "row pass (k_rows_dense + k_rows, the row envelope)" if cfg != "c4" else "k_band_* + k_raster (whole step)",
             "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(cfg)[0],
             "traffic_source": traffic_for(cfg)[1], "algorithmic_bytes_per_launch": kernel_bytes,
