@@ -227,42 +227,56 @@ def run_ours(args, rank, world, local_rank):
     value = job_px * args.steps / (total_ms * 1e-3) / 1e6
 
     # ---- e2e through the public API with HOST buffers (pinned), copies timed ----
+    # Two streams, each with its own device input/outputs and pinned host
+    # outputs: step k's device->host copies overlap step k+1's upload and
+    # compute (a streaming caller's pipeline).  Every step still copies its
+    # input in and all its result maps out inside the timed region.
     host_in = torch.from_numpy(img_np).pin_memory()
-    host_out = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in out.items()}
-    dev_in = torch.empty_like(img)
-
-    e2e_host_out = {}
-
-    def e2e_step():
-        dev_in.copy_(host_in, non_blocking=True)
-        nonlocal_img = dev_in
-        if sharded_mode and cfg == "c5":
-            _, _, sq = sharded.edt_column_striped(nonlocal_img, H5, W5, rank, world)
-            if "sq" not in e2e_host_out:
-                e2e_host_out["sq"] = torch.empty(sq.shape, dtype=sq.dtype).pin_memory()
-            e2e_host_out["sq"].copy_(sq, non_blocking=True)
-            return
-        if cfg == "c2":
-            dfc.edt_dual(nonlocal_img, out=out)
-        elif cfg in ("c1", "c5"):
-            dfc.edt(nonlocal_img, dist=cfg == "c1", out=out)
-        elif cfg == "c3":
-            dfc.edt_batched(nonlocal_img, dist=False, label=True, out=out)
-        else:
-            dfc.raster(nonlocal_img, out=out)
-        for k2, v in out.items():
-            host_out[k2].copy_(v, non_blocking=True)
-
-    e2e_steps = max(3, min(args.steps, 10))
+    streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    bufs = []
     for _ in range(2):
-        e2e_step()
+        o = {k: torch.empty_like(v) for k, v in out.items()}
+        bufs.append({"dev_in": torch.empty_like(img), "out": o,
+                     "host_out": {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in o.items()},
+                     "extra": {}})
+
+    def e2e_step(k):
+        bf = bufs[k & 1]
+        with torch.cuda.stream(streams[k & 1]):
+            bf["dev_in"].copy_(host_in, non_blocking=True)
+            x = bf["dev_in"]
+            o = bf["out"]
+            if sharded_mode and cfg == "c5":
+                _, _, sq = sharded.edt_column_striped(x, H5, W5, rank, world)
+                if "sq" not in bf["extra"]:
+                    bf["extra"]["sq"] = torch.empty(sq.shape, dtype=sq.dtype).pin_memory()
+                bf["extra"]["sq"].copy_(sq, non_blocking=True)
+                return
+            if cfg == "c2":
+                dfc.edt_dual(x, out=o)
+            elif cfg in ("c1", "c5"):
+                dfc.edt(x, dist=cfg == "c1", out=o)
+            elif cfg == "c3":
+                dfc.edt_batched(x, dist=False, label=True, out=o)
+            else:
+                dfc.raster(x, out=o)
+            for k2, v in o.items():
+                bf["host_out"][k2].copy_(v, non_blocking=True)
+
+    e2e_steps = max(4, min(args.steps, 10))
+    for k in range(2):
+        e2e_step(k)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     a.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
+    for s_ in streams:
+        s_.wait_event(a)
+    for k in range(e2e_steps):
+        e2e_step(k)
+    for s_ in streams:
+        stream.wait_stream(s_)
     b.record(stream)
     torch.cuda.synchronize()
     e2e_ms = a.elapsed_time(b) / e2e_steps
@@ -270,6 +284,8 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t[0])
+    host_out = bufs[0]["host_out"]
+    e2e_host_out = bufs[0]["extra"]
     h2d = int(host_in.numel() * host_in.element_size())
     d2h = int(sum(v.numel() * v.element_size() for v in host_out.values())) + \
         int(sum(v.numel() * v.element_size() for v in e2e_host_out.values()))
