@@ -209,10 +209,17 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
  * default, 1 = segment/merge kernel (k_rows), 2 = streaming lane-per-row
  * kernel (k_rows_stream, with k_rows as its overflow fallback), 3 = window
  * kernel (k_rows_win: per-segment stacks + bounded outward search, rows up to
- * 16384 columns; wider rows use k_rows).  Results are identical; this is a
- * performance/testing knob.
+ * 16384 columns; wider rows use k_rows), 4 = dense-row kernel (k_rows_dense)
+ * for rows with only short runs between object pixels and k_rows for the rest,
+ * 5 = lane-per-row chunk scan (k_rows_lr, with k_rows as its overflow
+ * fallback).  Results are identical; this is a performance/testing knob.
  */
 int dfc_set_row_kernel(int mode);
+
+/* Columns per warp chunk of the lane-per-row kernel (mode 5) for calls on the
+ * calling thread: a multiple of 32, 0 = default (DFC_LR_CHUNK or 512).
+ * Results are identical; a performance/testing knob. */
+int dfc_set_lr_chunk(int cols);
 
 /* Number of kernels the last successful call on this thread enqueued. */
 int dfc_last_launch_count(void);

@@ -50,6 +50,7 @@ _lib.dfc_last_cuda_error.restype = C.c_int
 _lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
 _lib.dfc_sqrt_i32.argtypes = [_vp, _vp, _i64, _vp]
 _lib.dfc_set_row_kernel.argtypes = [C.c_int]
+_lib.dfc_set_lr_chunk.argtypes = [C.c_int]
 _lib.dfc_column_nr_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
 _lib.dfc_rows_from_nr_u16.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp]
 _lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
@@ -62,7 +63,7 @@ _lib.dfc_labels_gray.argtypes = [_vp, _i64, _i64, _vp, _vp]
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
-    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel",
+    "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel", "dfc_set_lr_chunk",
     "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
 )
 
@@ -92,10 +93,18 @@ def set_profile_events(col_begin=None, row_begin=None, row_end=None) -> None:
     _check(_lib.dfc_set_profile_events(h(col_begin), h(row_begin), h(row_end)))
 
 
+def set_lr_chunk(cols: int) -> None:
+    """Columns per warp chunk of the "lr" row kernel (multiple of 32; 0 = default)."""
+    _check(_lib.dfc_set_lr_chunk(int(cols)))
+
+
 def set_row_kernel(mode: str) -> None:
-    """Stage-2 kernel for this thread's calls: "default", "segment", "stream" or
-    "window" (k_rows_win.cu, rows up to 16384 columns)."""
-    _check(_lib.dfc_set_row_kernel({"default": 0, "segment": 1, "stream": 2, "window": 3}[mode]))
+    """Stage-2 kernel for this thread's calls: "default", "segment", "stream",
+    "window" (k_rows_win.cu, rows up to 16384 columns), "dense" (k_rows_dense
+    for dense rows, the segment kernel for the rest) or "lr" (k_rows_lr.cu,
+    lane-per-row chunk scan)."""
+    _check(_lib.dfc_set_row_kernel(
+        {"default": 0, "segment": 1, "stream": 2, "window": 3, "dense": 4, "lr": 5}[mode]))
 
 
 def last_launch_count() -> int:

@@ -17,6 +17,7 @@ namespace {
 thread_local int g_last_cuda = 0;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+thread_local int g_lr_chunk = 0;  // k_rows_lr columns per warp chunk (0: default)
 thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming, 3: window,
                                   // 4: dense rows first, the rest by the segment kernel (default)
 
@@ -27,6 +28,8 @@ int env_row_mode() {
         if (v && strcmp(v, "stream") == 0) return 2;
         if (v && strcmp(v, "win") == 0) return 3;
         if (v && strcmp(v, "segment") == 0) return 1;
+        if (v && strcmp(v, "dense") == 0) return 4;
+        if (v && strcmp(v, "lr") == 0) return 5;
         return 4;  // default: dense-row kernel, then the segment/merge kernel for the other rows
     }();
     return m;
@@ -244,6 +247,55 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e);
+
+    // Lane-per-row chunk scan (k_rows_lr.cu) when the nr plane allows 16-byte
+    // loads; rows whose live stack overflows go to k_rows.
+    if (mode == 5 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 && a.tile_stride % 8 == 0 &&
+        a.nr_img_stride % 8 == 0) {
+        static const int chunk_env = [] {  // DFC_LR_CHUNK (tuning): columns per warp chunk
+            const char* v = getenv("DFC_LR_CHUNK");
+            const int c = v ? atoi(v) : 0;
+            return c >= 32 ? c & ~31 : 512;
+        }();
+        // chunk: a multiple of 32 columns, at most kLrCap*32 (the fill stages one
+        // row's list in the ring storage)
+        const int C = (int)std::min<int64_t>(std::min<int64_t>(round_up(W, 32), kLrCap * 32),
+                                             g_lr_chunk > 0 ? g_lr_chunk : chunk_env);
+        const int Ws = (int)round_up(W, 32);  // scratch row stride (16-byte granules of both lists)
+        const int64_t nchunks = (W + C - 1) / C;
+        const int64_t warps = (a.total_rows + 31) / 32 * nchunks;
+        const int64_t lblocks = (warps + kLrWarps - 1) / kLrWarps;
+        if (lblocks > 0x7fffffff) return DFC_ERR_SHAPE;
+        Scratch fl(st);
+        const size_t ent_bytes = (size_t)round_up(a.total_rows * Ws * 4, 256);
+        const size_t entr_bytes = (size_t)round_up(a.total_rows * Ws * 2, 256);
+        e = fl.alloc(ent_bytes + entr_bytes + (size_t)(a.total_rows + 1) * sizeof(int));
+        if (e != cudaSuccess) return cuda_fail(e);
+        uint32_t* ent = static_cast<uint32_t*>(fl.p);
+        uint16_t* entr = reinterpret_cast<uint16_t*>(static_cast<char*>(fl.p) + ent_bytes);
+        int* fail_count = reinterpret_cast<int*>(static_cast<char*>(fl.p) + ent_bytes + entr_bytes);
+        int* fail_rows = fail_count + 1;
+        e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        const void* lfn = take_new ? lr_kernel_ptr<true>() : lr_kernel_ptr<false>();
+        const int lsm = lr_smem_bytes();
+        e = cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm);
+        if (e != cudaSuccess) return cuda_fail(e);
+        int Cc = C, Wsc = Ws;
+        void* largs[] = {&a, &ent, &entr, &Wsc, &Cc, &fail_rows, &fail_count};
+        e = cudaLaunchKernel(lfn, dim3((unsigned)lblocks), dim3(32 * kLrWarps), largs, (size_t)lsm, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        ++g_launches;
+        RowArgs fb = a;  // fallback: the segment kernel over the overflowed rows
+        fb.row_list = fail_rows;
+        fb.row_count = fail_count;
+        void* fargs[] = {&fb};
+        const int64_t fblocks = std::min<int64_t>(blocks, 148 * 4);
+        e = cudaLaunchKernel(fn, dim3((unsigned)fblocks), dim3(g.R * g.T), fargs, (size_t)g.smem_bytes, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        ++g_launches;
+        return DFC_OK;
+    }
 
     // Streaming kernel (one lane = one row) when the nr plane allows coalesced
     // 16-byte tile loads; rows whose live stack overflows go to k_rows.
@@ -656,8 +708,14 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 }
 
 int dfc_set_row_kernel(int mode) {
-    if (mode < 0 || mode > 4) return DFC_ERR_ARG;
+    if (mode < 0 || mode > 5) return DFC_ERR_ARG;
     g_row_mode = mode;
+    return DFC_OK;
+}
+
+int dfc_set_lr_chunk(int cols) {
+    if (cols < 0 || cols % 32 != 0 || cols > 65536) return DFC_ERR_ARG;
+    g_lr_chunk = cols;
     return DFC_OK;
 }
 

@@ -1,0 +1,439 @@
+// k_rows_lr.cu -- stage 2 as a LANE-PER-ROW chunk scan with entry-level
+// eager finalisation, then a warp-cooperative fill.
+//
+// Same result as k_rows.cu (envelope_rows / meijster_scan / voronoi label
+// assembly, exact_edt.cpp:190-283, :362-369), different decomposition.  A warp
+// owns 32 consecutive rows and one column chunk [c0, c1); every lane runs the
+// reference's stack algorithm (exact_edt.cpp:208-223) over ITS row, left to
+// right (one 16-byte load = 8 columns, prefetched one group ahead).  There is
+// no merge step: the chunks of a row are independent.
+//
+//  bounds    owners are monotone in j (smallest and largest minimiser alike),
+//            so every owner of [c0, c1) lies in [owner(c0-1), owner(c1-1)]:
+//            each lane finds those two owners exactly (outward search from the
+//            column until the next unexamined distance d has d^2 > best) and
+//            scans only that range, at its own columns.
+//  domain    the envelope is kept over [F, c1) only: an empty stack pushes
+//            with start F (the first column not yet emitted), a parabola
+//            whose start lies past c1-1 is not pushed (:218 with cols -> c1).
+//  emission  every later parabola p >= m+1 has D_p(j) >= (m+1-j)^2 for
+//            j <= m+1.  The bottom entry (k_b, s_b) owns [s_b, e_b]; its value
+//            minus (m+1-j)^2 increases with j, so it is final once
+//                keep_old: g_b + (e_b-k_b)^2 <= (m+1-e_b)^2   (strict for take_new)
+//            and can no longer change (a later parabola cannot beat it in its
+//            range, so it can neither pop it nor start inside it).  Final
+//            entries leave the ring (kLrCap per lane, [entry][lane] in shared
+//            memory: each lane hits its own bank) and go to a per-row entry
+//            list in global scratch; the scan ends when the chunk's last
+//            entry is emitted.  A lane whose ring overflows gives its row to
+//            the merge-tree kernel (k_rows.cu, row-list mode).
+//  fill      lane = column: batches of rows have their lists staged into the
+//            idle ring storage (cp.async, all copies in flight), then the warp
+//            walks each row with a 32-entry window of the list (entry: column
+//            | start << 16, plus the column's nearest row).  Entries starting
+//            inside a 128-column block are marked in a 4-word mask (REDUX.OR);
+//            lane l owns columns b+4l..b+4l+3, and the owner of column c is
+//            the block's first owner plus the marks at or before c (popc).
+//            D, sqrt(D), label and nearest column leave with 16-byte stores.
+//            A block with 31 or more starts (a dense stretch) is done as one
+//            32-column block, lane = column.
+//
+// tests/lr_model.py is the statement-level model (fuzzed against brute force
+// for both tie rules, chunk widths 1..40).
+#include "dfc_kernels.cuh"
+
+namespace dfc {
+
+constexpr int kLrCap = 32;               // live entries per lane (ring, power of two)
+constexpr int kLrWarps = 4;              // warps per CTA
+constexpr uint32_t kLrInfK = 0xFFFFu;    // owner "column" of a featureless row
+
+struct LrSmem {
+    uint32_t ks[kLrCap][32];   // column | start << 16
+    uint16_t rr[kLrCap][32];   // nearest row of the column (vertical distance in vdist mode)
+};
+
+__device__ __forceinline__ const uint16_t* lr_col_ptr(const RowArgs& a, const uint16_t* rowp, int m) {
+    if (a.tile_cols >= a.W) return rowp + m;
+    const int t = m / a.tile_cols;
+    return rowp + t * a.tile_stride + (m - t * a.tile_cols);
+}
+
+template <bool TAKE_NEW>
+__global__ void __launch_bounds__(32 * kLrWarps) k_rows_lr(RowArgs a, uint32_t* ent, uint16_t* entr, int Ws,
+                                                           int C, int* fail_rows, int* fail_count) {
+    extern __shared__ uint4 lr_raw[];
+    LrSmem& sm = reinterpret_cast<LrSmem*>(lr_raw)[threadIdx.x >> 5];
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int W = a.W;
+    const int nchunks = (W + C - 1) / C;
+    const int64_t wid = (int64_t)blockIdx.x * kLrWarps + (threadIdx.x >> 5);
+    const int64_t band = wid / nchunks;
+    if (band * 32 >= a.total_rows) return;  // warp-uniform
+    const int c0 = (int)(wid - band * nchunks) * C, c1 = min(c0 + C, W);
+    const int64_t row = band * 32 + lane;
+    const bool active = row < a.total_rows;
+    const int img = active ? (int)(row / a.H) : 0;
+    const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
+    const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
+    const uint16_t* rowp = a.nr + (active ? img * a.nr_img_stride + (int64_t)i * a.Wp : 0);
+
+    auto load8 = [&](int m0) -> uint4 {
+        uint4 v = make_uint4(FULL, FULL, FULL, FULL);
+        if (active && m0 < W) {
+            v = __ldg(reinterpret_cast<const uint4*>(lr_col_ptr(a, rowp, m0)));
+            if (m0 + 8 > W) {  // columns past the row end: no candidate
+                const int valid = W - m0;  // 1..7
+                uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (2 * t >= valid) w[t] = FULL;
+                    else if (2 * t + 1 >= valid) w[t] |= 0xffff0000u;
+                }
+            }
+        }
+        return v;
+    };
+    auto half = [](const uint4& v, int t) -> uint32_t {
+        const uint32_t w = t < 2 ? (t == 0 ? v.x : v.y) : (t == 2 ? v.z : v.w);
+        return w;
+    };
+
+    // ---- exact scan bounds: the owners of the columns just left of the chunk
+    // and of its last column.  Owners are monotone in j under either tie rule,
+    // so every owner of [c0, c1) lies in [owner(c0-1), owner(c1-1)]: only those
+    // candidates are scanned.  Each lane searches its own row outward from b in
+    // 8-column groups until the nearest unexamined column d has d^2 > best. ----
+    auto owner_of = [&](int b) -> int {  // -1: the row has no candidate
+        uint32_t best = kInfU;
+        int bk = -1;
+        auto consider = [&](int k, uint32_t r) {
+            if (r == kNoRow) return;
+            const uint32_t av = gi > r ? gi - r : r - gi;
+            const int h = k - b;
+            const uint32_t v = av * av + (uint32_t)(h * h);
+            if (v < best || (v == best && (TAKE_NEW ? k > bk : k < bk))) {
+                best = v;
+                bk = k;
+            }
+        };
+        int lo = b & ~7, hi = lo + 8;  // examined columns [lo, hi)
+        bool go = active;
+        uint4 v = load8(lo);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) consider(lo + t, (half(v, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+        for (;;) {
+            const int dl = b - lo + 1, dr = hi - b;  // distance of the nearest unexamined column per side
+            const bool left = lo > 0 && (uint32_t)(dl * dl) <= best;
+            const bool right = hi < W && (uint32_t)(dr * dr) <= best;
+            go = go && (left || right);
+            if (!__any_sync(FULL, go)) break;
+            uint4 vl = make_uint4(FULL, FULL, FULL, FULL), vr = vl;
+            if (go && left) vl = load8(lo - 8);
+            if (go && right) vr = load8(hi);
+            if (go && left) {
+#pragma unroll
+                for (int t = 7; t >= 0; --t) consider(lo - 8 + t, (half(vl, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+                lo -= 8;
+            }
+            if (go && right) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) consider(hi + t, (half(vr, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+                hi += 8;
+            }
+        }
+        return bk;
+    };
+    int kS = 0, kE = W - 1;
+    bool featureless = false;
+    if (c0 > 0) {
+        kS = owner_of(c0 - 1);
+        featureless = kS < 0;
+    }
+    if (c1 < W) {
+        kE = owner_of(c1 - 1);
+        featureless = kE < 0;
+    }
+
+    // ---- scan ----
+    int n = 0, head = 0;                 // ring entries head .. head+n-1
+    int tk = 0, ts = 0;                  // top entry
+    uint32_t tg = 0;
+    int bk = 0, bs = 0, be = 0;          // bottom entry, last column of its range
+    uint32_t bg = 0;
+    int F = c0;                          // first column not yet emitted
+    int nout = 0;
+    bool done = !active, fail = false;
+    const int64_t eoff = active ? row * (int64_t)Ws + c0 : 0;
+    uint32_t* eout = ent + eoff;
+    uint16_t* rout = entr + eoff;
+
+    auto cand = [&](int m, uint32_t r) {
+        if (done || r == kNoRow) return;
+        const uint32_t av = gi > r ? gi - r : r - gi;
+        const uint32_t gm = av * av;
+        int start = F;
+        bool push = true;
+        while (n > 0) {
+            // num = g_m - g_k + m^2 - k^2, |num| < 2^31; ts*den, (c1-1)*den < 2^31
+            const int dm = m - tk;
+            const int num = (int)gm - (int)tg + dm * (m + tk);
+            const int den = 2 * dm;
+            const int lim = ts * den;  // start <= js[idx]: pop (:214)
+            if (TAKE_NEW ? num <= lim : num < lim) {
+                --n;
+                if (n > 0) {
+                    const int idx = (head + n - 1) & (kLrCap - 1);
+                    const uint32_t e = sm.ks[idx][lane];
+                    tk = (int)(e & 0xffffu);
+                    ts = (int)(e >> 16);
+                    const uint32_t rk = sm.rr[idx][lane];
+                    const uint32_t ak = gi > rk ? gi - rk : rk - gi;
+                    tg = ak * ak;
+                    if (n == 1) be = c1 - 1;
+                }
+                continue;
+            }
+            const int lim2 = (c1 - 1) * den;  // push iff start <= c1-1
+            push = TAKE_NEW ? num <= lim2 : num < lim2;
+            if (push) {  // 0 <= num, quotient < c1 <= 2^15
+                const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
+                // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
+                start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
+            }
+            break;
+        }
+        if (!push) return;
+        if (n == kLrCap) {  // ring full: the row goes to the merge-tree kernel
+            fail = true;
+            done = true;
+            n = 0;
+            fail_rows[atomicAdd(fail_count, 1)] = (int)row;
+            return;
+        }
+        const int idx = (head + n) & (kLrCap - 1);
+        sm.ks[idx][lane] = (uint32_t)m | ((uint32_t)start << 16);
+        sm.rr[idx][lane] = (uint16_t)r;
+        ++n;
+        tk = m;
+        ts = start;
+        tg = gm;
+        if (n == 1) {
+            bk = m;
+            bs = start;
+            bg = gm;
+            be = c1 - 1;
+        } else if (n == 2) {
+            be = start - 1;
+        }
+    };
+    auto pop_bottom = [&]() {  // emit the bottom entry, load the next one
+        rout[nout] = sm.rr[head][lane];
+        eout[nout++] = (uint32_t)bk | ((uint32_t)bs << 16);
+        F = be + 1;
+        head = (head + 1) & (kLrCap - 1);
+        --n;
+        if (n > 0) {
+            const uint32_t e = sm.ks[head][lane];
+            bk = (int)(e & 0xffffu);
+            bs = (int)(e >> 16);
+            const uint32_t rk = sm.rr[head][lane];
+            const uint32_t ak = gi > rk ? gi - rk : rk - gi;
+            bg = ak * ak;
+            be = n >= 2 ? (int)(sm.ks[(head + 1) & (kLrCap - 1)][lane] >> 16) - 1 : c1 - 1;
+        }
+    };
+    auto emit = [&](int m) {  // columns <= m scanned
+        while (n > 0) {
+            const int t = m + 1 - be, dd = be - bk;
+            const uint32_t d = bg + (uint32_t)(dd * dd), lim = (uint32_t)(t * t);
+            if (TAKE_NEW ? d >= lim : d > lim) break;
+            pop_bottom();
+            if (n == 0) done = true;  // the last entry owns through c1-1
+        }
+    };
+
+    // ---- scan [kS, kE], each lane at its own columns (8 per 16-byte load) ----
+    if (featureless) done = true;
+    int m0 = kS & ~7;
+    uint4 cur = load8(m0);
+    for (;;) {
+        const bool mine = !done && m0 <= kE;
+        if (!__any_sync(FULL, mine)) break;
+        const bool more = mine && m0 + 8 <= kE;
+        uint4 nxt = make_uint4(FULL, FULL, FULL, FULL);
+        if (more) nxt = load8(m0 + 8);
+        if (mine) {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) cand(m0 + t, (half(cur, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+            if (!done) emit(m0 + 7);
+        }
+        m0 += 8;
+        cur = nxt;
+    }
+    if (active && !fail) {  // no later candidate: everything left is final
+        while (n > 0) pop_bottom();
+        if (F < c1) {  // featureless row
+            rout[nout] = kNoRow;
+            eout[nout++] = kLrInfK | ((uint32_t)F << 16);
+        }
+        done = true;
+    }
+    __syncwarp();
+
+    // ---- fill: lane = column.  Rows are staged in batches: their entry lists
+    // (cp.async, 16-byte granules, L2) into the now idle ring storage ----
+    const int myn = (active && !fail) ? nout : 0;
+    const int maxn = (int)__reduce_max_sync(FULL, (unsigned)myn);
+    const int S = max(32, (maxn + 31) & ~31);          // staging stride per row (<= C <= kLrCap*32)
+    const int rpb = min(32, (kLrCap * 32) / S);         // rows per batch
+    uint32_t* sE = &sm.ks[0][0];
+    uint16_t* sR = &sm.rr[0][0];
+    const uint32_t sE_addr = (uint32_t)__cvta_generic_to_shared(sE);
+    const uint32_t sR_addr = (uint32_t)__cvta_generic_to_shared(sR);
+    for (int r0 = 0; r0 < 32; r0 += rpb) {
+        const int r1 = min(32, r0 + rpb);
+        __syncwarp();
+        for (int rho = r0; rho < r1; ++rho) {
+            const int nE = __shfl_sync(FULL, myn, rho);
+            const int64_t off = (band * 32 + rho) * (int64_t)Ws + c0;
+            const int slot = (rho - r0) * S;
+            for (int q = lane; 4 * q < nE; q += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sE_addr + 4u * (slot + 4 * q)),
+                             "l"(ent + off + 4 * q));
+            for (int q = lane; 8 * q < nE; q += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sR_addr + 2u * (slot + 8 * q)),
+                             "l"(entr + off + 8 * q));
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncwarp();
+        for (int rho = r0; rho < r1; ++rho) {
+            const int nE = __shfl_sync(FULL, myn, rho);
+            if (nE == 0) continue;  // failed (k_rows recomputes it) or no row
+            const uint32_t giR = __shfl_sync(FULL, gi, rho);
+            const int64_t rowR = band * 32 + rho;
+            const int imgR = (int)(rowR / a.H);
+            const int64_t iR = rowR - (int64_t)imgR * a.H;
+            int32_t* Drow = a.D ? reinterpret_cast<int32_t*>(a.D + imgR * a.sD) + iR * W : nullptr;
+            float* Srow = a.S ? reinterpret_cast<float*>(a.S + imgR * a.sS) + iR * W : nullptr;
+            int32_t* Lrow = a.LB ? reinterpret_cast<int32_t*>(a.LB + imgR * a.sL) + iR * W : nullptr;
+            int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + imgR * a.sN) + iR * W : nullptr;
+            const uint32_t* rE = sE + (rho - r0) * S;
+            const uint16_t* rR = sR + (rho - r0) * S;
+            const bool vec4 = a.vec;  // 16-byte stores legal (W % 4 == 0, aligned planes)
+            auto put = [&](int j, uint32_t d, uint32_t k, uint32_t r) {  // one column, scalar
+                const bool inf = k == kLrInfK;
+                if (Drow) __stcs(Drow + j, (int32_t)d);
+                if (Srow) __stcs(Srow + j, dist_f32(d));
+                if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(r * (uint32_t)W + k));
+                if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+            };
+            auto dval = [&](uint32_t g, uint32_t k, int j) -> uint32_t {
+                const int dj = j - (int)k;
+                return g == kInfU ? (uint32_t)DFC_INF_I32 : g + (uint32_t)(dj * dj);
+            };
+            int base = 0;  // entry owning column b
+            int b = c0;
+            while (b < c1) {
+                // window: lane e holds entry base + e; entries 1.. start after b-1
+                const int idx = base + lane;
+                const uint32_t we = idx < nE ? rE[idx] : FULL;
+                const uint32_t wr = idx < nE ? (uint32_t)rR[idx] : kNoRow;
+                const int s = (int)(we >> 16);
+                const uint32_t wk = we & 0xffffu;
+                const uint32_t wav = giR > wr ? giR - wr : wr - giR;
+                const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
+                const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
+                if (nin < 31) {
+                    // ---- 128-column block, 4 columns per lane: the window holds
+                    // every owner; bit (s-b)&31 of word (s-b)>>5 marks a start ----
+                    const bool in = lane >= 1 && s <= b + 127;
+                    const int off = s - b;
+                    uint32_t Zw[4];
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        Zw[w] = __reduce_or_sync(FULL, (in && (off >> 5) == w) ? 1u << (off & 31) : 0u);
+                    const int w = lane >> 3, bit = (4 * lane) & 31;
+                    const uint32_t Z = w == 0 ? Zw[0] : w == 1 ? Zw[1] : w == 2 ? Zw[2] : Zw[3];
+                    const int P = (w >= 1 ? __popc(Zw[0]) : 0) + (w >= 2 ? __popc(Zw[1]) : 0) +
+                                  (w >= 3 ? __popc(Zw[2]) : 0);
+                    const int o0 = P + __popc(Z & ((2u << bit) - 1u));
+                    const int o1 = o0 + (int)((Z >> (bit + 1)) & 1u);
+                    const int o2 = o1 + (int)((Z >> (bit + 2)) & 1u);
+                    const int o3 = o2 + (int)((Z >> (bit + 3)) & 1u);
+                    uint32_t k0 = __shfl_sync(FULL, wk, o0), g0 = __shfl_sync(FULL, wg, o0);
+                    uint32_t k3 = __shfl_sync(FULL, wk, o3), g3 = __shfl_sync(FULL, wg, o3);
+                    uint32_t k1 = o1 == o0 ? k0 : k3, g1 = o1 == o0 ? g0 : g3;
+                    uint32_t k2 = o2 == o3 ? k3 : k0, g2 = o2 == o3 ? g3 : g0;
+                    if (__any_sync(FULL, o3 - o0 >= 2)) {  // three or more owners in 4 columns
+                        k1 = __shfl_sync(FULL, wk, o1);
+                        g1 = __shfl_sync(FULL, wg, o1);
+                        k2 = __shfl_sync(FULL, wk, o2);
+                        g2 = __shfl_sync(FULL, wg, o2);
+                    }
+                    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+                    if (Lrow) {
+                        r0 = __shfl_sync(FULL, wr, o0);
+                        r1 = __shfl_sync(FULL, wr, o1);
+                        r2 = __shfl_sync(FULL, wr, o2);
+                        r3 = __shfl_sync(FULL, wr, o3);
+                    }
+                    const int j = b + 4 * lane;
+                    const uint32_t d0 = dval(g0, k0, j), d1 = dval(g1, k1, j + 1);
+                    const uint32_t d2 = dval(g2, k2, j + 2), d3 = dval(g3, k3, j + 3);
+                    if (vec4 && j + 3 < c1) {
+                        if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
+                        if (Srow)
+                            __stcs(reinterpret_cast<float4*>(Srow + j),
+                                   make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
+                        if (Lrow) {
+                            auto lab = [&](uint32_t k, uint32_t r) {
+                                return k == kLrInfK ? -1 : (int32_t)(r * (uint32_t)W + k);
+                            };
+                            __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab(k0, r0), lab(k1, r1), lab(k2, r2), lab(k3, r3)));
+                        }
+                        if (Nrow) {
+                            auto nc = [&](uint32_t k) { return k == kLrInfK ? -1 : (int32_t)k; };
+                            __stcs(reinterpret_cast<int4*>(Nrow + j), make_int4(nc(k0), nc(k1), nc(k2), nc(k3)));
+                        }
+                    } else {
+                        if (j < c1) put(j, d0, k0, r0);
+                        if (j + 1 < c1) put(j + 1, d1, k1, r1);
+                        if (j + 2 < c1) put(j + 2, d2, k2, r2);
+                        if (j + 3 < c1) put(j + 3, d3, k3, r3);
+                    }
+                    // the next block's first owner: the last entry starting <= b+128
+                    const int sn = __shfl_sync(FULL, s, min(nin + 1, 31));
+                    base += nin + ((nin + 1 <= 31 && sn == b + 128) ? 1 : 0);
+                    b += 128;
+                } else {
+                    // ---- dense stretch: one 32-column block, lane = column ----
+                    const bool in = lane >= 1 && s <= b + 31;
+                    const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
+                    const int ow = __popc(Z & ((2u << lane) - 1u));
+                    const uint32_t k = __shfl_sync(FULL, wk, ow);
+                    const uint32_t g = __shfl_sync(FULL, wg, ow);
+                    const uint32_t r = __shfl_sync(FULL, wr, ow);
+                    const int j = b + lane;
+                    if (j < c1) put(j, dval(g, k, j), k, r);
+                    // the next block's first owner: the last entry starting <= b+32
+                    // (up to 32 entries after base: entry base+32 is read by lane 0)
+                    const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (rE[base + 32] >> 16) : 0xffffu;
+                    base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
+                            ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
+                    b += 32;
+                }
+            }
+        }
+    }
+}
+
+template <bool TAKE_NEW>
+inline const void* lr_kernel_ptr() {
+    return (const void*)k_rows_lr<TAKE_NEW>;
+}
+
+inline int lr_smem_bytes() { return kLrWarps * (int)sizeof(LrSmem); }
+
+}  // namespace dfc

@@ -372,3 +372,51 @@ def test_dense_rows_border_gaps_and_ties(dfc):
     small = np.ones((6, 200), np.uint8)
     small[2] = 0           # a full-width gap row (no zero at all in the row)
     _check_edt(dfc, small)
+
+
+@pytest.fixture(params=[0, 32, 96])
+def lr_kernel(dfc, request):
+    """The lane-per-row chunk scan (k_rows_lr.cu) at the default chunk width and
+    at narrow chunks (many chunks per row: warm-ups and cross-chunk owners)."""
+    dfc.set_row_kernel("lr")
+    dfc.set_lr_chunk(request.param)
+    yield dfc
+    dfc.set_lr_chunk(0)
+    dfc.set_row_kernel("default")
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (33, 97), (64, 64), (40, 1031), (70, 600), (3, 4100), (100, 33)])
+@pytest.mark.parametrize("density", [0.0, 0.002, 0.02, 0.3, 1.0])
+def test_lr_row_kernel(lr_kernel, shape, density):
+    """The lane-per-row chunk scan gives the same maps, labels and columns."""
+    img = oracle.random_image(shape[0], shape[1], density, 13 * shape[0] + shape[1] + int(density * 1000))
+    _check_edt(lr_kernel, img)
+
+
+def test_lr_overflow_falls_back(lr_kernel):
+    """Equal-height parabolas under a far object line keep many entries alive per
+    row: rows beyond the ring capacity are recomputed exactly by k_rows."""
+    img = np.zeros((300, 257), np.uint8)
+    img[0, :] = 1
+    img[299, 100] = 1
+    _check_edt(lr_kernel, img)
+    img2 = np.zeros((200, 512), np.uint8)
+    img2[0, ::2] = 1
+    _check_edt(lr_kernel, img2)
+
+
+def test_lr_batched_dual_and_discs(lr_kernel):
+    from paper_2106_03503_b200 import workloads
+    imgs = workloads.points_batch(40, 96, 128, 30, 5)
+    out = lr_kernel.edt_batched(_dev(imgs), dist=True, label=True)
+    img = workloads.discs(256, 384, 10, 3)
+    dual = lr_kernel.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    for b in range(0, 40, 7):
+        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
+        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
+    np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+    np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
+    _check_edt(lr_kernel, img)
+    _check_edt(lr_kernel, img, polarity=1)
+    _check_edt(lr_kernel, workloads.discs(512, 1000, 12, 9))
