@@ -239,6 +239,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.row_count = nullptr;
     a.vec_nr = false;
     a.row_done = nullptr;
+    a.lr_gate = false;
     a.plane_counts = plane_counts;
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
     if (mode == 3 && W <= 16384) return row_pass_win(a, take_new, st);
@@ -248,44 +249,54 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e);
 
-    // Lane-per-row chunk scan (k_rows_lr.cu) when the nr plane allows 16-byte
-    // loads; rows whose live stack overflows go to k_rows.
-    if (mode == 5 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 && a.tile_stride % 8 == 0 &&
-        a.nr_img_stride % 8 == 0) {
-        static const int chunk_env = [] {  // DFC_LR_CHUNK (tuning): columns per warp chunk
-            const char* v = getenv("DFC_LR_CHUNK");
-            const int c = v ? atoi(v) : 0;
-            return c >= 32 ? c & ~31 : 512;
-        }();
-        // chunk: a multiple of 32 columns, at most kLrCap*32 (the fill stages one
-        // row's list in the ring storage)
-        const int C = (int)std::min<int64_t>(std::min<int64_t>(round_up(W, 32), kLrCap * 32),
-                                             g_lr_chunk > 0 ? g_lr_chunk : chunk_env);
-        const int Ws = (int)round_up(W, 32);  // scratch row stride (16-byte granules of both lists)
-        const int64_t nchunks = (W + C - 1) / C;
-        const int64_t warps = (a.total_rows + 31) / 32 * nchunks;
+    // Lane-per-row chunk scan (k_rows_lr.cu): needs 16-byte nr loads.
+    const bool lr_ok = aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 && a.tile_stride % 8 == 0 &&
+                       a.nr_img_stride % 8 == 0;
+    static const int chunk_env = [] {  // DFC_LR_CHUNK (tuning): columns per warp chunk
+        const char* v = getenv("DFC_LR_CHUNK");
+        const int c = v ? atoi(v) : 0;
+        return c >= 32 ? c & ~31 : 1024;
+    }();
+    // chunk: a multiple of 32 columns, at most kLrCap*32 (the fill stages one row's
+    // list in the ring storage)
+    const int lrC = (int)std::min<int64_t>(std::min<int64_t>(round_up(W, 32), kLrCap * 32),
+                                           g_lr_chunk > 0 ? g_lr_chunk : chunk_env);
+    const int lrWs = (int)round_up(W, 32);  // scratch row stride (16-byte granules of both lists)
+    const size_t ent_bytes = (size_t)round_up(a.total_rows * lrWs * 4, 256);
+    const size_t entr_bytes = (size_t)round_up(a.total_rows * lrWs * 2, 256);
+    auto launch_lr = [&](RowArgs la, void* scratch, int* fail_rows, int* fail_count) -> int {
+        const int64_t nchunks = (W + lrC - 1) / lrC;
+        const int64_t warps = (la.total_rows + 31) / 32 * nchunks;
         const int64_t lblocks = (warps + kLrWarps - 1) / kLrWarps;
         if (lblocks > 0x7fffffff) return DFC_ERR_SHAPE;
+        uint32_t* ent = static_cast<uint32_t*>(scratch);
+        uint16_t* entr = reinterpret_cast<uint16_t*>(static_cast<char*>(scratch) + ent_bytes);
+        const void* lfn = take_new ? lr_kernel_ptr<true>() : lr_kernel_ptr<false>();
+        const int lsm = lr_smem_bytes();
+        cudaError_t le = cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm);
+        if (le != cudaSuccess) return cuda_fail(le);
+        int Cc = lrC, Wsc = lrWs;
+        void* largs[] = {&la, &ent, &entr, &Wsc, &Cc, &fail_rows, &fail_count};
+        le = cudaLaunchKernel(lfn, dim3((unsigned)lblocks), dim3(32 * kLrWarps), largs, (size_t)lsm, st);
+        if (le != cudaSuccess) return cuda_fail(le);
+        ++g_launches;
+        return DFC_OK;
+    };
+
+    // Mode 5: every row by k_rows_lr; rows whose live stack overflows go to k_rows.
+    if (mode == 5 && lr_ok) {
         Scratch fl(st);
-        const size_t ent_bytes = (size_t)round_up(a.total_rows * Ws * 4, 256);
-        const size_t entr_bytes = (size_t)round_up(a.total_rows * Ws * 2, 256);
         e = fl.alloc(ent_bytes + entr_bytes + (size_t)(a.total_rows + 1) * sizeof(int));
         if (e != cudaSuccess) return cuda_fail(e);
-        uint32_t* ent = static_cast<uint32_t*>(fl.p);
-        uint16_t* entr = reinterpret_cast<uint16_t*>(static_cast<char*>(fl.p) + ent_bytes);
         int* fail_count = reinterpret_cast<int*>(static_cast<char*>(fl.p) + ent_bytes + entr_bytes);
         int* fail_rows = fail_count + 1;
         e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
         if (e != cudaSuccess) return cuda_fail(e);
-        const void* lfn = take_new ? lr_kernel_ptr<true>() : lr_kernel_ptr<false>();
-        const int lsm = lr_smem_bytes();
-        e = cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm);
-        if (e != cudaSuccess) return cuda_fail(e);
-        int Cc = C, Wsc = Ws;
-        void* largs[] = {&a, &ent, &entr, &Wsc, &Cc, &fail_rows, &fail_count};
-        e = cudaLaunchKernel(lfn, dim3((unsigned)lblocks), dim3(32 * kLrWarps), largs, (size_t)lsm, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        ++g_launches;
+        RowArgs la = a;
+        la.lr_gate = false;
+        la.row_done = nullptr;
+        int rc = launch_lr(la, fl.p, fail_rows, fail_count);
+        if (rc != DFC_OK) return rc;
         RowArgs fb = a;  // fallback: the segment kernel over the overflowed rows
         fb.row_list = fail_rows;
         fb.row_count = fail_count;
@@ -297,31 +308,67 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         return DFC_OK;
     }
 
-    // Streaming kernel (one lane = one row) when the nr plane allows coalesced
-    // 16-byte tile loads; rows whose live stack overflows go to k_rows.
-    if (mode == 4 && W <= kDenseMaxW) {
-        // dense rows (short runs between object pixels) by k_rows_dense, which
-        // flags them; the segment kernel then skips the flagged rows
+    // Default: per plane by its object count (column pass) -- dense planes
+    // (>= 50% object pixels, W <= kDenseMaxW) by k_rows_dense, sparse planes
+    // (< 1/256) by k_rows_lr, the rest (and rows those two flag) by k_rows.
+    if (mode == 4) {
+        const bool dense_on = W <= kDenseMaxW;
+        const bool lr_on = lr_ok && plane_counts != nullptr;
         Scratch fl(st);
-        e = fl.alloc((size_t)a.total_rows);
+        const size_t flag_bytes = (size_t)round_up(a.total_rows, 256);
+        const size_t list_bytes = (size_t)round_up((a.total_rows + 1) * 4, 256);
+        e = fl.alloc(flag_bytes + list_bytes + (lr_on ? ent_bytes + entr_bytes : 0));
         if (e != cudaSuccess) return cuda_fail(e);
         a.row_done = static_cast<uint8_t*>(fl.p);
-        a.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0 && a.tile_cols >= W;
-        const void* dfn = take_new ? dense_kernel_ptr<true>() : dense_kernel_ptr<false>();
-        const int dsm = dense_smem_bytes((int)W);
-        e = cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+        int* rest_count = reinterpret_cast<int*>(static_cast<char*>(fl.p) + flag_bytes);
+        int* rest_rows = rest_count + 1;
+        e = cudaMemsetAsync(a.row_done, 0, flag_bytes + 4, st);  // flags and the list count
         if (e != cudaSuccess) return cuda_fail(e);
-        const int64_t dblocks = std::min<int64_t>((a.total_rows + kDenseWarps - 1) / kDenseWarps, 148 * 16);
-        void* dargs[] = {&a};
-        e = cudaLaunchKernel(dfn, dim3((unsigned)dblocks), dim3(32 * kDenseWarps), dargs, (size_t)dsm, st);
-        if (e != cudaSuccess) return cuda_fail(e);
+        a.lr_gate = lr_on;
+        if (dense_on) {  // dense rows (short runs between object pixels): flagged 1
+            a.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0 && a.tile_cols >= W;
+            const void* dfn = take_new ? dense_kernel_ptr<true>() : dense_kernel_ptr<false>();
+            const int dsm = dense_smem_bytes((int)W);
+            e = cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+            if (e != cudaSuccess) return cuda_fail(e);
+            const int64_t dblocks = std::min<int64_t>((a.total_rows + kDenseWarps - 1) / kDenseWarps, 148 * 16);
+            void* dargs[] = {&a};
+            e = cudaLaunchKernel(dfn, dim3((unsigned)dblocks), dim3(32 * kDenseWarps), dargs, (size_t)dsm, st);
+            if (e != cudaSuccess) return cuda_fail(e);
+            ++g_launches;
+        }
+        if (lr_on) {  // rows of sparse planes; overflowed rows flagged 2
+            const int rc = launch_lr(a, static_cast<char*>(fl.p) + flag_bytes + list_bytes, nullptr, nullptr);
+            if (rc != DFC_OK) return rc;
+        }
+        // the segment kernel over the remaining rows: few rows -> one CTA group per
+        // row group, skipping flagged rows (cheapest); many rows -> a compact
+        // list first, so that skipped rows cost no CTA launch
+        if (a.total_rows <= 16384) {
+            void* args[] = {&a};
+            e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+            if (e != cudaSuccess) return cuda_fail(e);
+            ++g_launches;
+            return DFC_OK;
+        }
+        const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
+        k_rows_rest<<<(unsigned)rblocks, 256, 0, st>>>(a.row_done, plane_counts, a.total_rows, (int)H, (int)W,
+                                                       a.lr_gate, rest_rows, rest_count);
         ++g_launches;
-        void* args[] = {&a};
-        e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+        RowArgs ra = a;
+        ra.row_list = rest_rows;
+        ra.row_count = rest_count;
+        ra.row_done = nullptr;
+        void* args[] = {&ra};
+        const int64_t sblocks = std::min<int64_t>(blocks, 148 * 64);
+        e = cudaLaunchKernel(fn, dim3((unsigned)sblocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
         if (e != cudaSuccess) return cuda_fail(e);
         ++g_launches;
         return DFC_OK;
     }
+
+    // Streaming kernel (one lane = one row) when the nr plane allows coalesced
+    // 16-byte tile loads; rows whose live stack overflows go to k_rows.
     const bool stream_ok = mode == 2 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
                            a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
     if (stream_ok) {

@@ -38,7 +38,8 @@ struct RowArgs {
     bool vdist;               // nr holds vertical DISTANCES a (g = a^2), not rows
     const int* row_list;      // fallback mode: process only these rows (nullptr: all)
     const int* row_count;     // number of entries in row_list (device)
-    uint8_t* row_done;        // per row: 1 = written by k_rows_dense (the segment kernel skips it)
+    uint8_t* row_done;        // per row: 1 = written by k_rows_dense, 2 = k_rows_lr overflowed
+    bool lr_gate;             // rows of sparse planes belong to k_rows_lr (unless row_done == 2)
     const unsigned long long* plane_counts;  // object pixels per plane (dense gate), nullable
 };
 
@@ -51,6 +52,12 @@ struct RasterArgs {
     int32_t* chess;
     int32_t* cham;
 };
+
+// Sparse plane (object pixels < 1/256 of the plane): its rows go to the
+// lane-per-row kernel (k_rows_lr.cu) in the default mode.
+__host__ __device__ __forceinline__ bool lr_plane(const unsigned long long* counts, int img, int H, int W) {
+    return counts != nullptr && counts[img] * 256ull < (unsigned long long)H * (unsigned long long)W;
+}
 
 // The kernels themselves are defined in k_columns.cu / k_rows.cu / k_raster.cu and
 // compiled in ONE translation unit with the C ABI (dfc_all.cu), so no

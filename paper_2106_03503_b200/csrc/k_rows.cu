@@ -141,8 +141,12 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
         active = row < *a.row_count;
         row = active ? a.row_list[row] : 0;
     }
-    if (a.row_done) {  // rows k_rows_dense already wrote
-        if (active && a.row_done[row]) active = false;
+    if (a.row_done) {  // rows k_rows_dense / k_rows_lr already wrote
+        if (active) {
+            const uint8_t rd = a.row_done[row];
+            if (rd == 1 || (a.lr_gate && rd != 2 && lr_plane(a.plane_counts, (int)(row / a.H), a.H, a.W)))
+                active = false;
+        }
         if (__syncthreads_and(!active)) return;  // CTA-uniform
     }
     const int img = active ? (int)(row / a.H) : 0;

@@ -48,8 +48,10 @@ __global__ void __launch_bounds__(32 * kDenseWarps) k_rows_dense(RowArgs a) {
         const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
         const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
         // plane gate: fewer than half object pixels -> no short-run rows worth the staging
+        // (row_done is zeroed by the caller); skip the rest of the plane at once
         if (a.plane_counts && 2 * a.plane_counts[img] < (unsigned long long)a.H * (unsigned long long)W) {
-            if (lane == 0) a.row_done[row] = 0;
+            const int64_t end = (int64_t)(img + 1) * a.H, stride = (int64_t)gridDim.x * kDenseWarps;
+            row += ((end - row + stride - 1) / stride - 1) * stride;  // the loop step passes `end`
             continue;
         }
 

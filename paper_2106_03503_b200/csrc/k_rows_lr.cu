@@ -26,7 +26,9 @@
 //            memory: each lane hits its own bank) and go to a per-row entry
 //            list in global scratch; the scan ends when the chunk's last
 //            entry is emitted.  A lane whose ring overflows gives its row to
-//            the merge-tree kernel (k_rows.cu, row-list mode).
+//            the merge-tree kernel (k_rows.cu: row-list mode, or row_done = 2
+//            in the default mode, where this kernel takes the rows of sparse
+//            planes -- lr_plane -- and k_rows / k_rows_dense the others).
 //  fill      lane = column: batches of rows have their lists staged into the
 //            idle ring storage (cp.async, all copies in flight), then the warp
 //            walks each row with a 32-entry window of the list (entry: column
@@ -60,7 +62,7 @@ __device__ __forceinline__ const uint16_t* lr_col_ptr(const RowArgs& a, const ui
 }
 
 template <bool TAKE_NEW>
-__global__ void __launch_bounds__(32 * kLrWarps) k_rows_lr(RowArgs a, uint32_t* ent, uint16_t* entr, int Ws,
+__global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_t* ent, uint16_t* entr, int Ws,
                                                            int C, int* fail_rows, int* fail_count) {
     extern __shared__ uint4 lr_raw[];
     LrSmem& sm = reinterpret_cast<LrSmem*>(lr_raw)[threadIdx.x >> 5];
@@ -73,8 +75,12 @@ __global__ void __launch_bounds__(32 * kLrWarps) k_rows_lr(RowArgs a, uint32_t* 
     if (band * 32 >= a.total_rows) return;  // warp-uniform
     const int c0 = (int)(wid - band * nchunks) * C, c1 = min(c0 + C, W);
     const int64_t row = band * 32 + lane;
-    const bool active = row < a.total_rows;
+    bool active = row < a.total_rows;
     const int img = active ? (int)(row / a.H) : 0;
+    if (a.lr_gate) {  // default mode: only the rows of sparse planes
+        active = active && lr_plane(a.plane_counts, img, a.H, a.W);
+        if (!__any_sync(FULL, active)) return;
+    }
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
     const uint16_t* rowp = a.nr + (active ? img * a.nr_img_stride + (int64_t)i * a.Wp : 0);
@@ -209,7 +215,8 @@ __global__ void __launch_bounds__(32 * kLrWarps) k_rows_lr(RowArgs a, uint32_t* 
             fail = true;
             done = true;
             n = 0;
-            fail_rows[atomicAdd(fail_count, 1)] = (int)row;
+            if (a.row_done) a.row_done[row] = 2;  // default mode: k_rows picks it up
+            else fail_rows[atomicAdd(fail_count, 1)] = (int)row;
             return;
         }
         const int idx = (head + n) & (kLrCap - 1);
@@ -426,6 +433,25 @@ __global__ void __launch_bounds__(32 * kLrWarps) k_rows_lr(RowArgs a, uint32_t* 
                 }
             }
         }
+    }
+}
+
+// Rows the segment kernel still has to do in the default mode: not written by
+// k_rows_dense (flag 1), and not a sparse-plane row k_rows_lr completed
+// (sparse plane, flag != 2).  Appended to a list (any order).
+__global__ void k_rows_rest(const uint8_t* row_done, const unsigned long long* counts, int64_t total_rows,
+                            int H, int W, bool lr_gate, int* list, int* count) {
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < total_rows;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t rd = row_done[row];
+        const bool mine = rd == 2 || (rd == 0 && !(lr_gate && lr_plane(counts, (int)(row / H), H, W)));
+        const unsigned m = __ballot_sync(__activemask(), mine);
+        if (m == 0) continue;
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(count, __popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (mine) list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
     }
 }
 
