@@ -649,9 +649,30 @@ int dfc_rows_from_nr_u16(const uint16_t* d_nr, int64_t rows, int64_t cols, int64
     init_pool_once();
     g_launches = 0;
     prof(1, (cudaStream_t)stream);
+    // object pixels of this row stripe (the per-plane kernel choice of row_pass)
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch cs(st);
+    cudaError_t ce = cs.alloc(sizeof(unsigned long long));
+    if (ce != cudaSuccess) return cuda_fail(ce);
+    auto* counts = static_cast<unsigned long long*>(cs.p);
+    ce = cudaMemsetAsync(counts, 0, sizeof(unsigned long long), st);
+    if (ce != cudaSuccess) return cuda_fail(ce);
+    {
+        RowArgs ca{};
+        ca.nr = d_nr;
+        ca.Wp = (int)std::min<int64_t>(tile_cols, 1 << 30);
+        ca.tile_cols = ca.Wp;
+        ca.tile_stride = tile_stride_elems;
+        ca.row0 = (int)row0;
+        ca.H = (int)rows;
+        ca.W = (int)cols;
+        ca.total_rows = rows;
+        k_nr_count<<<(unsigned)std::min<int64_t>(rows, 148 * 8), 256, 0, st>>>(ca, counts);
+        ++g_launches;
+    }
     const int rc = row_pass(d_nr, 1, rows, cols, (int)std::min<int64_t>(tile_cols, 1 << 30), take_new != 0,
-                            d_sqdist, 0, d_dist, 0, d_label, 0, d_nearest_col, 0, (cudaStream_t)stream, false,
-                            (int)std::min<int64_t>(tile_cols, 1 << 30), tile_stride_elems, (int)row0);
+                            d_sqdist, 0, d_dist, 0, d_label, 0, d_nearest_col, 0, st, false,
+                            (int)std::min<int64_t>(tile_cols, 1 << 30), tile_stride_elems, (int)row0, counts);
     if (rc != DFC_OK) return rc;
     prof(2, (cudaStream_t)stream);
     const cudaError_t e = cudaGetLastError();

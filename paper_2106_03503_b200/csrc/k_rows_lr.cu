@@ -455,6 +455,19 @@ __global__ void k_rows_rest(const uint8_t* row_done, const unsigned long long* c
     }
 }
 
+// Object pixels of a (possibly column-tiled) nearest-row plane: cells whose
+// nearest object row is their own row (the sparse-plane gate of
+// dfc_rows_from_nr_u16, where no column pass of the whole image ran here).
+__global__ void k_nr_count(RowArgs a, unsigned long long* count) {
+    unsigned long long c = 0;
+    for (int64_t i = blockIdx.x; i < a.total_rows; i += gridDim.x) {
+        const uint16_t* rowp = a.nr + i * a.Wp;
+        for (int j = threadIdx.x; j < a.W; j += blockDim.x) c += __ldg(lr_col_ptr(a, rowp, j)) == (uint32_t)(i + a.row0);
+    }
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
 template <bool TAKE_NEW>
 inline const void* lr_kernel_ptr() {
     return (const void*)k_rows_lr<TAKE_NEW>;

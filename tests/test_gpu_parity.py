@@ -228,14 +228,17 @@ def test_envelope_from_vertical_plane(dfc, shape):
     np.testing.assert_array_equal(out["dist"].cpu().numpy(), oracle.sqrt_f32(oracle.to_i32(d)))
 
 
+@pytest.mark.parametrize("p", [0.02, 0.002])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_column_striped_path_emulated(dfc, world):
+def test_column_striped_path_emulated(dfc, world, p):
     """C5 path on one GPU: every 'rank' runs the real stage-1 kernel on its column
     stripe; the all-to-all is emulated by slicing; the real stage-2 kernel reads
-    the N tiles in place with global row numbers (dfc_rows_from_nr_u16)."""
+    the N tiles in place with global row numbers (dfc_rows_from_nr_u16).  At
+    p = 0.002 the row stripes are sparse planes (< 1/256 object pixels): the
+    lane-per-row kernel reads the tiles."""
     from paper_2106_03503_b200 import sharded, workloads
-    H, W = 96, 256
-    img = workloads.sparse_tiles(H, W, tile=32, n_on=6, p=0.02, seed=11 + world)
+    H, W = (96, 256) if p > 0.01 else (256, 1024)
+    img = workloads.sparse_tiles(H, W, tile=32, n_on=6 if p > 0.01 else 64, p=p, seed=11 + world)
     ops = sharded.KernelOps()
     Ws = W // world
     stripes = [ops.column_nr(_dev(np.ascontiguousarray(img[:, r * Ws:(r + 1) * Ws]))) for r in range(world)]

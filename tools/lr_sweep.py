@@ -23,7 +23,7 @@ else:
     calls = {"pol0": lambda: dfc.edt(img, polarity=0, dist=True), "pol1": lambda: dfc.edt(img, polarity=1, dist=True),
              "dual": lambda: dfc.edt_dual(img)}
 ref = {}
-for mode in ["default", "lr"]:
+for mode in (["default"] if chunks == [0] else ["default", "lr"]):
     dfc.set_row_kernel(mode)
     for ch in ([0] if mode == "default" else chunks):
         dfc.set_lr_chunk(ch)
