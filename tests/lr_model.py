@@ -18,45 +18,52 @@ no longer change (a later parabola cannot beat it anywhere in [sb, eb], so it
 can neither pop it nor start inside it).  The scan stops once the stack is
 empty after the chunk's last entry has been emitted.
 
-Warm-up: see warmup_start (no column left of S0 owns a column of the chunk).
+Bounds: owners are monotone in j under either tie rule, so every owner of
+[c0, c1) lies in [owner(c0-1), owner(c1-1)]; only that range is scanned.
 
 Test infrastructure only.
 """
 
 
-def isqrt_floor(x):
-    import math
-    return math.isqrt(x)
-
-
-def warmup_start(g, c0):
-    """S0 for chunk start c0 (0 if no candidate lies at or right of c0).
-
-    U = min over candidates F >= c0 of g_F + (F-c0)^2 bounds D(c0); sqrt(D) is
-    1-Lipschitz, so every column j >= c0 has sqrt(D(j)) <= sqrt(U) + (j-c0), and
-    its owner k (with (j-k)^2 <= D(j)) satisfies k >= c0 - floor(sqrt(U))."""
-    import math
+def owner(g, b, take_new=False):
+    """Owner of column b (smallest minimising column for keep_old, largest for
+    take_new), by the kernel's outward search: stop once the nearest
+    unexamined column d has d^2 > best.  None for a featureless row."""
     W = len(g)
-    U = None
-    for F in range(c0, W):
-        if U is not None and (F - c0) ** 2 >= U:
-            break
-        if g[F] is not None:
-            v = g[F] + (F - c0) ** 2
-            U = v if U is None else min(U, v)
-    if U is None:
-        return 0
-    return max(0, c0 - math.isqrt(U))
+    best, bk = None, None
+    lo, hi = b, b + 1  # examined [lo, hi)
+
+    def consider(k):
+        nonlocal best, bk
+        if g[k] is None:
+            return
+        v = g[k] + (k - b) ** 2
+        if best is None or v < best or (v == best and (k > bk if take_new else k < bk)):
+            best, bk = v, k
+
+    consider(b)
+    while True:
+        dl, dr = b - lo + 1, hi - b
+        left = lo > 0 and (best is None or dl * dl <= best)
+        right = hi < W and (best is None or dr * dr <= best)
+        if not (left or right):
+            return bk
+        if left:
+            lo -= 1
+            consider(lo)
+        if right:
+            consider(hi)
+            hi += 1
 
 
-def scan_chunk(g, c0, c1, S0, take_new=False, cap=None):
+def scan_chunk(g, c0, c1, kS, kE, take_new=False, cap=None):
     """Returns (entries, stats): entries = [(start, k)] covering [c0, c1) in order
     (k None: featureless row), stats = dict(last_m, max_live, pops, pushes)."""
     W = len(g)
     st = []        # live entries [k, start]
     out = []
     F = [c0]       # first column not yet emitted
-    stats = dict(max_live=0, pops=0, pushes=0, last_m=S0 - 1)
+    stats = dict(max_live=0, pops=0, pushes=0, last_m=kS - 1)
 
     def floor_div(a, b):
         return a // b
@@ -79,7 +86,7 @@ def scan_chunk(g, c0, c1, S0, take_new=False, cap=None):
         return False
 
     done = False
-    for m in range(S0, W):
+    for m in range(kS, kE + 1):
         stats["last_m"] = m
         if g[m] is not None:
             gm = g[m]
@@ -137,8 +144,13 @@ def lr_row(g, C, take_new=False):
     D, K = [], []
     for c0 in range(0, W, C):
         c1 = min(c0 + C, W)
-        S0 = warmup_start(g, c0)
-        ent, _ = scan_chunk(g, c0, c1, S0, take_new)
+        kS = owner(g, c0 - 1, take_new) if c0 > 0 else 0
+        kE = owner(g, c1 - 1, take_new) if c1 < W else W - 1
+        if kS is None or kE is None:  # featureless row
+            D += [None] * (c1 - c0)
+            K += [None] * (c1 - c0)
+            continue
+        ent, _ = scan_chunk(g, c0, c1, kS, kE, take_new)
         d, k = expand(ent, g, c0, c1)
         D += d
         K += k
