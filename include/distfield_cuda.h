@@ -217,7 +217,7 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 int dfc_set_row_kernel(int mode);
 
 /* Columns per warp chunk of the lane-per-row kernel (mode 5) for calls on the
- * calling thread: a multiple of 32, 0 = default (DFC_LR_CHUNK or 512).
+ * calling thread: a multiple of 32, 0 = default (DFC_LR_CHUNK, else as wide as ~4096 warps allow).
  * Results are identical; a performance/testing knob. */
 int dfc_set_lr_chunk(int cols);
 

@@ -255,12 +255,18 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     static const int chunk_env = [] {  // DFC_LR_CHUNK (tuning): columns per warp chunk
         const char* v = getenv("DFC_LR_CHUNK");
         const int c = v ? atoi(v) : 0;
-        return c >= 32 ? c & ~31 : 1024;
+        return c >= 32 ? c & ~31 : 0;
     }();
-    // chunk: a multiple of 32 columns, at most kLrCap*32 (the fill stages one row's
-    // list in the ring storage)
-    const int lrC = (int)std::min<int64_t>(std::min<int64_t>(round_up(W, 32), kLrCap * 32),
-                                           g_lr_chunk > 0 ? g_lr_chunk : chunk_env);
+    // chunk: a multiple of 32 columns.  Default: as wide as ~4096 warps allow
+    // (every chunk boundary costs two owner searches), at least 256 columns.
+    int lrC = g_lr_chunk > 0 ? g_lr_chunk : chunk_env;
+    if (lrC == 0) {
+        const int64_t bands = (a.total_rows + 31) / 32;
+        const int64_t nch = std::max<int64_t>(1, (4096 + bands - 1) / bands);
+        lrC = 256;
+        while (lrC < 32768 && (int64_t)lrC * nch < W) lrC <<= 1;
+    }
+    lrC = (int)std::min<int64_t>(round_up(W, 32), lrC);
     const int lrWs = (int)round_up(W, 32);  // scratch row stride (16-byte granules of both lists)
     const size_t ent_bytes = (size_t)round_up(a.total_rows * lrWs * 4, 256);
     const size_t entr_bytes = (size_t)round_up(a.total_rows * lrWs * 2, 256);

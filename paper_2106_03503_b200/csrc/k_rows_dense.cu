@@ -48,10 +48,22 @@ __global__ void __launch_bounds__(32 * kDenseWarps) k_rows_dense(RowArgs a) {
         const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
         const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
         // plane gate: fewer than half object pixels -> no short-run rows worth the staging
-        // (row_done is zeroed by the caller); skip the rest of the plane at once
+        // (row_done is zeroed by the caller); not a dense plane: jump to this
+        // warp's first row of the next dense plane (32 plane counts per probe)
         if (a.plane_counts && 2 * a.plane_counts[img] < (unsigned long long)a.H * (unsigned long long)W) {
-            const int64_t end = (int64_t)(img + 1) * a.H, stride = (int64_t)gridDim.x * kDenseWarps;
-            row += ((end - row + stride - 1) / stride - 1) * stride;  // the loop step passes `end`
+            const int64_t nplanes = a.total_rows / a.H, stride = (int64_t)gridDim.x * kDenseWarps;
+            int64_t next = nplanes;
+            for (int64_t p0 = img + 1; p0 < nplanes; p0 += 32) {
+                const int64_t p = p0 + lane;
+                const bool dense = p < nplanes && 2 * a.plane_counts[p] >= (unsigned long long)a.H * (unsigned long long)W;
+                const unsigned m = __ballot_sync(0xffffffffu, dense);
+                if (m) {
+                    next = p0 + __ffs(m) - 1;
+                    break;
+                }
+            }
+            const int64_t first = next * a.H;  // rows >= first with row == start (mod stride)
+            row += ((first - row + stride - 1) / stride - 1) * stride;  // the loop step reaches it
             continue;
         }
 

@@ -291,10 +291,12 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
 
     // ---- fill: lane = column.  Rows are staged in batches: their entry lists
     // (cp.async, 16-byte granules, L2) into the now idle ring storage ----
-    const int myn = (active && !fail) ? nout : 0;
+    constexpr int kStage = kLrCap * 32;                // staging capacity (entries)
+    const int myall = (active && !fail) ? nout : 0;
+    const int myn = myall <= kStage ? myall : 0;      // longer lists: direct pass below
     const int maxn = (int)__reduce_max_sync(FULL, (unsigned)myn);
-    const int S = max(32, (maxn + 31) & ~31);          // staging stride per row (<= C <= kLrCap*32)
-    const int rpb = min(32, (kLrCap * 32) / S);         // rows per batch
+    const int S = max(32, (maxn + 31) & ~31);          // staging stride per row (<= kStage)
+    const int rpb = min(32, kStage / S);               // rows per batch
     uint32_t* sE = &sm.ks[0][0];
     uint16_t* sR = &sm.rr[0][0];
     const uint32_t sE_addr = (uint32_t)__cvta_generic_to_shared(sE);
@@ -432,6 +434,49 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
                     b += 32;
                 }
             }
+        }
+    }
+    // rows whose list exceeds the staging capacity (chunks wider than kStage
+    // columns with dense envelopes): 32-column blocks straight from L2
+    const uint32_t big = __ballot_sync(FULL, myall > kStage);
+    for (uint32_t bm = big; bm; bm &= bm - 1) {
+        const int rho = __ffs(bm) - 1;
+        const int nE = __shfl_sync(FULL, myall, rho);
+        const uint32_t giR = __shfl_sync(FULL, gi, rho);
+        const int64_t rowR = band * 32 + rho;
+        const int imgR = (int)(rowR / a.H);
+        const int64_t iR = rowR - (int64_t)imgR * a.H;
+        int32_t* Drow = a.D ? reinterpret_cast<int32_t*>(a.D + imgR * a.sD) + iR * W : nullptr;
+        float* Srow = a.S ? reinterpret_cast<float*>(a.S + imgR * a.sS) + iR * W : nullptr;
+        int32_t* Lrow = a.LB ? reinterpret_cast<int32_t*>(a.LB + imgR * a.sL) + iR * W : nullptr;
+        int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + imgR * a.sN) + iR * W : nullptr;
+        const int64_t off = rowR * (int64_t)Ws + c0;
+        int base = 0;
+        for (int b = c0; b < c1; b += 32) {
+            const int idx = base + lane;
+            const uint32_t we = idx < nE ? __ldcg(ent + off + idx) : FULL;
+            const uint32_t wr = idx < nE ? (uint32_t)__ldcg(entr + off + idx) : kNoRow;
+            const int s = (int)(we >> 16);
+            const bool in = lane >= 1 && s <= b + 31;
+            const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
+            const int ow = __popc(Z & ((2u << lane) - 1u));
+            const uint32_t ke = __shfl_sync(FULL, we, ow);
+            const uint32_t kr = __shfl_sync(FULL, wr, ow);
+            const int j = b + lane;
+            if (j < c1) {
+                const uint32_t k = ke & 0xffffu;
+                const bool inf = k == kLrInfK;
+                const uint32_t av = giR > kr ? giR - kr : kr - giR;
+                const int dj = j - (int)k;
+                const uint32_t d = inf ? (uint32_t)DFC_INF_I32 : av * av + (uint32_t)(dj * dj);
+                if (Drow) __stcs(Drow + j, (int32_t)d);
+                if (Srow) __stcs(Srow + j, dist_f32(d));
+                if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(kr * (uint32_t)W + k));
+                if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+            }
+            const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (__ldcg(ent + off + base + 32) >> 16) : 0xffffu;
+            base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
+                    ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
         }
     }
 }

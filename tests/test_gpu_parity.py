@@ -377,7 +377,7 @@ def test_dense_rows_border_gaps_and_ties(dfc):
     _check_edt(dfc, small)
 
 
-@pytest.fixture(params=[0, 32, 96])
+@pytest.fixture(params=[0, 32, 96, 2048])
 def lr_kernel(dfc, request):
     """The lane-per-row chunk scan (k_rows_lr.cu) at the default chunk width and
     at narrow chunks (many chunks per row: warm-ups and cross-chunk owners)."""

@@ -3,6 +3,7 @@ Usage: python tools/launches.py launches.csv [skip_first_n_launches]"""
 import collections, csv, sys
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10]
 skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+rows = rows[next(i for i, r in enumerate(rows) if "Kernel Name" in r):]
 h = rows[0]
 ki, mi, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
 per = collections.OrderedDict()

@@ -17,6 +17,6 @@ for _ in range(3):
     if img.dim() == 3:
         out = dfc.edt_batched(img, dist=False, label=True)
     else:
-        out = dfc.edt(img, polarity=pol, dist=True)
+        out = dfc.edt(img, polarity=pol, dist=cfg != "c5")  # c5: squared distances only
 torch.cuda.synchronize()
 print("ok")
