@@ -272,8 +272,10 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
         uint4 nxt = make_uint4(FULL, FULL, FULL, FULL);
         if (more) nxt = load8(m0 + 8);
         if (mine) {
+            if ((cur.x & cur.y & cur.z & cur.w) != FULL) {  // any candidate among the 8 columns
 #pragma unroll
-            for (int t = 0; t < 8; ++t) cand(m0 + t, (half(cur, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+                for (int t = 0; t < 8; ++t) cand(m0 + t, (half(cur, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+            }
             if (!done) emit(m0 + 7);
         }
         m0 += 8;
