@@ -356,7 +356,61 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
                 const uint32_t wav = giR > wr ? giR - wr : wr - giR;
                 const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
                 const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
-                if (nin < 31) {
+                if (nin <= 3) {
+                    // ---- 128-column block with at most 3 owner changes (sparse rows):
+                    // broadcast the block's owners, each column keeps the last one
+                    // starting at or before it ----
+                    const int j = b + 4 * lane;
+                    uint32_t kc[4], gc[4], rc[4];
+                    {
+                        const uint32_t k0 = __shfl_sync(FULL, wk, 0), g0 = __shfl_sync(FULL, wg, 0);
+                        const uint32_t r0 = __shfl_sync(FULL, wr, 0);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            kc[t] = k0;
+                            gc[t] = g0;
+                            rc[t] = r0;
+                        }
+                    }
+                    for (int e = 1; e <= nin; ++e) {  // warp-uniform trip count
+                        const int se = __shfl_sync(FULL, s, e);
+                        const uint32_t ke = __shfl_sync(FULL, wk, e), ge = __shfl_sync(FULL, wg, e);
+                        const uint32_t re = __shfl_sync(FULL, wr, e);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (j + t >= se) {
+                                kc[t] = ke;
+                                gc[t] = ge;
+                                rc[t] = re;
+                            }
+                    }
+                    const uint32_t d0 = dval(gc[0], kc[0], j), d1 = dval(gc[1], kc[1], j + 1);
+                    const uint32_t d2 = dval(gc[2], kc[2], j + 2), d3 = dval(gc[3], kc[3], j + 3);
+                    if (vec4 && j + 3 < c1) {
+                        if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
+                        if (Srow)
+                            __stcs(reinterpret_cast<float4*>(Srow + j),
+                                   make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
+                        auto lab = [&](uint32_t k, uint32_t r) {
+                            return k == kLrInfK ? -1 : (int32_t)(r * (uint32_t)W + k);
+                        };
+                        auto nc = [&](uint32_t k) { return k == kLrInfK ? -1 : (int32_t)k; };
+                        if (Lrow)
+                            __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab(kc[0], rc[0]), lab(kc[1], rc[1]),
+                                                                               lab(kc[2], rc[2]), lab(kc[3], rc[3])));
+                        if (Nrow)
+                            __stcs(reinterpret_cast<int4*>(Nrow + j), make_int4(nc(kc[0]), nc(kc[1]), nc(kc[2]), nc(kc[3])));
+                    } else {
+                        if (j < c1) put(j, d0, kc[0], rc[0]);
+                        if (j + 1 < c1) put(j + 1, d1, kc[1], rc[1]);
+                        if (j + 2 < c1) put(j + 2, d2, kc[2], rc[2]);
+                        if (j + 3 < c1) put(j + 3, d3, kc[3], rc[3]);
+                    }
+                    // the next block's first owner: the last entry starting <= b+128
+                    const int sn = __shfl_sync(FULL, s, nin + 1);
+                    base += nin + (sn == b + 128 ? 1 : 0);
+                    b += 128;
+                } else if (nin < 31) {
                     // ---- 128-column block, 4 columns per lane: the window holds
                     // every owner; bit (s-b)&31 of word (s-b)>>5 marks a start ----
                     const bool in = lane >= 1 && s <= b + 127;
