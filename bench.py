@@ -55,6 +55,16 @@ CONFIGS = {
 }
 
 
+# what the timed "row pass" of each config runs (the default per-plane dispatch)
+ROW_KERNELS = {
+    "c1": "row pass (k_rows: both planes are neither dense nor sparse)",
+    "c2": "row pass (k_rows_dense for the object->background plane + k_rows for the other)",
+    "c3": "row pass (k_rows_lr: every image is a sparse plane)",
+    "c4": "k_band_* + k_raster (whole step)",
+    "c5": "row pass (k_rows_lr: a sparse plane)",
+}
+
+
 def traffic_for(cfg):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
     try:
@@ -317,7 +327,7 @@ def run_ours(args, rank, world, local_rank):
                                    f"column stripes -> NCCL all-to-all -> row stripes x{world}"),
                    "l2": "256 MiB flush between timed steps (outside the events)"},
         "roofline": {
-            "bound": "hbm", "kernel": "row pass (k_rows_dense + k_rows, the row envelope)" if cfg != "c4" else "k_band_* + k_raster (whole step)",
+            "bound": "hbm", "kernel": ROW_KERNELS.get(cfg, "row pass (the row envelope)"),
             "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic_for(cfg)[0],
             "traffic_source": traffic_for(cfg)[1], "algorithmic_bytes_per_launch": kernel_bytes,
