@@ -166,8 +166,6 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
     int n = 0, head = 0;                 // ring entries head .. head+n-1
     int tk = 0, ts = 0;                  // top entry
     uint32_t tg = 0;
-    int bk = 0, bs = 0, be = 0;          // bottom entry, last column of its range
-    uint32_t bg = 0;
     int F = c0;                          // first column not yet emitted
     int nout = 0;
     bool done = !active, fail = false;
@@ -175,12 +173,12 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
     uint32_t* eout = ent + eoff;
     uint16_t* rout = entr + eoff;
 
+    // one candidate column: pops, then a push (ring room is checked per group)
     auto cand = [&](int m, uint32_t r) {
-        if (done || r == kNoRow) return;
+        if (r == kNoRow) return;
         const uint32_t av = gi > r ? gi - r : r - gi;
         const uint32_t gm = av * av;
         int start = F;
-        bool push = true;
         while (n > 0) {
             // num = g_m - g_k + m^2 - k^2, |num| < 2^31; ts*den, (c1-1)*den < 2^31
             const int dm = m - tk;
@@ -188,8 +186,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
             const int den = 2 * dm;
             const int lim = ts * den;  // start <= js[idx]: pop (:214)
             if (TAKE_NEW ? num <= lim : num < lim) {
-                --n;
-                if (n > 0) {
+                if (--n > 0) {
                     const int idx = (head + n - 1) & (kLrCap - 1);
                     const uint32_t e = sm.ks[idx][lane];
                     tk = (int)(e & 0xffffu);
@@ -197,27 +194,15 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
                     const uint32_t rk = sm.rr[idx][lane];
                     const uint32_t ak = gi > rk ? gi - rk : rk - gi;
                     tg = ak * ak;
-                    if (n == 1) be = c1 - 1;
                 }
                 continue;
             }
-            const int lim2 = (c1 - 1) * den;  // push iff start <= c1-1
-            push = TAKE_NEW ? num <= lim2 : num < lim2;
-            if (push) {  // 0 <= num, quotient < c1 <= 2^15
-                const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
-                // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
-                start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
-            }
+            // push iff start <= c1-1 (:218); 0 <= num, quotient < c1 <= 2^15
+            if (TAKE_NEW ? num > (c1 - 1) * den : num >= (c1 - 1) * den) return;
+            const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
+            // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
+            start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
             break;
-        }
-        if (!push) return;
-        if (n == kLrCap) {  // ring full: the row goes to the merge-tree kernel
-            fail = true;
-            done = true;
-            n = 0;
-            if (a.row_done) a.row_done[row] = 2;  // default mode: k_rows picks it up
-            else fail_rows[atomicAdd(fail_count, 1)] = (int)row;
-            return;
         }
         const int idx = (head + n) & (kLrCap - 1);
         sm.ks[idx][lane] = (uint32_t)m | ((uint32_t)start << 16);
@@ -226,38 +211,25 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
         tk = m;
         ts = start;
         tg = gm;
-        if (n == 1) {
-            bk = m;
-            bs = start;
-            bg = gm;
-            be = c1 - 1;
-        } else if (n == 2) {
-            be = start - 1;
-        }
     };
-    auto pop_bottom = [&]() {  // emit the bottom entry, load the next one
-        rout[nout] = sm.rr[head][lane];
-        eout[nout++] = (uint32_t)bk | ((uint32_t)bs << 16);
-        F = be + 1;
-        head = (head + 1) & (kLrCap - 1);
-        --n;
-        if (n > 0) {
-            const uint32_t e = sm.ks[head][lane];
-            bk = (int)(e & 0xffffu);
-            bs = (int)(e >> 16);
-            const uint32_t rk = sm.rr[head][lane];
-            const uint32_t ak = gi > rk ? gi - rk : rk - gi;
-            bg = ak * ak;
-            be = n >= 2 ? (int)(sm.ks[(head + 1) & (kLrCap - 1)][lane] >> 16) - 1 : c1 - 1;
-        }
-    };
-    auto emit = [&](int m) {  // columns <= m scanned
+    // emit final bottom entries (columns <= m scanned); the bottom is read from the ring
+    auto emit = [&](int m, bool force) {
         while (n > 0) {
-            const int t = m + 1 - be, dd = be - bk;
-            const uint32_t d = bg + (uint32_t)(dd * dd), lim = (uint32_t)(t * t);
-            if (TAKE_NEW ? d >= lim : d > lim) break;
-            pop_bottom();
-            if (n == 0) done = true;  // the last entry owns through c1-1
+            const uint32_t e = sm.ks[head][lane];
+            const int bk = (int)(e & 0xffffu), bs = (int)(e >> 16);
+            const uint32_t rk = sm.rr[head][lane];
+            const int be = n >= 2 ? (int)(sm.ks[(head + 1) & (kLrCap - 1)][lane] >> 16) - 1 : c1 - 1;
+            if (!force) {
+                const uint32_t ak = gi > rk ? gi - rk : rk - gi;
+                const int t = m + 1 - be, dd = be - bk;
+                const uint32_t d = ak * ak + (uint32_t)(dd * dd), lim = (uint32_t)(t * t);
+                if (TAKE_NEW ? d >= lim : d > lim) break;
+            }
+            rout[nout] = (uint16_t)rk;
+            eout[nout++] = e;
+            F = be + 1;
+            head = (head + 1) & (kLrCap - 1);
+            if (--n == 0) done = true;  // the last entry owns through c1-1
         }
     };
 
@@ -273,16 +245,24 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
         if (more) nxt = load8(m0 + 8);
         if (mine) {
             if ((cur.x & cur.y & cur.z & cur.w) != FULL) {  // any candidate among the 8 columns
+                if (n > kLrCap - 8) {  // no room for 8 pushes: the row goes to the merge-tree kernel
+                    fail = true;
+                    done = true;
+                    n = 0;
+                    if (a.row_done) a.row_done[row] = 2;  // default mode: k_rows picks it up
+                    else fail_rows[atomicAdd(fail_count, 1)] = (int)row;
+                } else {
 #pragma unroll
-                for (int t = 0; t < 8; ++t) cand(m0 + t, (half(cur, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+                    for (int t = 0; t < 8; ++t) cand(m0 + t, (half(cur, t >> 1) >> (16 * (t & 1))) & 0xffffu);
+                }
             }
-            if (!done) emit(m0 + 7);
+            if (!done) emit(m0 + 7, false);
         }
         m0 += 8;
         cur = nxt;
     }
     if (active && !fail) {  // no later candidate: everything left is final
-        while (n > 0) pop_bottom();
+        emit(0, true);
         if (F < c1) {  // featureless row
             rout[nout] = kNoRow;
             eout[nout++] = kLrInfK | ((uint32_t)F << 16);
