@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
     auto emit = [&](int m, bool force) {
         while (n > 0) {
             const uint32_t e = sm.ks[head][lane];
-            const int bk = (int)(e & 0xffffu), bs = (int)(e >> 16);
+            const int bk = (int)(e & 0xffffu);
             const uint32_t rk = sm.rr[head][lane];
             const int be = n >= 2 ? (int)(sm.ks[(head + 1) & (kLrCap - 1)][lane] >> 16) - 1 : c1 - 1;
             if (!force) {
