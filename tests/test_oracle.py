@@ -158,6 +158,27 @@ def test_separable_closed_forms():
         assert (ch == oracle.chamfer34(img).astype(np.int64)).all()
 
 
+def test_raster_argmin_monotone():
+    """The smallest minimising column of min_k max(a_k,|j-k|) (chessboard) and of
+    min_k 3 max + min (chamfer-3-4) is non-decreasing along a row: the divide and
+    conquer of k_raster.cu relies on it (SURVEY finding 5)."""
+    for t in range(40):
+        img = oracle.random_image(3 + t % 25, 3 + (7 * t) % 60, [0.005, 0.02, 0.08, 0.3][t % 4], 700 + t)
+        if not img.any():
+            continue
+        a, big = _a_cols(img)
+        r, c = img.shape
+        h = np.abs(np.arange(c)[:, None] - np.arange(c)[None, :])  # [j, k]
+        A = a[:, None, :]
+        H = h[None, :, :]
+        mx, mn = np.maximum(A, H), np.minimum(A, H)
+        valid = A < big
+        for f in (mx, 3 * mx + mn):
+            v = np.where(valid, f, 4 * big)
+            kstar = v.argmin(axis=2)  # numpy argmin = smallest minimiser
+            assert (np.diff(kstar, axis=1) >= 0).all()
+
+
 def test_label_tie_rule_min_column_then_min_row():
     """voronoi_labels = (smallest minimizing column, then upper row); nearest_col =
     largest minimizing column (SURVEY finding 4)."""
