@@ -127,6 +127,19 @@ int dfc_column_nr_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t p
                      uint16_t* d_nr, int64_t nr_pitch, dfc_stream_t stream);
 
 /*
+ * The two directions of stage one separately, over an arbitrary squared-
+ * distance map in place (uint64 cells, UINT64_MAX = infinity, row pitch in
+ * elements): vertical_down_pass / vertical_up_pass (exact_edt.cpp:74-110),
+ * including the odd-step increment chain, the strict '>' update and the
+ * unsigned arithmetic of the reference.  down followed by up over
+ * init_distance_map(img) is vertical_pass (:112-117).
+ */
+int dfc_vertical_down_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems,
+                               dfc_stream_t stream);
+int dfc_vertical_up_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems,
+                             dfc_stream_t stream);
+
+/*
  * Stage two alone from a nearest-row plane that may be split into column
  * tiles: element (i, j) at d_nr[(j / tile_cols) * tile_stride_elems +
  * i * tile_cols + j % tile_cols]; tile_cols >= cols means one row-major

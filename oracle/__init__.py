@@ -125,6 +125,28 @@ def vertical_pass(img):
     return out
 
 
+def init_map(img):
+    """init_distance_map (grid.cpp:85-91), squared Euclidean: 0 at objects, INF elsewhere."""
+    img, r, c = _img(img)
+    out = np.empty((r, c), np.uint64)
+    orc.orc_init_map(img, r, c, out)
+    return out
+
+
+def vertical_down_pass(dm):
+    """vertical_down_pass (exact_edt.cpp:74-91) on a copy of a uint64 map."""
+    out = np.ascontiguousarray(dm, dtype=np.uint64).copy()
+    orc.orc_vertical_down_pass(out, out.shape[0], out.shape[1])
+    return out
+
+
+def vertical_up_pass(dm):
+    """vertical_up_pass (exact_edt.cpp:93-110) on a copy of a uint64 map."""
+    out = np.ascontiguousarray(dm, dtype=np.uint64).copy()
+    orc.orc_vertical_up_pass(out, out.shape[0], out.shape[1])
+    return out
+
+
 def edt(img):
     """Exact squared EDT, uint64 with INF (exact_edt.cpp:285-317)."""
     img, r, c = _img(img)

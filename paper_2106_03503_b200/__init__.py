@@ -40,6 +40,8 @@ _lib.dfc_edt_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, 
 _lib.dfc_edt_u8_dual.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]
 _lib.dfc_edt_u8_batched.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp]
 _lib.dfc_vertical_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp]
+_lib.dfc_vertical_down_pass_u64.argtypes = [_vp, _i64, _i64, _i64, _vp]
+_lib.dfc_vertical_up_pass_u64.argtypes = [_vp, _i64, _i64, _i64, _vp]
 _lib.dfc_raster_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp]
 _lib.dfc_label_ordinals.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp, _vp]
 _lib.dfc_status_string.restype = C.c_char_p
@@ -62,6 +64,7 @@ _lib.dfc_labels_gray.argtypes = [_vp, _i64, _i64, _vp, _vp]
 
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
+    "dfc_vertical_down_pass_u64", "dfc_vertical_up_pass_u64",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
     "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel", "dfc_set_lr_chunk",
     "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
@@ -204,6 +207,25 @@ def vertical(img: torch.Tensor, stream=None) -> torch.Tensor:
     out = _empty((h, w), torch.int32, img)
     _check(_lib.dfc_vertical_u8(_ptr(img), h, w, pitch, _ptr(out), _stream(stream)))
     return out
+
+
+def vertical_down_pass(dm: torch.Tensor, stream=None) -> torch.Tensor:
+    """vertical_down_pass (exact_edt.cpp:74-91) IN PLACE on a 2-D int64 tensor
+    holding uint64 cells (bit pattern; -1 = kInfinity).  Returns dm."""
+    _vpass(dm, _lib.dfc_vertical_down_pass_u64, stream)
+    return dm
+
+
+def vertical_up_pass(dm: torch.Tensor, stream=None) -> torch.Tensor:
+    """vertical_up_pass (exact_edt.cpp:93-110) IN PLACE, as vertical_down_pass."""
+    _vpass(dm, _lib.dfc_vertical_up_pass_u64, stream)
+    return dm
+
+
+def _vpass(dm, fn, stream):
+    if not dm.is_cuda or dm.dim() != 2 or dm.dtype not in (torch.int64, torch.uint64) or dm.stride(1) != 1:
+        raise ValueError("expected a 2-D CUDA int64/uint64 tensor with unit column stride")
+    _check(fn(_ptr(dm), dm.shape[0], dm.shape[1], dm.stride(0), _stream(stream)))
 
 
 def raster(img: torch.Tensor, cityblock: bool = True, chessboard: bool = True,

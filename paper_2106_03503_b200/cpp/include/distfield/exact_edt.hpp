@@ -45,6 +45,9 @@ enum class EdtAlgorithm : std::uint8_t { bruteforce, simple, improved, envelope 
 enum class Orientation : std::uint8_t { automatic, rows, columns };
 
 // Stage one: per column, the squared vertical distance to the nearest object.
+// The two directions in place over any squared-distance map (exact_edt.cpp:74-110).
+void vertical_down_pass(DistanceMap& dm, unsigned threads = 1);
+void vertical_up_pass(DistanceMap& dm, unsigned threads = 1);
 DistanceMap vertical_pass(const BinaryImage& img, unsigned threads = 1);
 
 // Stage two over a vertical map (meijster_scan, take_new ties: nearest_col is

@@ -4,6 +4,7 @@
 // :319-371 (voronoi_labels).
 #include "distfield/exact_edt.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <stdexcept>
 
@@ -56,6 +57,34 @@ Scan scan_rows(const DistanceMap& vert, std::size_t row0, std::size_t nrows) {
 }
 
 }  // namespace
+
+namespace {
+void vertical_direction(DistanceMap& dm, bool up) {
+    const std::size_t rows = dm.rows(), cols = dm.cols();
+    std::vector<std::uint64_t> host(rows * cols);
+    for (std::size_t i = 0; i < rows; ++i) {
+        const auto r = dm.row(i);
+        std::copy(r.begin(), r.end(), host.begin() + static_cast<std::ptrdiff_t>(i * cols));
+    }
+    DeviceBuffer<std::uint64_t> d(host.size());
+    d.upload(host.data());
+    dfc_check(up ? dfc_vertical_up_pass_u64(d.get(), (int64_t)rows, (int64_t)cols, (int64_t)cols, stream())
+                 : dfc_vertical_down_pass_u64(d.get(), (int64_t)rows, (int64_t)cols, (int64_t)cols, stream()),
+              up ? "vertical_up_pass" : "vertical_down_pass");
+    host = d.download();
+    for (std::size_t i = 0; i < rows; ++i) {
+        auto r = dm.row(i);
+        std::copy(host.begin() + static_cast<std::ptrdiff_t>(i * cols),
+                  host.begin() + static_cast<std::ptrdiff_t>((i + 1) * cols), r.begin());
+    }
+}
+}  // namespace
+
+// exact_edt.cpp:74-91
+void vertical_down_pass(DistanceMap& dm, unsigned) { vertical_direction(dm, false); }
+
+// exact_edt.cpp:93-110
+void vertical_up_pass(DistanceMap& dm, unsigned) { vertical_direction(dm, true); }
 
 DistanceMap vertical_pass(const BinaryImage& img, unsigned) {
     auto dimg = detail::upload_image(img);

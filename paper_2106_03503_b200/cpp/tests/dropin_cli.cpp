@@ -51,6 +51,16 @@ int main(int argc, char** argv) {
             put_map(out, edt(img, EdtAlgorithm::simple, Orientation::columns));
         } else if (op == "vertical") {
             put_map(out, vertical_pass(img));
+        } else if (op == "vertical_down" || op == "vertical_up") {  // over init_distance_map(img)
+            DistanceMap dm = init_distance_map(img, DistanceKind::squared_euclidean);
+            if (op == "vertical_down") vertical_down_pass(dm, 2);
+            else vertical_up_pass(dm, 2);
+            put_map(out, dm);
+        } else if (op == "vertical_both") {  // down then up == vertical_pass (exact_edt.cpp:112-117)
+            DistanceMap dm = init_distance_map(img, DistanceKind::squared_euclidean);
+            vertical_down_pass(dm);
+            vertical_up_pass(dm);
+            put_map(out, dm);
         } else if (op == "meijster") {
             const auto r = meijster_scan(vertical_pass(img));
             put_map(out, r.map);

@@ -553,6 +553,33 @@ int dfc_vertical_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pi
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 
+namespace {
+int vpass(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems, bool up, dfc_stream_t stream) {
+    if (!d_map) return DFC_ERR_ARG;
+    if (rows < 1 || cols < 1 || pitch_elems < cols) return DFC_ERR_ARG;
+    g_launches = 0;
+    const int64_t blocks = (cols + 255) / 256;
+    if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
+    if (up)
+        k_vpass_u64<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_map, rows, cols, pitch_elems);
+    else
+        k_vpass_u64<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_map, rows, cols, pitch_elems);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+}  // namespace
+
+int dfc_vertical_down_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems,
+                               dfc_stream_t stream) {
+    return vpass(d_map, rows, cols, pitch_elems, false, stream);
+}
+
+int dfc_vertical_up_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems,
+                             dfc_stream_t stream) {
+    return vpass(d_map, rows, cols, pitch_elems, true, stream);
+}
+
 int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitch_bytes,
                   int32_t* d_cityblock, int32_t* d_chessboard, int32_t* d_chamfer34,
                   dfc_stream_t stream) {

@@ -247,6 +247,47 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
     }
 }
 
+// Per-direction vertical passes over an arbitrary squared-distance map
+// (uint64, in place, INF = UINT64_MAX): vertical_down_pass / vertical_up_pass
+// (exact_edt.cpp:74-110) -- the odd-step increment chain with the strict '>'
+// update and the step reset, same unsigned arithmetic.  One thread per
+// column (coalesced across the warp), serial over rows, 4 rows of loads in
+// flight ahead of the dependent chain.
+template <bool UP>
+__global__ void k_vpass_u64(uint64_t* __restrict__ dm, int64_t rows, int64_t cols, int64_t pitch) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cols || rows < 2) return;
+    constexpr uint64_t kInf = ~0ull;
+    uint64_t* col = dm + j;
+    const int64_t step_i = UP ? -pitch : pitch;
+    uint64_t* p = col + (UP ? (rows - 1) * pitch : 0);
+    uint64_t prev = *p;  // row 0 (down) / rows-1 (up) is never updated
+    uint64_t step = 1;
+    int64_t n = rows - 1;
+    p += step_i;
+    while (n > 0) {
+        const int c = n >= 4 ? 4 : (int)n;
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = u < c ? p[u * step_i] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (u >= c) break;
+            uint64_t cur = v[u];
+            if (prev != kInf && (cur == kInf || cur > prev + step)) {
+                cur = prev + step;
+                p[u * step_i] = cur;
+                step += 2;
+            } else {
+                step = 1;
+            }
+            prev = cur;
+        }
+        p += c * step_i;
+        n -= c;
+    }
+}
+
 template __global__ void k_band_fill<false>(ColArgs, const uint16_t*, const uint16_t*, uint16_t*, int32_t*);
 template __global__ void k_band_fill<true>(ColArgs, const uint16_t*, const uint16_t*, uint16_t*, int32_t*);
 

@@ -21,6 +21,7 @@ import numpy as np
 import torch
 
 from . import INF_I32, edt as _edt, label_ordinals, raster as _raster, vertical as _vertical
+from . import vertical_down_pass as _vdown, vertical_up_pass as _vup
 
 INF = np.uint64(2**64 - 1)
 NO_COLUMN = np.uint32(2**32 - 1)
@@ -72,6 +73,33 @@ def edt(img, algorithm=EdtAlgorithm.envelope, orient=Orientation.automatic, stat
 def vertical_pass(img, threads=1):
     """vertical_pass -- exact_edt.cpp:112-117."""
     return _u64(_vertical(_to_device(img)))
+
+
+def _vpass_np(dm, fn):
+    a = np.ascontiguousarray(dm, dtype=np.uint64)
+    if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise ValueError("grid dimensions must be at least 1x1")  # grid.hpp:22-23
+    d = torch.from_numpy(a.view(np.int64)).cuda()
+    fn(d)
+    return d.cpu().numpy().view(np.uint64)
+
+
+def vertical_down_pass(dm, threads=1):
+    """vertical_down_pass -- exact_edt.cpp:74-91.  The reference mutates a
+    DistanceMap in place; here the updated uint64 map is returned (and written
+    back into ``dm`` when it is a writable C-contiguous uint64 array)."""
+    out = _vpass_np(dm, _vdown)
+    if isinstance(dm, np.ndarray) and dm.dtype == np.uint64 and dm.flags.c_contiguous and dm.flags.writeable:
+        dm[...] = out
+    return out
+
+
+def vertical_up_pass(dm, threads=1):
+    """vertical_up_pass -- exact_edt.cpp:93-110 (see vertical_down_pass)."""
+    out = _vpass_np(dm, _vup)
+    if isinstance(dm, np.ndarray) and dm.dtype == np.uint64 and dm.flags.c_contiguous and dm.flags.writeable:
+        dm[...] = out
+    return out
 
 
 def meijster_scan_image(img, threads=1):

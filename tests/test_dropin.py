@@ -42,6 +42,10 @@ def test_six_point_goldens():
     assert (run("edt", img) == ref("kSquaredEuclidean")).all()
     assert (run("edt_simple", img) == ref("kSquaredEuclidean")).all()
     assert (run("vertical", img) == ref("kVerticalFinal")).all()
+    assert (run("vertical_down", img) == ref("kVerticalDown")).all()
+    assert (run("vertical_both", img) == ref("kVerticalFinal")).all()
+    want_up = oracle.vertical_up_pass(oracle.init_map(img)).ravel()
+    assert (run("vertical_up", img) == want_up).all()
     assert (run("cityblock", img) == ref("kCityblockFinal")).all()
     assert (run("chamfer", img) == ref("kChamferFinal")).all()
     v = run("rowenv", img, 0, dtype=np.int64)

@@ -423,3 +423,42 @@ def test_lr_batched_dual_and_discs(lr_kernel):
     _check_edt(lr_kernel, img)
     _check_edt(lr_kernel, img, polarity=1)
     _check_edt(lr_kernel, workloads.discs(512, 1000, 12, 9))
+
+
+def test_vertical_direction_passes(dfc):
+    """vertical_down_pass / vertical_up_pass (exact_edt.cpp:74-110) in place over
+    arbitrary uint64 maps -- infinities, zeros, squares and arbitrary values,
+    odd pitches -- against the oracle; down then up over init_distance_map is
+    vertical_pass; the six-point golden pins the down pass alone."""
+    rng = np.random.default_rng(5)
+    inf = np.uint64(2**64 - 1)
+    for r, c in [(1, 1), (1, 7), (9, 1), (37, 53), (256, 300), (1000, 33)]:
+        dm = rng.integers(0, 400, size=(r, c)).astype(np.uint64)
+        dm[rng.random((r, c)) < 0.5] = inf
+        dm[rng.random((r, c)) < 0.05] = 0
+        dm[rng.random((r, c)) < 0.01] = np.uint64(2**63 + 5)  # unsigned arithmetic as in the reference
+        for fn, ofn in ((dfc.vertical_down_pass, oracle.vertical_down_pass),
+                        (dfc.vertical_up_pass, oracle.vertical_up_pass)):
+            pitch = c + 3  # a padded device map
+            buf = torch.zeros((r, pitch), dtype=torch.int64, device="cuda")
+            buf[:, :c] = torch.from_numpy(dm.view(np.int64)).cuda()
+            fn(buf[:, :c])
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(buf[:, :c].cpu().numpy().view(np.uint64), ofn(dm))
+    for t in range(6):
+        img = oracle.random_image(20 + 7 * t, 31 + 5 * t, [0.0, 0.01, 0.1][t % 3], 90 + t)
+        d = torch.from_numpy(oracle.init_map(img).view(np.int64)).cuda()
+        dfc.vertical_down_pass(d)
+        dfc.vertical_up_pass(d)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(d.cpu().numpy().view(np.uint64), oracle.vertical_pass(img))
+    g = json.load(open(os.path.join(GOLD, "six_point.json")))
+    img = np.zeros((g["rows"], g["cols"]), np.uint8)
+    for a, b in g["points"]:
+        img[a, b] = 1
+    d = torch.from_numpy(oracle.init_map(img).view(np.int64)).cuda()
+    dfc.vertical_down_pass(d)
+    want = np.array(g["kVerticalDown"], dtype=np.int64)
+    got = d.cpu().numpy()
+    np.testing.assert_array_equal(np.where(want < 0, -1, got), np.where(want < 0, -1, want))
+    assert (got[want < 0] == -1).all()
