@@ -120,7 +120,8 @@ RowGeom row_geom(int W) {
 // Stage 1 into a uint16 nearest-row plane [npol][n][H][Wp].
 int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
-                cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr) {
+                cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr,
+                uint32_t* pts = nullptr) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -133,6 +134,9 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.pol0 = pol0;
     c.npol = npol;
     c.vec = aligned(img, 4) && pitch % 4 == 0 && istride % 4 == 0;
+    c.pts = counts ? pts : nullptr;
+    c.pcounts = counts;
+    const unsigned long long* skip = c.pts ? counts : nullptr;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
     if (counts) {
@@ -142,11 +146,11 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     k_band_summary<<<grid, tpb, 0, st>>>(c, first, last, counts);
     if (c.nb <= 64) {  // short columns: serial over bands, one thread per column
         dim3 gs((unsigned)((W + 255) / 256), (unsigned)(npol * n));
-        k_band_scan_serial<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
+        k_band_scan_serial<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last, skip);
     } else {           // tall columns: chunks of bands scanned in parallel
         const int nc = std::min(32, c.nb / 4);
         dim3 gs((unsigned)((W + 31) / 32), (unsigned)(npol * n));
-        k_band_scan<<<gs, 32 * nc, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last);
+        k_band_scan<<<gs, 32 * nc, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last, skip);
     }
     if (vsq)
         k_band_fill<true><<<grid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
@@ -208,7 +212,8 @@ int row_pass_win(RowArgs a, bool take_new, cudaStream_t st) {
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
              int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
              int64_t sN, cudaStream_t st, bool vdist = false, int tile_cols = 0,
-             int64_t tile_stride = 0, int row0 = 0, const unsigned long long* plane_counts = nullptr) {
+             int64_t tile_stride = 0, int row0 = 0, const unsigned long long* plane_counts = nullptr,
+             const uint32_t* pts = nullptr) {
     const RowGeom g = row_geom((int)W);
     RowArgs a;
     a.nr = nr;
@@ -240,6 +245,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.vec_nr = false;
     a.row_done = nullptr;
     a.lr_gate = false;
+    a.pts_gate = false;
     a.plane_counts = plane_counts;
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
     if (mode == 3 && W <= 16384) return row_pass_win(a, take_new, st);
@@ -331,6 +337,15 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         e = cudaMemsetAsync(a.row_done, 0, flag_bytes + 4, st);  // flags and the list count
         if (e != cudaSuccess) return cuda_fail(e);
         a.lr_gate = lr_on;
+        a.pts_gate = pts != nullptr && plane_counts != nullptr && H % 32 == 0;
+        if (a.pts_gate) {  // point planes: from K1a's object list, no nearest-row plane
+            const void* pfn = take_new ? pts_kernel_ptr<true>() : pts_kernel_ptr<false>();
+            const int64_t pblocks = ((a.total_rows + 31) / 32 + kPtsWarps - 1) / kPtsWarps;
+            void* pargs[] = {&a, &pts};
+            e = cudaLaunchKernel(pfn, dim3((unsigned)pblocks), dim3(32 * kPtsWarps), pargs, 0, st);
+            if (e != cudaSuccess) return cuda_fail(e);
+            ++g_launches;
+        }
         if (dense_on) {  // dense rows (short runs between object pixels): flagged 1
             a.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0 && a.tile_cols >= W;
             const void* dfn = take_new ? dense_kernel_ptr<true>() : dense_kernel_ptr<false>();
@@ -359,7 +374,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         }
         const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
         k_rows_rest<<<(unsigned)rblocks, 256, 0, st>>>(a.row_done, plane_counts, a.total_rows, (int)H, (int)W,
-                                                       a.lr_gate, rest_rows, rest_count);
+                                                       a.lr_gate, a.pts_gate, rest_rows, rest_count);
         ++g_launches;
         RowArgs ra = a;
         ra.row_list = rest_rows;
@@ -438,15 +453,20 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     const int64_t planes = (int64_t)npol * n;
     const size_t carry_elems = (size_t)(planes * nb * Wp);
     const size_t nr_elems = (size_t)(planes * H * Wp);
+    // point planes (k_rows_pts) in the default row pass when planes are whole warps of rows
+    const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
+    const bool pts_on = mode == 4 && H % 32 == 0;
     Scratch sc(st);
-    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 256 + (size_t)planes * 8);
+    cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 512 + (size_t)planes * 8 +
+                             (pts_on ? (size_t)planes * kPtsCap * 4 : 0));
     if (e != cudaSuccess) return cuda_fail(e);
     uint16_t* first = static_cast<uint16_t*>(sc.p);
     uint16_t* last = first + carry_elems;
     uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry_elems), 16));
     auto* counts = reinterpret_cast<unsigned long long*>(round_up(reinterpret_cast<uintptr_t>(nr + nr_elems), 16));
+    uint32_t* pts = pts_on ? reinterpret_cast<uint32_t*>(counts + planes) : nullptr;
     prof(0, st);
-    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts);
+    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts, pts);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -468,23 +488,23 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
         if (want_keep) {
             rc = row_pass(nr, nimg, H, W, Wp, false, o.D[0], stride_of(o.D[0], o.D[1]), o.S[0],
                           o.S[0] ? stride_of(o.S[0], o.S[1]) : 0, o.LB[0],
-                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st, false, 0, 0, 0, counts);
+                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st, false, 0, 0, 0, counts, pts);
             if (rc != DFC_OK) return rc;
         }
         if (o.NC[0]) {
             rc = row_pass(nr, nimg, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[0],
-                          stride_of(o.NC[0], o.NC[1]), st, false, 0, 0, 0, counts);
+                          stride_of(o.NC[0], o.NC[1]), st, false, 0, 0, 0, counts, pts);
             if (rc != DFC_OK) return rc;
         }
     } else {
         for (int s = 0; s < npol; ++s) {
             const uint16_t* pl = nr + (int64_t)s * H * Wp;
             rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st, false, 0, 0, 0,
-                          counts + s);
+                          counts + s, pts ? pts + (int64_t)s * kPtsCap : nullptr);
             if (rc != DFC_OK) return rc;
             if (o.NC[s]) {
                 rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st, false, 0, 0,
-                              0, counts + s);
+                              0, counts + s, pts ? pts + (int64_t)s * kPtsCap : nullptr);
                 if (rc != DFC_OK) return rc;
             }
         }

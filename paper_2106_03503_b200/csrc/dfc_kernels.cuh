@@ -14,6 +14,10 @@ struct ColArgs {
     int nb;              // bands per image
     int pol0, npol;      // first polarity and number of polarity slots (1 or 2)
     bool vec;            // 4-byte loads are legal (pitch, base aligned)
+    // point planes (<= kPtsCap object pixels, default row pass): K1a lists their
+    // object pixels, K1b/K1c skip them (k_rows_pts works from the list)
+    uint32_t* pts;                           // [plane][kPtsCap] keys col << 16 | row, nullable
+    const unsigned long long* pcounts;       // object pixels per plane (K1a), for the skip
 };
 
 // Stage 2 (k_rows.cu)
@@ -40,6 +44,7 @@ struct RowArgs {
     const int* row_count;     // number of entries in row_list (device)
     uint8_t* row_done;        // per row: 1 = written by k_rows_dense, 2 = k_rows_lr overflowed
     bool lr_gate;             // rows of sparse planes belong to k_rows_lr (unless row_done == 2)
+    bool pts_gate;            // rows of point planes belong to k_rows_pts
     const unsigned long long* plane_counts;  // object pixels per plane (dense gate), nullable
 };
 
@@ -52,6 +57,15 @@ struct RasterArgs {
     int32_t* chess;
     int32_t* cham;
 };
+
+// Point plane: at most kPtsCap object pixels (C3's 30-point images).  With
+// the points path on (default row pass, rows per plane a multiple of 32) its
+// rows go to k_rows_pts, which works from K1a's list of object pixels; no
+// nearest-row plane is written or read for it.
+constexpr int kPtsCap = 64;
+__host__ __device__ __forceinline__ bool pts_plane(const unsigned long long* counts, int img, bool on) {
+    return on && counts != nullptr && counts[img] <= (unsigned long long)kPtsCap;
+}
 
 // Sparse plane (object pixels < 1/256 of the plane): its rows go to the
 // lane-per-row kernel (k_rows_lr.cu) in the default mode.

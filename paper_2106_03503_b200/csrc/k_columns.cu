@@ -83,9 +83,27 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
             l[c] = mk[c] ? (uint16_t)(r0 + 31 - __clz(mk[c])) : kNoRow;
         }
         if (counts) {
-            unsigned long long c = (unsigned)(__popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]));
+            const unsigned mine = (unsigned)(__popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]));
+            unsigned long long c = mine;
             for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-            if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts + (int64_t)s * a.n_img + im, c);
+            const int lane = threadIdx.x & 31;
+            const int64_t plane = (int64_t)s * a.n_img + im;
+            unsigned long long old = 0;
+            if (lane == 0 && c) old = atomicAdd(counts + plane, c);
+            old = __shfl_sync(0xffffffffu, old, 0);
+            // the plane's first kPtsCap object pixels go to its point list (the
+            // running count is the position; a longer plane's list is unused)
+            if (a.pts && c && old + c <= (unsigned long long)kPtsCap) {
+                unsigned pre = mine;  // inclusive prefix of the per-lane counts
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned v = __shfl_up_sync(0xffffffffu, pre, o);
+                    if (lane >= o) pre += v;
+                }
+                uint32_t* dst = a.pts + plane * kPtsCap + old + (pre - mine);
+                for (int cc = 0; cc < 4; ++cc)
+                    for (uint32_t m = mk[cc]; m; m &= m - 1)
+                        *dst++ = ((uint32_t)(j0 + cc) << 16) | (uint32_t)(r0 + __ffs(m) - 1);
+            }
         }
         if (!live) continue;
         const int64_t off = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
@@ -100,10 +118,11 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
 // over the bands with 4 independent loads in flight; same in-place result as
 // the chunked scan below.
 __global__ void k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint16_t* __restrict__ first,
-                                   uint16_t* __restrict__ last) {
+                                   uint16_t* __restrict__ last, const unsigned long long* skip_counts) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t plane = blockIdx.y;
     if (j >= W || plane >= n_planes) return;
+    if (skip_counts && skip_counts[plane] <= (unsigned long long)kPtsCap) return;  // point plane
     uint16_t* F = first + plane * nb * (int64_t)Wp + j;
     uint16_t* Lp = last + plane * nb * (int64_t)Wp + j;
     uint16_t run = kNoRow;
@@ -149,7 +168,10 @@ __global__ void k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint
 // twice (aggregate, then carry-in + write) -- coalesced across the columns,
 // and parallel over the chunks instead of a serial walk over all bands.
 __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64_t n_planes,
-                                                    uint16_t* __restrict__ first, uint16_t* __restrict__ last) {
+                                                    uint16_t* __restrict__ first, uint16_t* __restrict__ last,
+                                                    const unsigned long long* skip_counts) {
+    if (skip_counts && blockIdx.y < n_planes && skip_counts[blockIdx.y] <= (unsigned long long)kPtsCap)
+        return;  // point plane (CTA-uniform)
     __shared__ int agg_last[32][33];
     __shared__ int agg_first[32][33];
     const int cx = threadIdx.x & 31, ch = threadIdx.x >> 5, nc = blockDim.x >> 5;
@@ -203,6 +225,7 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
     band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
+        if (a.pts && a.pcounts[(int64_t)s * a.n_img + im] <= (unsigned long long)kPtsCap) continue;  // point plane
         const int64_t coff = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
         const uint2 ab = *reinterpret_cast<const uint2*>(above + coff);
         const uint2 bl = *reinterpret_cast<const uint2*>(below + coff);

@@ -144,7 +144,9 @@ __device__ __forceinline__ void rows_group(const RowArgs& a, int64_t grp) {
     if (a.row_done) {  // rows k_rows_dense / k_rows_lr already wrote
         if (active) {
             const uint8_t rd = a.row_done[row];
-            if (rd == 1 || (a.lr_gate && rd != 2 && lr_plane(a.plane_counts, (int)(row / a.H), a.H, a.W)))
+            const int pl = (int)(row / a.H);
+            if (rd == 1 || pts_plane(a.plane_counts, pl, a.pts_gate) ||
+                (a.lr_gate && rd != 2 && lr_plane(a.plane_counts, pl, a.H, a.W)))
                 active = false;
         }
         if (__syncthreads_and(!active)) return;  // CTA-uniform

@@ -50,12 +50,14 @@ __global__ void __launch_bounds__(32 * kDenseWarps) k_rows_dense(RowArgs a) {
         // plane gate: fewer than half object pixels -> no short-run rows worth the staging
         // (row_done is zeroed by the caller); not a dense plane: jump to this
         // warp's first row of the next dense plane (32 plane counts per probe)
-        if (a.plane_counts && 2 * a.plane_counts[img] < (unsigned long long)a.H * (unsigned long long)W) {
+        if (a.plane_counts && (2 * a.plane_counts[img] < (unsigned long long)a.H * (unsigned long long)W ||
+                               pts_plane(a.plane_counts, img, a.pts_gate))) {
             const int64_t nplanes = a.total_rows / a.H, stride = (int64_t)gridDim.x * kDenseWarps;
             int64_t next = nplanes;
             for (int64_t p0 = img + 1; p0 < nplanes; p0 += 32) {
                 const int64_t p = p0 + lane;
-                const bool dense = p < nplanes && 2 * a.plane_counts[p] >= (unsigned long long)a.H * (unsigned long long)W;
+                const bool dense = p < nplanes && 2 * a.plane_counts[p] >= (unsigned long long)a.H * (unsigned long long)W &&
+                                   !pts_plane(a.plane_counts, (int)p, a.pts_gate);
                 const unsigned m = __ballot_sync(0xffffffffu, dense);
                 if (m) {
                     next = p0 + __ffs(m) - 1;

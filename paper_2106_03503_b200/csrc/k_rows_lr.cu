@@ -61,6 +61,174 @@ __device__ __forceinline__ const uint16_t* lr_col_ptr(const RowArgs& a, const ui
     return rowp + t * a.tile_stride + (m - t * a.tile_cols);
 }
 
+// Fill one row's columns [c0, c1) from its entry list (column | start << 16,
+// plus the column's nearest row), lane = column; shared by k_rows_lr and
+// k_rows_pts.  rE / rR are in shared memory.
+__device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE, const uint16_t* rR, int nE,
+                                            uint32_t giR, int32_t* Drow, float* Srow, int32_t* Lrow,
+                                            int32_t* Nrow, int c0, int c1, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int W = a.W;
+    const bool vec4 = a.vec;  // 16-byte stores legal (W % 4 == 0, aligned planes)
+    auto put = [&](int j, uint32_t d, uint32_t k, uint32_t r) {  // one column, scalar
+        const bool inf = k == kLrInfK;
+        if (Drow) __stcs(Drow + j, (int32_t)d);
+        if (Srow) __stcs(Srow + j, dist_f32(d));
+        if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(r * (uint32_t)W + k));
+        if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+    };
+    auto dval = [&](uint32_t g, uint32_t k, int j) -> uint32_t {
+        const int dj = j - (int)k;
+        return g == kInfU ? (uint32_t)DFC_INF_I32 : g + (uint32_t)(dj * dj);
+    };
+    int base = 0;  // entry owning column b
+    int b = c0;
+    while (b < c1) {
+        // window: lane e holds entry base + e; entries 1.. start after b-1
+        const int idx = base + lane;
+        const uint32_t we = idx < nE ? rE[idx] : FULL;
+        const uint32_t wr = idx < nE ? (uint32_t)rR[idx] : kNoRow;
+        const int s = (int)(we >> 16);
+        const uint32_t wk = we & 0xffffu;
+        const uint32_t wav = giR > wr ? giR - wr : wr - giR;
+        const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
+        const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
+        if (nin <= 3) {
+            // ---- 128-column block with at most 3 owner changes (sparse rows):
+            // broadcast the block's owners, each column keeps the last one
+            // starting at or before it ----
+            const int j = b + 4 * lane;
+            uint32_t kc[4], gc[4], rc[4];
+            {
+                const uint32_t k0 = __shfl_sync(FULL, wk, 0), g0 = __shfl_sync(FULL, wg, 0);
+                const uint32_t r0 = __shfl_sync(FULL, wr, 0);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    kc[t] = k0;
+                    gc[t] = g0;
+                    rc[t] = r0;
+                }
+            }
+            for (int e = 1; e <= nin; ++e) {  // warp-uniform trip count
+                const int se = __shfl_sync(FULL, s, e);
+                const uint32_t ke = __shfl_sync(FULL, wk, e), ge = __shfl_sync(FULL, wg, e);
+                const uint32_t re = __shfl_sync(FULL, wr, e);
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (j + t >= se) {
+                        kc[t] = ke;
+                        gc[t] = ge;
+                        rc[t] = re;
+                    }
+            }
+            const uint32_t d0 = dval(gc[0], kc[0], j), d1 = dval(gc[1], kc[1], j + 1);
+            const uint32_t d2 = dval(gc[2], kc[2], j + 2), d3 = dval(gc[3], kc[3], j + 3);
+            if (vec4 && j + 3 < c1) {
+                if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
+                if (Srow)
+                    __stcs(reinterpret_cast<float4*>(Srow + j),
+                           make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
+                auto lab = [&](uint32_t k, uint32_t r) {
+                    return k == kLrInfK ? -1 : (int32_t)(r * (uint32_t)W + k);
+                };
+                auto nc = [&](uint32_t k) { return k == kLrInfK ? -1 : (int32_t)k; };
+                if (Lrow)
+                    __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab(kc[0], rc[0]), lab(kc[1], rc[1]),
+                                                                       lab(kc[2], rc[2]), lab(kc[3], rc[3])));
+                if (Nrow)
+                    __stcs(reinterpret_cast<int4*>(Nrow + j), make_int4(nc(kc[0]), nc(kc[1]), nc(kc[2]), nc(kc[3])));
+            } else {
+                if (j < c1) put(j, d0, kc[0], rc[0]);
+                if (j + 1 < c1) put(j + 1, d1, kc[1], rc[1]);
+                if (j + 2 < c1) put(j + 2, d2, kc[2], rc[2]);
+                if (j + 3 < c1) put(j + 3, d3, kc[3], rc[3]);
+            }
+            // the next block's first owner: the last entry starting <= b+128
+            const int sn = __shfl_sync(FULL, s, nin + 1);
+            base += nin + (sn == b + 128 ? 1 : 0);
+            b += 128;
+        } else if (nin < 31) {
+            // ---- 128-column block, 4 columns per lane: the window holds
+            // every owner; bit (s-b)&31 of word (s-b)>>5 marks a start ----
+            const bool in = lane >= 1 && s <= b + 127;
+            const int off = s - b;
+            uint32_t Zw[4];
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+                Zw[w] = __reduce_or_sync(FULL, (in && (off >> 5) == w) ? 1u << (off & 31) : 0u);
+            const int w = lane >> 3, bit = (4 * lane) & 31;
+            const uint32_t Z = w == 0 ? Zw[0] : w == 1 ? Zw[1] : w == 2 ? Zw[2] : Zw[3];
+            const int P = (w >= 1 ? __popc(Zw[0]) : 0) + (w >= 2 ? __popc(Zw[1]) : 0) +
+                          (w >= 3 ? __popc(Zw[2]) : 0);
+            const int o0 = P + __popc(Z & ((2u << bit) - 1u));
+            const int o1 = o0 + (int)((Z >> (bit + 1)) & 1u);
+            const int o2 = o1 + (int)((Z >> (bit + 2)) & 1u);
+            const int o3 = o2 + (int)((Z >> (bit + 3)) & 1u);
+            uint32_t k0 = __shfl_sync(FULL, wk, o0), g0 = __shfl_sync(FULL, wg, o0);
+            uint32_t k3 = __shfl_sync(FULL, wk, o3), g3 = __shfl_sync(FULL, wg, o3);
+            uint32_t k1 = o1 == o0 ? k0 : k3, g1 = o1 == o0 ? g0 : g3;
+            uint32_t k2 = o2 == o3 ? k3 : k0, g2 = o2 == o3 ? g3 : g0;
+            if (__any_sync(FULL, o3 - o0 >= 2)) {  // three or more owners in 4 columns
+                k1 = __shfl_sync(FULL, wk, o1);
+                g1 = __shfl_sync(FULL, wg, o1);
+                k2 = __shfl_sync(FULL, wk, o2);
+                g2 = __shfl_sync(FULL, wg, o2);
+            }
+            uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+            if (Lrow) {
+                r0 = __shfl_sync(FULL, wr, o0);
+                r1 = __shfl_sync(FULL, wr, o1);
+                r2 = __shfl_sync(FULL, wr, o2);
+                r3 = __shfl_sync(FULL, wr, o3);
+            }
+            const int j = b + 4 * lane;
+            const uint32_t d0 = dval(g0, k0, j), d1 = dval(g1, k1, j + 1);
+            const uint32_t d2 = dval(g2, k2, j + 2), d3 = dval(g3, k3, j + 3);
+            if (vec4 && j + 3 < c1) {
+                if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
+                if (Srow)
+                    __stcs(reinterpret_cast<float4*>(Srow + j),
+                           make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
+                if (Lrow) {
+                    auto lab = [&](uint32_t k, uint32_t r) {
+                        return k == kLrInfK ? -1 : (int32_t)(r * (uint32_t)W + k);
+                    };
+                    __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab(k0, r0), lab(k1, r1), lab(k2, r2), lab(k3, r3)));
+                }
+                if (Nrow) {
+                    auto nc = [&](uint32_t k) { return k == kLrInfK ? -1 : (int32_t)k; };
+                    __stcs(reinterpret_cast<int4*>(Nrow + j), make_int4(nc(k0), nc(k1), nc(k2), nc(k3)));
+                }
+            } else {
+                if (j < c1) put(j, d0, k0, r0);
+                if (j + 1 < c1) put(j + 1, d1, k1, r1);
+                if (j + 2 < c1) put(j + 2, d2, k2, r2);
+                if (j + 3 < c1) put(j + 3, d3, k3, r3);
+            }
+            // the next block's first owner: the last entry starting <= b+128
+            const int sn = __shfl_sync(FULL, s, min(nin + 1, 31));
+            base += nin + ((nin + 1 <= 31 && sn == b + 128) ? 1 : 0);
+            b += 128;
+        } else {
+            // ---- dense stretch: one 32-column block, lane = column ----
+            const bool in = lane >= 1 && s <= b + 31;
+            const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
+            const int ow = __popc(Z & ((2u << lane) - 1u));
+            const uint32_t k = __shfl_sync(FULL, wk, ow);
+            const uint32_t g = __shfl_sync(FULL, wg, ow);
+            const uint32_t r = __shfl_sync(FULL, wr, ow);
+            const int j = b + lane;
+            if (j < c1) put(j, dval(g, k, j), k, r);
+            // the next block's first owner: the last entry starting <= b+32
+            // (up to 32 entries after base: entry base+32 is read by lane 0)
+            const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (rE[base + 32] >> 16) : 0xffffu;
+            base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
+                    ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
+            b += 32;
+        }
+    }
+}
+
 template <bool TAKE_NEW>
 __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_t* ent, uint16_t* entr, int Ws,
                                                            int C, int* fail_rows, int* fail_count) {
@@ -78,7 +246,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
     bool active = row < a.total_rows;
     const int img = active ? (int)(row / a.H) : 0;
     if (a.lr_gate) {  // default mode: only the rows of sparse planes
-        active = active && lr_plane(a.plane_counts, img, a.H, a.W);
+        active = active && lr_plane(a.plane_counts, img, a.H, a.W) && !pts_plane(a.plane_counts, img, a.pts_gate);
         if (!__any_sync(FULL, active)) return;
     }
     const uint32_t i = active ? (uint32_t)(row - (int64_t)img * a.H) : 0u;
@@ -312,164 +480,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
             int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + imgR * a.sN) + iR * W : nullptr;
             const uint32_t* rE = sE + (rho - r0) * S;
             const uint16_t* rR = sR + (rho - r0) * S;
-            const bool vec4 = a.vec;  // 16-byte stores legal (W % 4 == 0, aligned planes)
-            auto put = [&](int j, uint32_t d, uint32_t k, uint32_t r) {  // one column, scalar
-                const bool inf = k == kLrInfK;
-                if (Drow) __stcs(Drow + j, (int32_t)d);
-                if (Srow) __stcs(Srow + j, dist_f32(d));
-                if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(r * (uint32_t)W + k));
-                if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
-            };
-            auto dval = [&](uint32_t g, uint32_t k, int j) -> uint32_t {
-                const int dj = j - (int)k;
-                return g == kInfU ? (uint32_t)DFC_INF_I32 : g + (uint32_t)(dj * dj);
-            };
-            int base = 0;  // entry owning column b
-            int b = c0;
-            while (b < c1) {
-                // window: lane e holds entry base + e; entries 1.. start after b-1
-                const int idx = base + lane;
-                const uint32_t we = idx < nE ? rE[idx] : FULL;
-                const uint32_t wr = idx < nE ? (uint32_t)rR[idx] : kNoRow;
-                const int s = (int)(we >> 16);
-                const uint32_t wk = we & 0xffffu;
-                const uint32_t wav = giR > wr ? giR - wr : wr - giR;
-                const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
-                const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
-                if (nin <= 3) {
-                    // ---- 128-column block with at most 3 owner changes (sparse rows):
-                    // broadcast the block's owners, each column keeps the last one
-                    // starting at or before it ----
-                    const int j = b + 4 * lane;
-                    uint32_t kc[4], gc[4], rc[4];
-                    {
-                        const uint32_t k0 = __shfl_sync(FULL, wk, 0), g0 = __shfl_sync(FULL, wg, 0);
-                        const uint32_t r0 = __shfl_sync(FULL, wr, 0);
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            kc[t] = k0;
-                            gc[t] = g0;
-                            rc[t] = r0;
-                        }
-                    }
-                    for (int e = 1; e <= nin; ++e) {  // warp-uniform trip count
-                        const int se = __shfl_sync(FULL, s, e);
-                        const uint32_t ke = __shfl_sync(FULL, wk, e), ge = __shfl_sync(FULL, wg, e);
-                        const uint32_t re = __shfl_sync(FULL, wr, e);
-#pragma unroll
-                        for (int t = 0; t < 4; ++t)
-                            if (j + t >= se) {
-                                kc[t] = ke;
-                                gc[t] = ge;
-                                rc[t] = re;
-                            }
-                    }
-                    const uint32_t d0 = dval(gc[0], kc[0], j), d1 = dval(gc[1], kc[1], j + 1);
-                    const uint32_t d2 = dval(gc[2], kc[2], j + 2), d3 = dval(gc[3], kc[3], j + 3);
-                    if (vec4 && j + 3 < c1) {
-                        if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
-                        if (Srow)
-                            __stcs(reinterpret_cast<float4*>(Srow + j),
-                                   make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
-                        auto lab = [&](uint32_t k, uint32_t r) {
-                            return k == kLrInfK ? -1 : (int32_t)(r * (uint32_t)W + k);
-                        };
-                        auto nc = [&](uint32_t k) { return k == kLrInfK ? -1 : (int32_t)k; };
-                        if (Lrow)
-                            __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab(kc[0], rc[0]), lab(kc[1], rc[1]),
-                                                                               lab(kc[2], rc[2]), lab(kc[3], rc[3])));
-                        if (Nrow)
-                            __stcs(reinterpret_cast<int4*>(Nrow + j), make_int4(nc(kc[0]), nc(kc[1]), nc(kc[2]), nc(kc[3])));
-                    } else {
-                        if (j < c1) put(j, d0, kc[0], rc[0]);
-                        if (j + 1 < c1) put(j + 1, d1, kc[1], rc[1]);
-                        if (j + 2 < c1) put(j + 2, d2, kc[2], rc[2]);
-                        if (j + 3 < c1) put(j + 3, d3, kc[3], rc[3]);
-                    }
-                    // the next block's first owner: the last entry starting <= b+128
-                    const int sn = __shfl_sync(FULL, s, nin + 1);
-                    base += nin + (sn == b + 128 ? 1 : 0);
-                    b += 128;
-                } else if (nin < 31) {
-                    // ---- 128-column block, 4 columns per lane: the window holds
-                    // every owner; bit (s-b)&31 of word (s-b)>>5 marks a start ----
-                    const bool in = lane >= 1 && s <= b + 127;
-                    const int off = s - b;
-                    uint32_t Zw[4];
-#pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        Zw[w] = __reduce_or_sync(FULL, (in && (off >> 5) == w) ? 1u << (off & 31) : 0u);
-                    const int w = lane >> 3, bit = (4 * lane) & 31;
-                    const uint32_t Z = w == 0 ? Zw[0] : w == 1 ? Zw[1] : w == 2 ? Zw[2] : Zw[3];
-                    const int P = (w >= 1 ? __popc(Zw[0]) : 0) + (w >= 2 ? __popc(Zw[1]) : 0) +
-                                  (w >= 3 ? __popc(Zw[2]) : 0);
-                    const int o0 = P + __popc(Z & ((2u << bit) - 1u));
-                    const int o1 = o0 + (int)((Z >> (bit + 1)) & 1u);
-                    const int o2 = o1 + (int)((Z >> (bit + 2)) & 1u);
-                    const int o3 = o2 + (int)((Z >> (bit + 3)) & 1u);
-                    uint32_t k0 = __shfl_sync(FULL, wk, o0), g0 = __shfl_sync(FULL, wg, o0);
-                    uint32_t k3 = __shfl_sync(FULL, wk, o3), g3 = __shfl_sync(FULL, wg, o3);
-                    uint32_t k1 = o1 == o0 ? k0 : k3, g1 = o1 == o0 ? g0 : g3;
-                    uint32_t k2 = o2 == o3 ? k3 : k0, g2 = o2 == o3 ? g3 : g0;
-                    if (__any_sync(FULL, o3 - o0 >= 2)) {  // three or more owners in 4 columns
-                        k1 = __shfl_sync(FULL, wk, o1);
-                        g1 = __shfl_sync(FULL, wg, o1);
-                        k2 = __shfl_sync(FULL, wk, o2);
-                        g2 = __shfl_sync(FULL, wg, o2);
-                    }
-                    uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-                    if (Lrow) {
-                        r0 = __shfl_sync(FULL, wr, o0);
-                        r1 = __shfl_sync(FULL, wr, o1);
-                        r2 = __shfl_sync(FULL, wr, o2);
-                        r3 = __shfl_sync(FULL, wr, o3);
-                    }
-                    const int j = b + 4 * lane;
-                    const uint32_t d0 = dval(g0, k0, j), d1 = dval(g1, k1, j + 1);
-                    const uint32_t d2 = dval(g2, k2, j + 2), d3 = dval(g3, k3, j + 3);
-                    if (vec4 && j + 3 < c1) {
-                        if (Drow) __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
-                        if (Srow)
-                            __stcs(reinterpret_cast<float4*>(Srow + j),
-                                   make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
-                        if (Lrow) {
-                            auto lab = [&](uint32_t k, uint32_t r) {
-                                return k == kLrInfK ? -1 : (int32_t)(r * (uint32_t)W + k);
-                            };
-                            __stcs(reinterpret_cast<int4*>(Lrow + j), make_int4(lab(k0, r0), lab(k1, r1), lab(k2, r2), lab(k3, r3)));
-                        }
-                        if (Nrow) {
-                            auto nc = [&](uint32_t k) { return k == kLrInfK ? -1 : (int32_t)k; };
-                            __stcs(reinterpret_cast<int4*>(Nrow + j), make_int4(nc(k0), nc(k1), nc(k2), nc(k3)));
-                        }
-                    } else {
-                        if (j < c1) put(j, d0, k0, r0);
-                        if (j + 1 < c1) put(j + 1, d1, k1, r1);
-                        if (j + 2 < c1) put(j + 2, d2, k2, r2);
-                        if (j + 3 < c1) put(j + 3, d3, k3, r3);
-                    }
-                    // the next block's first owner: the last entry starting <= b+128
-                    const int sn = __shfl_sync(FULL, s, min(nin + 1, 31));
-                    base += nin + ((nin + 1 <= 31 && sn == b + 128) ? 1 : 0);
-                    b += 128;
-                } else {
-                    // ---- dense stretch: one 32-column block, lane = column ----
-                    const bool in = lane >= 1 && s <= b + 31;
-                    const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
-                    const int ow = __popc(Z & ((2u << lane) - 1u));
-                    const uint32_t k = __shfl_sync(FULL, wk, ow);
-                    const uint32_t g = __shfl_sync(FULL, wg, ow);
-                    const uint32_t r = __shfl_sync(FULL, wr, ow);
-                    const int j = b + lane;
-                    if (j < c1) put(j, dval(g, k, j), k, r);
-                    // the next block's first owner: the last entry starting <= b+32
-                    // (up to 32 entries after base: entry base+32 is read by lane 0)
-                    const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (rE[base + 32] >> 16) : 0xffffu;
-                    base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
-                            ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
-                    b += 32;
-                }
-            }
+            lr_fill_row(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
         }
     }
     // rows whose list exceeds the staging capacity (chunks wider than kStage
@@ -521,11 +532,13 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
 // k_rows_dense (flag 1), and not a sparse-plane row k_rows_lr completed
 // (sparse plane, flag != 2).  Appended to a list (any order).
 __global__ void k_rows_rest(const uint8_t* row_done, const unsigned long long* counts, int64_t total_rows,
-                            int H, int W, bool lr_gate, int* list, int* count) {
+                            int H, int W, bool lr_gate, bool pts_gate, int* list, int* count) {
     for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < total_rows;
          row += (int64_t)gridDim.x * blockDim.x) {
         const uint8_t rd = row_done[row];
-        const bool mine = rd == 2 || (rd == 0 && !(lr_gate && lr_plane(counts, (int)(row / H), H, W)));
+        const int img = (int)(row / H);
+        const bool mine = !pts_plane(counts, img, pts_gate) &&
+                          (rd == 2 || (rd == 0 && !(lr_gate && lr_plane(counts, img, H, W))));
         const unsigned m = __ballot_sync(__activemask(), mine);
         if (m == 0) continue;
         const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;

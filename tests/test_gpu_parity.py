@@ -462,3 +462,43 @@ def test_vertical_direction_passes(dfc):
     got = d.cpu().numpy()
     np.testing.assert_array_equal(np.where(want < 0, -1, got), np.where(want < 0, -1, want))
     assert (got[want < 0] == -1).all()
+
+
+@pytest.mark.parametrize("npts", [0, 1, 2, 30, 63, 64, 65, 200])
+def test_point_planes(dfc, npts):
+    """Planes with at most 64 object pixels (k_rows_pts: K1a's object list, no
+    nearest-row plane): same maps, labels and nearest columns as the oracle, at
+    the 64-pixel boundary of the path and beyond it; several points per column
+    (vertical ties), corners, and a featureless plane."""
+    rng = np.random.default_rng(100 + npts)
+    H, W = 96, 160
+    img = np.zeros((H, W), np.uint8)
+    cols = rng.integers(0, 12, size=npts) * 13 % W  # few distinct columns: many points per column
+    rows = rng.integers(0, H, size=npts)
+    img[rows, cols] = 1
+    if npts >= 2:
+        img[0, 0] = img[H - 1, W - 1] = 1
+        img[10, 50] = img[20, 50] = 1  # an equidistant pair in one column (upper row wins at row 15)
+    k = int(img.sum())
+    assert (k <= 64) == (npts <= 63) or npts in (64, 65, 200)
+    _check_edt(dfc, img)
+    batch = np.stack([img, np.roll(img, 7, axis=1), np.zeros_like(img), img[::-1].copy()])
+    out = dfc.edt_batched(_dev(batch), dist=True, label=True)
+    torch.cuda.synchronize()
+    for b in range(batch.shape[0]):
+        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(batch[b])))
+        lab = oracle.voronoi_labels(batch[b], linear=True)
+        want = np.full((H, W), -1, np.int32) if lab is None else lab[1]
+        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), want)
+
+
+def test_point_plane_dual_polarity(dfc):
+    """An image with only a few BACKGROUND pixels: its object->background plane is
+    a point plane while the other is dense."""
+    img = np.ones((64, 200), np.uint8)
+    img[5, 7] = img[40, 7] = img[63, 199] = img[20, 100] = 0
+    _check_edt(dfc, img, polarity=1)
+    dual = dfc.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
+    np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
