@@ -62,7 +62,7 @@ struct RasterArgs {
 // the points path on (default row pass, rows per plane a multiple of 32) its
 // rows go to k_rows_pts, which works from K1a's list of object pixels; no
 // nearest-row plane is written or read for it.
-constexpr int kPtsCap = 64;
+constexpr int kPtsCap = 32;
 __host__ __device__ __forceinline__ bool pts_plane(const unsigned long long* counts, int img, bool on) {
     return on && counts != nullptr && counts[img] <= (unsigned long long)kPtsCap;
 }

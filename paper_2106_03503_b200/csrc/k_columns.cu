@@ -218,6 +218,11 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
     const int j0 = 4 * g;
     if (j0 >= a.W) return;
     const int b = blockIdx.y, im = blockIdx.z;
+    if (a.pts) {  // every slot a point plane: nothing to write (CTA-uniform)
+        bool all = true;
+        for (int s = 0; s < a.npol; ++s) all = all && a.pcounts[(int64_t)s * a.n_img + im] <= (unsigned long long)kPtsCap;
+        if (all) return;
+    }
     const int r0 = b * kBand;
     const int nrows = min(kBand, a.H - r0);
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);

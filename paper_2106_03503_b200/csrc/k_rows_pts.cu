@@ -7,8 +7,8 @@
 // pixels, so K1b/K1c skip the plane and this kernel reads only that list.
 //
 //  list    one warp = 32 rows of one plane (rows per plane a multiple of 32).
-//          The warp sorts the plane's <= kPtsCap keys (column << 16 | row) by
-//          rank counting (keys are distinct pixels) and compacts the distinct
+//          The warp sorts the plane's <= kPtsCap (32) keys (column << 16 | row)
+//          by rank counting (keys are distinct pixels) and compacts the distinct
 //          object columns with their row ranges.
 //  build   lane = row i: for every object column k in order, the nearest object
 //          row of that column (binary search in the column's sorted rows; the
@@ -24,7 +24,7 @@
 
 namespace dfc {
 
-constexpr int kPtsWarps = 2;  // ~17 KB of static shared memory per warp
+constexpr int kPtsWarps = 4;  // ~8.6 KB of static shared memory per warp
 constexpr int kPtsStride = kPtsCap + 1;  // words per row's envelope (odd: conflict-free)
 
 struct PtsSmem {
@@ -51,16 +51,11 @@ __global__ void __launch_bounds__(32 * kPtsWarps) k_rows_pts(RowArgs a, const ui
 
     // ---- sort the plane's keys (rank = number of smaller keys) ----
     const uint32_t* src = pts + (int64_t)img * kPtsCap;
+    static_assert(kPtsCap <= 32, "one key per lane");
     const uint32_t k0 = lane < n ? __ldg(src + lane) : FULL;
-    const uint32_t k1 = lane + 32 < n ? __ldg(src + lane + 32) : FULL;
-    int rank0 = 0, rank1 = 0;
-    for (int q = 0; q < n; ++q) {
-        const uint32_t kq = __shfl_sync(FULL, q < 32 ? k0 : k1, q & 31);
-        rank0 += kq < k0;
-        rank1 += kq < k1;
-    }
+    int rank0 = 0;
+    for (int q = 0; q < n; ++q) rank0 += __shfl_sync(FULL, k0, q) < k0;
     if (lane < n) sm.key[rank0] = k0;
-    if (lane + 32 < n) sm.key[rank1] = k1;
     __syncwarp();
     // ---- distinct columns: a key starts a column when its column differs ----
     int nu = 0;
