@@ -47,7 +47,7 @@ CONFIGS = {
     "c2": dict(desc="c2: 4096x4096 uint8, 200 seeded discs (r 8..64), exact squared EDT both "
                     "polarities int32 + float32 distances", bytes_alg=17, bytes_kernel=4 + 16),
     "c3": dict(desc="c3: 1024 images 1024x1024 uint8, 30 seeded points each, exact squared EDT "
-                    "int32 + int32 Voronoi labels", bytes_alg=9, bytes_kernel=2 + 8),
+                    "int32 + int32 Voronoi labels", bytes_alg=9, bytes_kernel=8),  # point planes: no nr plane
     "c4": dict(desc="c4: 8192x8192 uint8, 2000 seeded discs/rectangles, city-block + chessboard + "
                     "chamfer-3-4 int32", bytes_alg=13, bytes_kernel=2 + 12),
     "c5": dict(desc="c5: 32768x32768 uint8, Bernoulli 1e-4 in 256 of 1024 tiles, exact squared "
@@ -59,7 +59,7 @@ CONFIGS = {
 ROW_KERNELS = {
     "c1": "row pass (k_rows: both planes are neither dense nor sparse)",
     "c2": "row pass (k_rows_dense for the object->background plane + k_rows for the other)",
-    "c3": "row pass (k_rows_lr: every image is a sparse plane)",
+    "c3": "row pass (k_rows_pts: every image is a point plane, <= 32 object pixels)",
     "c4": "k_band_* + k_raster (whole step)",
     "c5": "row pass (k_rows_lr: a sparse plane)",
 }
