@@ -225,7 +225,11 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
  * 16384 columns; wider rows use k_rows), 4 = dense-row kernel (k_rows_dense)
  * for rows with only short runs between object pixels and k_rows for the rest,
  * 5 = lane-per-row chunk scan (k_rows_lr, with k_rows as its overflow
- * fallback).  Results are identical; this is a performance/testing knob.
+ * fallback), 6 = the default: as 4, but anchored segments (k_rows_anc: one
+ * CTA per row, one lane per column of a 32-column segment, rows up to 16384
+ * columns) instead of k_rows for every row the point-plane, dense-row and
+ * sparse-plane kernels do not take.  Results are identical; this is a
+ * performance/testing knob.
  */
 int dfc_set_row_kernel(int mode);
 

@@ -30,7 +30,10 @@ int env_row_mode() {
         if (v && strcmp(v, "segment") == 0) return 1;
         if (v && strcmp(v, "dense") == 0) return 4;
         if (v && strcmp(v, "lr") == 0) return 5;
-        return 4;  // default: dense-row kernel, then the segment/merge kernel for the other rows
+        if (v && strcmp(v, "anc") == 0) return 6;
+        // default: point planes, dense rows, sparse planes, then anchored
+        // segments for the rest (k_rows where those do not apply)
+        return 6;
     }();
     return m;
 }
@@ -320,10 +323,15 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         return DFC_OK;
     }
 
-    // Default: per plane by its object count (column pass) -- dense planes
-    // (>= 50% object pixels, W <= kDenseMaxW) by k_rows_dense, sparse planes
-    // (< 1/256) by k_rows_lr, the rest (and rows those two flag) by k_rows.
-    if (mode == 4) {
+    // Default (6): per plane by its object count (column pass) -- point planes
+    // by k_rows_pts, dense planes (>= 50% object pixels, W <= kDenseMaxW) by
+    // k_rows_dense, sparse planes (< 1/256) by k_rows_lr, the rest (and rows
+    // those flag) by k_rows_anc; by k_rows where k_rows_anc does not apply
+    // (rows wider than kAncMaxW, column-tiled planes) and in mode 4.
+    if (mode == 4 || mode == 6) {
+        // anchored segments (k_rows_anc.cu) for every row the point / sparse
+        // kernels do not own: one tile, W <= kAncMaxW
+        const bool anc_on = mode == 6 && W <= kAncMaxW && a.tile_cols >= W && row0 == 0 && H <= 32768;
         const bool dense_on = W <= kDenseMaxW;
         const bool lr_on = lr_ok && plane_counts != nullptr;
         Scratch fl(st);
@@ -361,6 +369,22 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         if (lr_on) {  // rows of sparse planes; overflowed rows flagged 2
             const int rc = launch_lr(a, static_cast<char*>(fl.p) + flag_bytes + list_bytes, nullptr, nullptr);
             if (rc != DFC_OK) return rc;
+        }
+        if (anc_on) {
+            RowArgs aa = a;
+            aa.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0;
+            const bool owners = LB != nullptr || NC != nullptr;
+            const void* afn = take_new ? (owners ? anc_kernel_ptr<true, true>() : anc_kernel_ptr<true, false>())
+                                       : (owners ? anc_kernel_ptr<false, true>() : anc_kernel_ptr<false, false>());
+            const int asm_bytes = anc_smem_bytes((int)W);
+            e = cudaFuncSetAttribute(afn, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes);
+            if (e != cudaSuccess) return cuda_fail(e);
+            const int64_t ablocks = std::min<int64_t>(a.total_rows, 148 * 16);
+            void* aargs[] = {&aa};
+            e = cudaLaunchKernel(afn, dim3((unsigned)ablocks), dim3(32 * kAncWarps), aargs, (size_t)asm_bytes, st);
+            if (e != cudaSuccess) return cuda_fail(e);
+            ++g_launches;
+            return DFC_OK;
         }
         // the segment kernel over the remaining rows: few rows -> one CTA group per
         // row group, skipping flagged rows (cheapest); many rows -> a compact
@@ -455,7 +479,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     const size_t nr_elems = (size_t)(planes * H * Wp);
     // point planes (k_rows_pts) in the default row pass when planes are whole warps of rows
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
-    const bool pts_on = mode == 4 && H % 32 == 0;
+    const bool pts_on = (mode == 4 || mode == 6) && H % 32 == 0;
     Scratch sc(st);
     cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 512 + (size_t)planes * 8 +
                              (pts_on ? (size_t)planes * kPtsCap * 4 : 0));
@@ -829,7 +853,7 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 }
 
 int dfc_set_row_kernel(int mode) {
-    if (mode < 0 || mode > 5) return DFC_ERR_ARG;
+    if (mode < 0 || mode > 6) return DFC_ERR_ARG;
     g_row_mode = mode;
     return DFC_OK;
 }

@@ -1,0 +1,301 @@
+// k_rows_anc.cu -- stage 2 as ANCHORED SEGMENTS: one CTA per row, anchors by
+// divide and conquer, then a uniform brute-force pass per 32-column segment.
+//
+// Same result as k_rows.cu (envelope_rows / meijster_scan / voronoi label
+// assembly, exact_edt.cpp:190-283, :362-369), different decomposition.  The
+// reference builds the lower envelope of the parabolas D_k(j) = g_k + (j-k)^2
+// with a stack (exact_edt.cpp:208-223); its owners (the smallest minimiser
+// under keep_old, the largest under take_new, :205/:275) are monotone in j.
+// This kernel uses only that monotonicity:
+//
+//  stage    the row's vertical values g_k = (i - nr_k)^2 (kAncInf: no object
+//           in column k, :212) go to the CTA's shared memory once.
+//  anchors  owner(32 s) for every segment s, by divide and conquer over s:
+//           owner(32 s) lies in [owner(32 s_lo), owner(32 s_hi)] for any
+//           computed s_lo < s < s_hi (bounds: the first / last finite column).
+//           Each anchor is a warp-parallel scan of its candidate range (lane =
+//           candidate, the tie rule within a lane by scan order) and a REDUX
+//           min over the values, then min / max over the columns attaining it.
+//           The ranges of one level overlap only at their ends, so a level
+//           costs about W/32 warp iterations.
+//  segments lane = column j of segment [32 s, 32 s + 32): brute force over the
+//           candidates [owner(32 s), owner(32 s + 32)] (owner(W) := the last
+//           finite column) in increasing order, keep_old updating on <,
+//           take_new on <=.  Every iteration is warp-uniform: no divergence,
+//           no stack, and the ranges of a row sum to about W + W/32.
+//
+// A row with no finite g is written as featureless (D = DFC_INF_I32).
+#include "dfc_kernels.cuh"
+
+namespace dfc {
+
+constexpr int kAncWarps = 4;               // warps per CTA (one row per CTA)
+constexpr int kAncMaxW = 16384;
+// Shared memory holds h_k = g_k + k^2 (int32), so that D_k(j) - j^2 = h_k - 2 j k
+// is one multiply-add (or, with 2 j k carried along, one 3-way add).  A column
+// without objects gets g = kAncInf: above every real D (rows <= 32768, columns
+// <= kAncMaxW: D <= 32767^2 + 16383^2 < 1.35e9), and h, h - 2jk stay inside int32.
+constexpr int32_t kAncInf = 0x60000000;
+
+__host__ __device__ __forceinline__ int anc_segs(int W) { return (W + 31) >> 5; }
+// words: g (W, 16-byte granules), anchors (S + 1), per-warp partial owners (2 NW), bounds (2 NW)
+__host__ __device__ __forceinline__ int anc_gwords(int W) { return (W + 3) & ~3; }
+inline int anc_smem_bytes(int W) { return (anc_gwords(W) + anc_segs(W) + 1 + 4 * kAncWarps) * 4; }
+
+// The rows this kernel owns in the default row pass: not a point plane; in a
+// sparse plane (k_rows_lr) only the rows that kernel flagged (2); elsewhere the
+// rows k_rows_dense did not write (1).
+__device__ __forceinline__ bool anc_row_mine(const RowArgs& a, int64_t row, int img) {
+    if (pts_plane(a.plane_counts, img, a.pts_gate)) return false;
+    const uint8_t rd = a.row_done ? a.row_done[row] : 0;
+    if (a.lr_gate && lr_plane(a.plane_counts, img, a.H, a.W)) return rd == 2;
+    return rd != 1;
+}
+
+constexpr int32_t kAncNone = 0x7FFFFFFF;  // "no candidate" (empty range)
+
+// Minimum of D_k(j) - j^2 = h_k - 2 j k over the candidates [lo, hi] (possibly
+// empty: kAncNone) and the column attaining it: lane = candidate, ascending per
+// lane (two candidates per step); then a REDUX min over the values and, among
+// the lanes attaining it, the smallest (keep_old) or largest (take_new) column.
+template <bool TAKE_NEW>
+__device__ __forceinline__ int32_t anc_owner(const int32_t* h, int j, int lo, int hi, int lane, int& col) {
+    int32_t best = kAncNone;
+    int bk = lo;
+    const int c = -2 * j;
+    int k = lo + lane;
+    for (; k + 32 <= hi; k += 64) {
+        const int32_t v0 = h[k] + c * k, v1 = h[k + 32] + c * (k + 32);
+        if (TAKE_NEW ? v0 <= best : v0 < best) {
+            best = v0;
+            bk = k;
+        }
+        if (TAKE_NEW ? v1 <= best : v1 < best) {
+            best = v1;
+            bk = k + 32;
+        }
+    }
+    if (k <= hi) {
+        const int32_t v0 = h[k] + c * k;
+        if (TAKE_NEW ? v0 <= best : v0 < best) {
+            best = v0;
+            bk = k;
+        }
+    }
+    const int32_t m = __reduce_min_sync(0xffffffffu, best);
+    col = TAKE_NEW ? (int)__reduce_max_sync(0xffffffffu, best == m ? (uint32_t)bk : 0u)
+                   : (int)__reduce_min_sync(0xffffffffu, best == m ? (uint32_t)bk : 0xFFFFFFFFu);
+    return m;
+}
+
+template <bool TAKE_NEW, bool OWNERS>
+__global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
+    extern __shared__ uint4 ancsm[];
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int NW = kAncWarps;
+    const int W = a.W;
+    const int S = anc_segs(W);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    int32_t* g = reinterpret_cast<int32_t*>(ancsm);         // h_k = g_k + k^2
+    int* anc = reinterpret_cast<int*>(g + anc_gwords(W));  // [S + 1]
+    int32_t* pv = reinterpret_cast<int32_t*>(anc + S + 1);  // [NW] partial minima
+    int* pk = reinterpret_cast<int*>(pv + NW);                // [NW] their columns
+    int* rf = pk + NW;                                        // [NW] first finite column per warp
+    int* rl = rf + NW;                                        // [NW] last finite column per warp
+    int P = 1;                                                // power of two >= S
+    while (P < S) P <<= 1;
+
+    for (int64_t row = blockIdx.x; row < a.total_rows; row += gridDim.x) {
+        const int img = (int)(row / a.H);
+        if (!anc_row_mine(a, row, img)) continue;  // CTA-uniform
+        const uint32_t i = (uint32_t)(row - (int64_t)img * a.H);
+        const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
+        const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
+
+        // ---- stage g and the first / last finite column ----
+        int ff = W, lf = -1;
+        auto gval = [&](int j, uint32_t r) -> int32_t {
+            int32_t gv = kAncInf;
+            if (r != kNoRow) {
+                ff = min(ff, j);
+                lf = max(lf, j);
+                const uint32_t av = gi > r ? gi - r : r - gi;
+                gv = (int32_t)(av * av);
+            }
+            return gv + j * j;
+        };
+        if (a.vec_nr) {
+            const uint4* src = reinterpret_cast<const uint4*>(rowp);
+            const int nvec = (W + 7) >> 3;
+            for (int v = tid; v < nvec; v += 32 * NW) {
+                const uint4 q = __ldg(src + v);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                int32_t o[8];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int j = 8 * v + 2 * t;
+                    o[2 * t] = j < W ? gval(j, w[t] & 0xffffu) : kAncInf + j * j;
+                    o[2 * t + 1] = j + 1 < W ? gval(j + 1, w[t] >> 16) : kAncInf + (j + 1) * (j + 1);
+                }
+                if (8 * v + 7 < W || (W & 3) == 0) {
+                    reinterpret_cast<int4*>(g)[2 * v] = make_int4(o[0], o[1], o[2], o[3]);
+                    if (8 * v + 4 < W) reinterpret_cast<int4*>(g)[2 * v + 1] = make_int4(o[4], o[5], o[6], o[7]);
+                } else {
+                    for (int t = 0; t < 8 && 8 * v + t < anc_gwords(W); ++t) g[8 * v + t] = o[t];
+                }
+            }
+        } else {
+            for (int j = tid; j < anc_gwords(W); j += 32 * NW) g[j] = j < W ? gval(j, __ldg(rowp + j)) : kAncInf + j * j;
+        }
+        ff = __reduce_min_sync(FULL, ff);
+        lf = __reduce_max_sync(FULL, lf);
+        if (lane == 0) {
+            rf[warp] = ff;
+            rl[warp] = lf;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            ff = min(ff, rf[w]);
+            lf = max(lf, rl[w]);
+        }
+
+        int32_t* Drow = a.D ? reinterpret_cast<int32_t*>(a.D + img * a.sD) + (int64_t)i * W : nullptr;
+        float* Srow = a.S ? reinterpret_cast<float*>(a.S + img * a.sS) + (int64_t)i * W : nullptr;
+        int32_t* Lrow = a.LB ? reinterpret_cast<int32_t*>(a.LB + img * a.sL) + (int64_t)i * W : nullptr;
+        int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + img * a.sN) + (int64_t)i * W : nullptr;
+
+        if (lf < 0) {  // featureless row (CTA-uniform)
+            for (int j = tid; j < W; j += 32 * NW) {
+                if (Drow) __stcs(Drow + j, DFC_INF_I32);
+                if (Srow) __stcs(Srow + j, __int_as_float(0x7f800000));
+                if (Lrow) __stcs(Lrow + j, -1);
+                if (Nrow) __stcs(Nrow + j, -1);
+            }
+            __syncthreads();
+            continue;
+        }
+
+        // ---- anchors owner(32 s), s < S: levels of a divide and conquer over
+        // [0, P] (index >= S stands for owner(W) := lf; index 0 comes last with
+        // lower bound ff).  A level with n >= NW anchors gives each warp whole
+        // anchors; with fewer, each anchor's range is split over NW / n warps
+        // (ascending parts) and the parts are combined with the tie rule. ----
+        if (tid == 0) anc[S] = lf;
+        for (int step = P >> 1; step >= 0; step >>= 1) {
+            const bool last = step == 0;  // anchor 0
+            const int s0 = last ? 0 : step, ds = last ? 1 : 2 * step;
+            const int n = last ? 1 : (S - step + ds - 1) / ds;
+            if (n <= 0) continue;
+            __syncthreads();
+            auto bounds = [&](int s, int& lo, int& hi) {
+                lo = (last || s - step == 0) ? ff : anc[s - step];
+                hi = last ? (S > 1 ? anc[1] : lf) : (s + step >= S ? lf : anc[s + step]);
+            };
+            if (n >= NW) {
+                for (int t = warp; t < n; t += NW) {
+                    const int s = s0 + t * ds;
+                    int lo, hi, col;
+                    bounds(s, lo, hi);
+                    anc_owner<TAKE_NEW>(g, 32 * s, lo, hi, lane, col);
+                    if (lane == 0) anc[s] = col;
+                }
+            } else {
+                const int q = NW / n;
+                const int t = warp / q, part = warp - t * q;
+                int32_t m = kAncNone;
+                int col = 0;
+                if (t < n) {
+                    const int s = s0 + t * ds;
+                    int lo, hi;
+                    bounds(s, lo, hi);
+                    const int c = (hi - lo + q) / q;  // ceil((hi - lo + 1) / q)
+                    const int plo = lo + part * c, phi = min(hi, plo + c - 1);
+                    m = anc_owner<TAKE_NEW>(g, 32 * s, plo, phi, lane, col);
+                }
+                if (lane == 0) {
+                    pv[warp] = m;
+                    pk[warp] = col;
+                }
+                __syncthreads();
+                if (tid < n) {
+                    int32_t bm = kAncNone;
+                    int bc = 0;
+                    for (int p = 0; p < q; ++p) {  // ascending column ranges
+                        const int32_t v = pv[tid * q + p];
+                        if (TAKE_NEW ? (v <= bm && v != kAncNone) : v < bm) {
+                            bm = v;
+                            bc = pk[tid * q + p];
+                        }
+                    }
+                    anc[s0 + tid * ds] = bc;
+                }
+            }
+            if (last) break;
+        }
+        __syncthreads();
+
+        // ---- segments: lane = column, brute force over [owner(j0), owner(j0 + 32)] ----
+        for (int s = warp; s < S; s += NW) {
+            const int j = 32 * s + lane;
+            const int lo = anc[s], hi = anc[s + 1];
+            // D_k(j) - j^2 = h_k - 2 j k, ascending k; the j^2 goes back at the end
+            const int c = -2 * j;
+            int32_t best;
+            int bk = lo;
+            if (OWNERS) {  // the minimiser too: one ordered scan (tie rule by order)
+                best = kAncNone;
+                int ck = c * lo;
+#pragma unroll 4
+                for (int k = lo; k <= hi; ++k, ck += c) {
+                    const int32_t v = g[k] + ck;
+                    if (TAKE_NEW ? v <= best : v < best) {
+                        best = v;
+                        bk = k;
+                    }
+                }
+            } else {
+                // the value only: running minima over the aligned superset
+                // [lo & ~3, hi | 3] of the range (extra candidates cannot go
+                // below the minimum, which the range attains; the padding past
+                // W holds kAncInf + k^2), 16-byte loads of h
+                int32_t b0 = kAncNone, b1 = b0;
+                const int c2 = 2 * c, c3 = 3 * c;
+                int k = lo & ~3;
+                for (; k + 4 <= hi; k += 8) {
+                    const int4 q = *reinterpret_cast<const int4*>(g + k);
+                    const int4 r = *reinterpret_cast<const int4*>(g + k + 4);
+                    const int ck = c * k, ck4 = ck + 2 * c2;
+                    b0 = min(b0, min(q.x + ck, q.y + (ck + c)));
+                    b1 = min(b1, min(q.z + (ck + c2), q.w + (ck + c3)));
+                    b0 = min(b0, min(r.x + ck4, r.y + (ck4 + c)));
+                    b1 = min(b1, min(r.z + (ck4 + c2), r.w + (ck4 + c3)));
+                }
+                if (k <= hi) {
+                    const int4 q = *reinterpret_cast<const int4*>(g + k);
+                    const int ck = c * k;
+                    b0 = min(b0, min(q.x + ck, q.y + (ck + c)));
+                    b1 = min(b1, min(q.z + (ck + c2), q.w + (ck + c3)));
+                }
+                best = min(b0, b1);
+            }
+            const uint32_t dval = (uint32_t)(best + j * j);
+            if (j < W) {
+                if (Drow) __stcs(Drow + j, (int32_t)dval);
+                if (Srow) __stcs(Srow + j, dist_f32(dval));
+                if (OWNERS) {
+                    if (Lrow) __stcs(Lrow + j, (int32_t)((uint32_t)__ldg(rowp + bk) * (uint32_t)W + (uint32_t)bk));
+                    if (Nrow) __stcs(Nrow + j, bk);
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <bool TAKE_NEW, bool OWNERS>
+inline const void* anc_kernel_ptr() {
+    return (const void*)k_rows_anc<TAKE_NEW, OWNERS>;
+}
+
+}  // namespace dfc

@@ -425,6 +425,77 @@ def test_lr_batched_dual_and_discs(lr_kernel):
     _check_edt(lr_kernel, workloads.discs(512, 1000, 12, 9))
 
 
+@pytest.fixture
+def anc_kernel(dfc):
+    """Anchored segments (k_rows_anc.cu) for every non-point, non-sparse row."""
+    dfc.set_row_kernel("anc")
+    yield dfc
+    dfc.set_row_kernel("default")
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (33, 97), (64, 64), (40, 1031), (70, 600), (3, 4100),
+                                   (100, 33), (17, 16384), (9, 2049)])
+@pytest.mark.parametrize("density", [0.0, 0.002, 0.02, 0.3, 0.9, 1.0])
+def test_anc_row_kernel(anc_kernel, shape, density):
+    """Anchored segments give the same maps, labels (keep_old) and nearest columns (take_new)."""
+    img = oracle.random_image(shape[0], shape[1], density, 7 * shape[0] + shape[1] + int(density * 1000))
+    _check_edt(anc_kernel, img)
+    _check_edt(anc_kernel, img, polarity=1)
+
+
+@pytest.fixture
+def merge_kernel(dfc):
+    """The previous default: k_rows (merge tree) for the rows anchored segments now take."""
+    dfc.set_row_kernel("dense")
+    yield dfc
+    dfc.set_row_kernel("default")
+
+
+@pytest.mark.parametrize("shape", [(5, 7), (33, 97), (40, 1031), (3, 4100), (9, 2049)])
+@pytest.mark.parametrize("density", [0.0, 0.02, 0.3, 0.9])
+def test_merge_row_kernel(merge_kernel, shape, density):
+    img = oracle.random_image(shape[0], shape[1], density, 5 * shape[0] + shape[1] + int(density * 1000))
+    _check_edt(merge_kernel, img)
+    _check_edt(merge_kernel, img, polarity=1)
+
+
+def test_anc_ties_and_long_runs(anc_kernel):
+    """Equal-height parabolas (every column a tie candidate), object lines, long
+    empty runs and a single far object: anchors on ties, pops to an empty stack."""
+    img = np.zeros((300, 257), np.uint8)
+    img[0, :] = 1
+    img[299, 100] = 1
+    _check_edt(anc_kernel, img)
+    img2 = np.zeros((200, 512), np.uint8)
+    img2[0, ::2] = 1
+    img2[199, 1::3] = 1
+    _check_edt(anc_kernel, img2)
+    img3 = np.zeros((64, 3000), np.uint8)
+    img3[10, 2999] = 1
+    img3[50, 0] = 1
+    _check_edt(anc_kernel, img3)
+    img4 = np.zeros((40, 640), np.uint8)
+    img4[:, 320] = 1
+    img4[::7, 0] = 1
+    _check_edt(anc_kernel, img4)
+
+
+def test_anc_batched_dual_and_discs(anc_kernel):
+    from paper_2106_03503_b200 import workloads
+    imgs = workloads.points_batch(40, 96, 128, 30, 5)
+    out = anc_kernel.edt_batched(_dev(imgs), dist=True, label=True)
+    img = workloads.discs(256, 384, 10, 3)
+    dual = anc_kernel.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    for b in range(0, 40, 7):
+        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
+        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
+    np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+    np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
+    _check_edt(anc_kernel, workloads.discs(512, 1000, 12, 9))
+    _check_edt(anc_kernel, workloads.discs(512, 1000, 12, 9), polarity=1)
+
+
 def test_vertical_direction_passes(dfc):
     """vertical_down_pass / vertical_up_pass (exact_edt.cpp:74-110) in place over
     arbitrary uint64 maps -- infinities, zeros, squares and arbitrary values,
