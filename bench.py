@@ -58,7 +58,7 @@ CONFIGS = {
 # what the timed "row pass" of each config runs (the default per-plane dispatch)
 ROW_KERNELS = {
     "c1": "row pass (k_rows_anc: the plane is neither dense nor sparse)",
-    "c2": "row pass (k_rows_dense for the object->background plane + k_rows_anc for the other)",
+    "c2": "row pass (k_rows_anc, both planes)",
     "c3": "row pass (k_rows_pts: every image is a point plane, <= 32 object pixels)",
     "c4": "k_band_* + k_raster (whole step)",
     "c5": "row pass (k_rows_lr: a sparse plane)",

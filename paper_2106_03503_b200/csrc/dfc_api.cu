@@ -324,15 +324,21 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     }
 
     // Default (6): per plane by its object count (column pass) -- point planes
-    // by k_rows_pts, dense planes (>= 50% object pixels, W <= kDenseMaxW) by
-    // k_rows_dense, sparse planes (< 1/256) by k_rows_lr, the rest (and rows
-    // those flag) by k_rows_anc; by k_rows where k_rows_anc does not apply
-    // (rows wider than kAncMaxW, column-tiled planes) and in mode 4.
+    // by k_rows_pts, sparse planes (< 1/256) by k_rows_lr, every other row by
+    // k_rows_anc.  Where k_rows_anc does not apply (rows wider than kAncMaxW,
+    // column-tiled planes) and in mode 4: dense planes (>= 50% object pixels,
+    // W <= kDenseMaxW) by k_rows_dense and the rest by k_rows.
     if (mode == 4 || mode == 6) {
         // anchored segments (k_rows_anc.cu) for every row the point / sparse
         // kernels do not own: one tile, W <= kAncMaxW
         const bool anc_on = mode == 6 && W <= kAncMaxW && a.tile_cols >= W && row0 == 0 && H <= 32768;
-        const bool dense_on = W <= kDenseMaxW;
+        // dense planes by k_rows_anc too (all-object segments and anchors on
+        // object pixels are free there); DFC_ANC_DENSE=0 keeps k_rows_dense (A/B)
+        static const bool anc_dense = [] {
+            const char* v = getenv("DFC_ANC_DENSE");
+            return !(v && v[0] == '0');
+        }();
+        const bool dense_on = W <= kDenseMaxW && !(anc_on && anc_dense);
         const bool lr_on = lr_ok && plane_counts != nullptr;
         Scratch fl(st);
         const size_t flag_bytes = (size_t)round_up(a.total_rows, 256);

@@ -185,19 +185,23 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         for (int step = P >> 1; step >= 0; step >>= 1) {
             const bool last = step == 0;  // anchor 0
             const int s0 = last ? 0 : step, ds = last ? 1 : 2 * step;
-            const int n = last ? 1 : (S - step + ds - 1) / ds;
+            const int n = last ? 1 : (S - step + ds - 1) >> (__ffs(ds) - 1);  // ds: a power of two
             if (n <= 0) continue;
             __syncthreads();
             auto bounds = [&](int s, int& lo, int& hi) {
                 lo = (last || s - step == 0) ? ff : anc[s - step];
                 hi = last ? (S > 1 ? anc[1] : lf) : (s + step >= S ? lf : anc[s + step]);
             };
+            // an object pixel on the row owns itself (g = 0: the unique minimum)
+            auto on_row = [&](int j) { return g[j] == j * j; };
             if (n >= NW) {
                 for (int t = warp; t < n; t += NW) {
                     const int s = s0 + t * ds;
-                    int lo, hi, col;
-                    bounds(s, lo, hi);
-                    anc_owner<TAKE_NEW>(g, 32 * s, lo, hi, lane, col);
+                    int lo, hi, col = 32 * s;
+                    if (!on_row(32 * s)) {
+                        bounds(s, lo, hi);
+                        anc_owner<TAKE_NEW>(g, 32 * s, lo, hi, lane, col);
+                    }
                     if (lane == 0) anc[s] = col;
                 }
             } else {
@@ -207,11 +211,18 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
                 int col = 0;
                 if (t < n) {
                     const int s = s0 + t * ds;
-                    int lo, hi;
-                    bounds(s, lo, hi);
-                    const int c = (hi - lo + q) / q;  // ceil((hi - lo + 1) / q)
-                    const int plo = lo + part * c, phi = min(hi, plo + c - 1);
-                    m = anc_owner<TAKE_NEW>(g, 32 * s, plo, phi, lane, col);
+                    if (on_row(32 * s)) {
+                        if (part == 0) {
+                            m = -(32 * s) * (32 * s);
+                            col = 32 * s;
+                        }
+                    } else {
+                        int lo, hi;
+                        bounds(s, lo, hi);
+                        const int c = (hi - lo + q) / q;  // ceil((hi - lo + 1) / q)
+                        const int plo = lo + part * c, phi = min(hi, plo + c - 1);
+                        m = anc_owner<TAKE_NEW>(g, 32 * s, plo, phi, lane, col);
+                    }
                 }
                 if (lane == 0) {
                     pv[warp] = m;
@@ -238,6 +249,17 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         // ---- segments: lane = column, brute force over [owner(j0), owner(j0 + 32)] ----
         for (int s = warp; s < S; s += NW) {
             const int j = 32 * s + lane;
+            if (__all_sync(FULL, j >= W || g[j] == j * j)) {  // every column an object pixel on the row
+                if (j < W) {
+                    if (Drow) __stcs(Drow + j, 0);
+                    if (Srow) __stcs(Srow + j, 0.0f);
+                    if (OWNERS) {
+                        if (Lrow) __stcs(Lrow + j, (int32_t)((uint32_t)__ldg(rowp + j) * (uint32_t)W + (uint32_t)j));
+                        if (Nrow) __stcs(Nrow + j, j);
+                    }
+                }
+                continue;
+            }
             const int lo = anc[s], hi = anc[s + 1];
             // D_k(j) - j^2 = h_k - 2 j k, ascending k; the j^2 goes back at the end
             const int c = -2 * j;
