@@ -124,7 +124,7 @@ RowGeom row_geom(int W) {
 int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
                 cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr,
-                uint32_t* pts = nullptr) {
+                uint32_t* pts = nullptr, uint32_t* bmask = nullptr) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -139,6 +139,8 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.vec = aligned(img, 4) && pitch % 4 == 0 && istride % 4 == 0;
     c.pts = counts ? pts : nullptr;
     c.pcounts = counts;
+    c.bmask = bmask;
+    c.skip_full = bmask != nullptr && counts != nullptr;
     const unsigned long long* skip = c.pts ? counts : nullptr;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
@@ -210,13 +212,32 @@ int row_pass_win(RowArgs a, bool take_new, cudaStream_t st) {
     return DFC_OK;
 }
 
+// dense planes by k_rows_anc too (all-object segments and anchors on object
+// pixels are free there); DFC_ANC_DENSE=0 keeps k_rows_dense (A/B)
+bool anc_dense_on() {
+    static const bool on = [] {
+        const char* v = getenv("DFC_ANC_DENSE");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// Band source of k_rows_anc (see RowArgs): masks [img][nb][Wp], carries
+// above / below [plane][nb][Wp] of this call's planes, first polarity.
+struct BandSrc {
+    const uint32_t* bmask = nullptr;
+    const uint16_t* above = nullptr;
+    const uint16_t* below = nullptr;
+    int nb = 0, n_img = 1, pol0 = 0;
+};
+
 // Stage 2 over `nimg` planes of H rows.  Plane b writes its outputs at
 // base + b*stride.  take_new selects meijster_scan's tie rule.
 int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, bool take_new,
              int32_t* D, int64_t sD, float* S, int64_t sS, int32_t* LB, int64_t sL, int32_t* NC,
              int64_t sN, cudaStream_t st, bool vdist = false, int tile_cols = 0,
              int64_t tile_stride = 0, int row0 = 0, const unsigned long long* plane_counts = nullptr,
-             const uint32_t* pts = nullptr) {
+             const uint32_t* pts = nullptr, const BandSrc& band = BandSrc()) {
     const RowGeom g = row_geom((int)W);
     RowArgs a;
     a.nr = nr;
@@ -250,6 +271,11 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.lr_gate = false;
     a.pts_gate = false;
     a.plane_counts = plane_counts;
+    a.bmask = nullptr;
+    a.babove = a.bbelow = nullptr;
+    a.nb = band.nb;
+    a.n_img = band.n_img;
+    a.bpol0 = band.pol0;
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
     if (mode == 3 && W <= 16384) return row_pass_win(a, take_new, st);
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
@@ -332,13 +358,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         // anchored segments (k_rows_anc.cu) for every row the point / sparse
         // kernels do not own: one tile, W <= kAncMaxW
         const bool anc_on = mode == 6 && W <= kAncMaxW && a.tile_cols >= W && row0 == 0 && H <= 32768;
-        // dense planes by k_rows_anc too (all-object segments and anchors on
-        // object pixels are free there); DFC_ANC_DENSE=0 keeps k_rows_dense (A/B)
-        static const bool anc_dense = [] {
-            const char* v = getenv("DFC_ANC_DENSE");
-            return !(v && v[0] == '0');
-        }();
-        const bool dense_on = W <= kDenseMaxW && !(anc_on && anc_dense);
+        const bool dense_on = W <= kDenseMaxW && !(anc_on && anc_dense_on());
         const bool lr_on = lr_ok && plane_counts != nullptr;
         Scratch fl(st);
         const size_t flag_bytes = (size_t)round_up(a.total_rows, 256);
@@ -379,12 +399,27 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         if (anc_on) {
             RowArgs aa = a;
             aa.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0;
+            if (band.bmask && anc_dense_on()) {  // stage rows from the bands (no nr plane)
+                aa.bmask = band.bmask;
+                aa.babove = band.above;
+                aa.bbelow = band.below;
+            }
             const bool owners = LB != nullptr || NC != nullptr;
             const void* afn = take_new ? (owners ? anc_kernel_ptr<true, true>() : anc_kernel_ptr<true, false>())
                                        : (owners ? anc_kernel_ptr<false, true>() : anc_kernel_ptr<false, false>());
             const int asm_bytes = anc_smem_bytes((int)W);
             e = cudaFuncSetAttribute(afn, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes);
             if (e != cudaSuccess) return cuda_fail(e);
+            if (a.total_rows > 16384 && (a.pts_gate || a.lr_gate)) {
+                // many rows, some owned by other kernels (C3: every plane a point
+                // plane): a compact list first, so that skipped rows cost nothing
+                const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
+                k_rows_rest<<<(unsigned)rblocks, 256, 0, st>>>(a.row_done, plane_counts, a.total_rows, (int)H,
+                                                               (int)W, a.lr_gate, a.pts_gate, rest_rows, rest_count);
+                ++g_launches;
+                aa.row_list = rest_rows;
+                aa.row_count = rest_count;
+            }
             const int64_t ablocks = std::min<int64_t>(a.total_rows, 148 * 16);
             void* aargs[] = {&aa};
             e = cudaLaunchKernel(afn, dim3((unsigned)ablocks), dim3(32 * kAncWarps), aargs, (size_t)asm_bytes, st);
@@ -486,17 +521,28 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     // point planes (k_rows_pts) in the default row pass when planes are whole warps of rows
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
     const bool pts_on = (mode == 4 || mode == 6) && H % 32 == 0;
+    // band source: k_rows_anc stages the rows of the planes it owns from the
+    // column pass's band masks and carries; K1c writes no nearest-row plane there
+    // (single images: K1a writes the masks before the point-plane test is known,
+    // which would cost batches of point planes, C3, a mask write per pixel / 8)
+    const bool band_on = mode == 6 && anc_dense_on() && W <= kAncMaxW && H <= 32768 && n == 1;
+    const size_t bmask_elems = band_on ? (size_t)(n * nb * Wp) : 0;
     Scratch sc(st);
     cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 512 + (size_t)planes * 8 +
-                             (pts_on ? (size_t)planes * kPtsCap * 4 : 0));
+                             (pts_on ? (size_t)planes * kPtsCap * 4 : 0) + bmask_elems * 4 + 16);
     if (e != cudaSuccess) return cuda_fail(e);
     uint16_t* first = static_cast<uint16_t*>(sc.p);
     uint16_t* last = first + carry_elems;
     uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry_elems), 16));
     auto* counts = reinterpret_cast<unsigned long long*>(round_up(reinterpret_cast<uintptr_t>(nr + nr_elems), 16));
     uint32_t* pts = pts_on ? reinterpret_cast<uint32_t*>(counts + planes) : nullptr;
+    uint32_t* bmask = band_on ? reinterpret_cast<uint32_t*>(round_up(
+                                    reinterpret_cast<uintptr_t>(reinterpret_cast<char*>(counts + planes) +
+                                                                (pts_on ? (size_t)planes * kPtsCap * 4 : 0)), 16))
+                              : nullptr;
     prof(0, st);
-    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts, pts);
+    int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts, pts,
+                         bmask);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -515,26 +561,40 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     const bool want_keep = o.D[0] || o.S[0] || o.LB[0];
     if (uniform) {
         const int64_t nimg = planes;
+        BandSrc bs;
+        bs.bmask = bmask;
+        bs.above = last;
+        bs.below = first;
+        bs.nb = (int)nb;
+        bs.n_img = (int)n;
+        bs.pol0 = pol0;
         if (want_keep) {
             rc = row_pass(nr, nimg, H, W, Wp, false, o.D[0], stride_of(o.D[0], o.D[1]), o.S[0],
                           o.S[0] ? stride_of(o.S[0], o.S[1]) : 0, o.LB[0],
-                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st, false, 0, 0, 0, counts, pts);
+                          o.LB[0] ? stride_of(o.LB[0], o.LB[1]) : 0, nullptr, 0, st, false, 0, 0, 0, counts, pts, bs);
             if (rc != DFC_OK) return rc;
         }
         if (o.NC[0]) {
             rc = row_pass(nr, nimg, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[0],
-                          stride_of(o.NC[0], o.NC[1]), st, false, 0, 0, 0, counts, pts);
+                          stride_of(o.NC[0], o.NC[1]), st, false, 0, 0, 0, counts, pts, bs);
             if (rc != DFC_OK) return rc;
         }
     } else {
         for (int s = 0; s < npol; ++s) {
             const uint16_t* pl = nr + (int64_t)s * H * Wp;
+            BandSrc bs;  // n == 1 here
+            bs.bmask = bmask;
+            bs.above = last + (int64_t)s * nb * Wp;
+            bs.below = first + (int64_t)s * nb * Wp;
+            bs.nb = (int)nb;
+            bs.n_img = 1;
+            bs.pol0 = pol0 + s;
             rc = row_pass(pl, 1, H, W, Wp, false, o.D[s], 0, o.S[s], 0, o.LB[s], 0, nullptr, 0, st, false, 0, 0, 0,
-                          counts + s, pts ? pts + (int64_t)s * kPtsCap : nullptr);
+                          counts + s, pts ? pts + (int64_t)s * kPtsCap : nullptr, bs);
             if (rc != DFC_OK) return rc;
             if (o.NC[s]) {
                 rc = row_pass(pl, 1, H, W, Wp, true, nullptr, 0, nullptr, 0, nullptr, 0, o.NC[s], 0, st, false, 0, 0,
-                              0, counts + s, pts ? pts + (int64_t)s * kPtsCap : nullptr);
+                              0, counts + s, pts ? pts + (int64_t)s * kPtsCap : nullptr, bs);
                 if (rc != DFC_OK) return rc;
             }
         }

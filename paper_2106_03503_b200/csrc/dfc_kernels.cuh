@@ -18,6 +18,12 @@ struct ColArgs {
     // object pixels, K1b/K1c skip them (k_rows_pts works from the list)
     uint32_t* pts;                           // [plane][kPtsCap] keys col << 16 | row, nullable
     const unsigned long long* pcounts;       // object pixels per plane (K1a), for the skip
+    // band masks (bit r = row 32 b + r of the column is nonzero) [img][nb][Wp],
+    // written by K1a when non-null; with skip_full, K1c writes no nearest-row
+    // plane for planes the row pass reads from the bands (neither point nor
+    // sparse planes: k_rows_anc stages those rows from masks + carries)
+    uint32_t* bmask;
+    bool skip_full;
 };
 
 // Stage 2 (k_rows.cu)
@@ -46,6 +52,13 @@ struct RowArgs {
     bool lr_gate;             // rows of sparse planes belong to k_rows_lr (unless row_done == 2)
     bool pts_gate;            // rows of point planes belong to k_rows_pts
     const unsigned long long* plane_counts;  // object pixels per plane (dense gate), nullable
+    // band source (k_rows_anc, nullable bmask = read nr): the column pass's band
+    // masks [img][nb][Wp] and carries (nearest object row above / below each
+    // band) [plane][nb][Wp]; plane p of this call is polarity bpol0 + p / n_img
+    const uint32_t* bmask;
+    const uint16_t* babove;
+    const uint16_t* bbelow;
+    int nb, n_img, bpol0;
 };
 
 // Raster transforms (k_raster.cu)
@@ -71,6 +84,12 @@ __host__ __device__ __forceinline__ bool pts_plane(const unsigned long long* cou
 // lane-per-row kernel (k_rows_lr.cu) in the default mode.
 __host__ __device__ __forceinline__ bool lr_plane(const unsigned long long* counts, int img, int H, int W) {
     return counts != nullptr && counts[img] * 256ull < (unsigned long long)H * (unsigned long long)W;
+}
+
+// Object mask of polarity `pol` (0: object = nonzero, 1: object = zero) from
+// the nonzero mask m of a band with `valid` rows.
+__host__ __device__ __forceinline__ uint32_t pol_mask(uint32_t m, int pol, uint32_t valid) {
+    return pol ? (~m & valid) : m;
 }
 
 // The kernels themselves are defined in k_columns.cu / k_rows.cu / k_raster.cu and

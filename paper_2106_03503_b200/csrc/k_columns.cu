@@ -52,10 +52,6 @@ __device__ __forceinline__ void band_masks(const uint8_t* __restrict__ base, int
     }
 }
 
-// Mask of the polarity `slot_pol` (0: object = nonzero, 1: object = zero).
-__device__ __forceinline__ uint32_t pol_mask(uint32_t m, int pol, uint32_t valid) {
-    return pol ? (~m & valid) : m;
-}
 
 
 // K1a: grid (ceil(W/4)/blockDim, nb, n_img)
@@ -72,6 +68,8 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
     uint32_t m[4] = {0u, 0u, 0u, 0u};
     if (live) band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    if (a.bmask && live)
+        *reinterpret_cast<uint4*>(a.bmask + ((int64_t)im * a.nb + b) * a.Wp + j0) = make_uint4(m[0], m[1], m[2], m[3]);
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
         uint16_t f[4], l[4];
@@ -218,9 +216,16 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
     const int j0 = 4 * g;
     if (j0 >= a.W) return;
     const int b = blockIdx.y, im = blockIdx.z;
-    if (a.pts) {  // every slot a point plane: nothing to write (CTA-uniform)
+    // planes without a nearest-row plane: point planes (k_rows_pts) and, with
+    // skip_full, planes k_rows_anc stages from the bands (CTA-uniform)
+    auto skip_plane = [&](int s) {
+        const int64_t p = (int64_t)s * a.n_img + im;
+        if (a.pts && a.pcounts[p] <= (unsigned long long)kPtsCap) return true;
+        return a.skip_full && a.pcounts && !lr_plane(a.pcounts, (int)p, a.H, a.W);
+    };
+    if (a.pts || a.skip_full) {
         bool all = true;
-        for (int s = 0; s < a.npol; ++s) all = all && a.pcounts[(int64_t)s * a.n_img + im] <= (unsigned long long)kPtsCap;
+        for (int s = 0; s < a.npol; ++s) all = all && skip_plane(s);
         if (all) return;
     }
     const int r0 = b * kBand;
@@ -230,7 +235,7 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
     band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
-        if (a.pts && a.pcounts[(int64_t)s * a.n_img + im] <= (unsigned long long)kPtsCap) continue;  // point plane
+        if ((a.pts || a.skip_full) && skip_plane(s)) continue;
         const int64_t coff = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
         const uint2 ab = *reinterpret_cast<const uint2*>(above + coff);
         const uint2 bl = *reinterpret_cast<const uint2*>(below + coff);

@@ -100,31 +100,60 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
     int* anc = reinterpret_cast<int*>(g + anc_gwords(W));  // [S + 1]
     int32_t* pv = reinterpret_cast<int32_t*>(anc + S + 1);  // [NW] partial minima
     int* pk = reinterpret_cast<int*>(pv + NW);                // [NW] their columns
-    int* rf = pk + NW;                                        // [NW] first finite column per warp
-    int* rl = rf + NW;                                        // [NW] last finite column per warp
     int P = 1;                                                // power of two >= S
     while (P < S) P <<= 1;
 
-    for (int64_t row = blockIdx.x; row < a.total_rows; row += gridDim.x) {
+    // all rows (skipping the ones other kernels own), or a compact list of them
+    const int64_t nrows = a.row_list ? (int64_t)*a.row_count : a.total_rows;
+    for (int64_t q = blockIdx.x; q < nrows; q += gridDim.x) {
+        const int64_t row = a.row_list ? (int64_t)a.row_list[q] : q;
         const int img = (int)(row / a.H);
-        if (!anc_row_mine(a, row, img)) continue;  // CTA-uniform
+        if (!a.row_list && !anc_row_mine(a, row, img)) continue;  // CTA-uniform
         const uint32_t i = (uint32_t)(row - (int64_t)img * a.H);
         const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
         const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
 
-        // ---- stage g and the first / last finite column ----
-        int ff = W, lf = -1;
+        // ---- stage h = g + k^2 (and whether any column is finite) ----
+        bool any = false;
         auto gval = [&](int j, uint32_t r) -> int32_t {
-            int32_t gv = kAncInf;
-            if (r != kNoRow) {
-                ff = min(ff, j);
-                lf = max(lf, j);
-                const uint32_t av = gi > r ? gi - r : r - gi;
-                gv = (int32_t)(av * av);
-            }
-            return gv + j * j;
+            const uint32_t av = gi > r ? gi - r : r - gi;
+            any |= r != kNoRow;
+            return (r != kNoRow ? (int32_t)(av * av) : kAncInf) + j * j;
         };
-        if (a.vec_nr) {
+        // band source: nearest object row of column k from the band's mask and
+        // carries (as K1c, k_columns.cu), without a nearest-row plane
+        const int bb = (int)(i >> 5), br = (int)(i & 31);
+        const int slot = a.bmask ? img / a.n_img : 0;
+        const int bpol = a.bpol0 + slot;
+        const uint32_t bvalid = a.bmask && a.H - 32 * bb < 32 ? (1u << (a.H - 32 * bb)) - 1u : 0xffffffffu;
+        const uint32_t* mrow = a.bmask ? a.bmask + ((int64_t)(img - slot * a.n_img) * a.nb + bb) * a.Wp : nullptr;
+        const uint16_t* arow = a.bmask ? a.babove + ((int64_t)img * a.nb + bb) * a.Wp : nullptr;
+        const uint16_t* brow = a.bmask ? a.bbelow + ((int64_t)img * a.nb + bb) * a.Wp : nullptr;
+        auto band_nr = [&](uint32_t m, uint32_t ca, uint32_t cb) -> uint32_t {
+            const uint32_t mk = pol_mask(m, bpol, bvalid);
+            const uint32_t up = mk & (0xffffffffu >> (31 - br));  // rows 32 bb .. i
+            const uint32_t dn = mk >> br;                          // rows i ..
+            const uint32_t ra = up ? (uint32_t)(32 * bb + 31 - __clz(up)) : ca;
+            const uint32_t rb = dn ? (uint32_t)(i + __ffs(dn) - 1) : cb;
+            return pick_nearest(i, ra, rb);
+        };
+        if (a.bmask) {
+            for (int q = tid; 4 * q < W; q += 32 * NW) {
+                const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(mrow) + q);
+                const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(arow) + q);
+                const uint2 b2 = __ldg(reinterpret_cast<const uint2*>(brow) + q);
+                const uint32_t mm[4] = {m4.x, m4.y, m4.z, m4.w};
+                const uint32_t ca[4] = {a2.x & 0xffffu, a2.x >> 16, a2.y & 0xffffu, a2.y >> 16};
+                const uint32_t cb[4] = {b2.x & 0xffffu, b2.x >> 16, b2.y & 0xffffu, b2.y >> 16};
+                int32_t o[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int j = 4 * q + t;
+                    o[t] = j < W ? gval(j, band_nr(mm[t], ca[t], cb[t])) : kAncInf + j * j;
+                }
+                reinterpret_cast<int4*>(g)[q] = make_int4(o[0], o[1], o[2], o[3]);
+            }
+        } else if (a.vec_nr) {
             const uint4* src = reinterpret_cast<const uint4*>(rowp);
             const int nvec = (W + 7) >> 3;
             for (int v = tid; v < nvec; v += 32 * NW) {
@@ -147,25 +176,17 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         } else {
             for (int j = tid; j < anc_gwords(W); j += 32 * NW) g[j] = j < W ? gval(j, __ldg(rowp + j)) : kAncInf + j * j;
         }
-        ff = __reduce_min_sync(FULL, ff);
-        lf = __reduce_max_sync(FULL, lf);
-        if (lane == 0) {
-            rf[warp] = ff;
-            rl[warp] = lf;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            ff = min(ff, rf[w]);
-            lf = max(lf, rl[w]);
-        }
+        // the owner search bounds are the row ends: a range containing columns
+        // without objects still holds its finite owner, which beats them
+        const int ff = 0, lf = W - 1;
+        any = __syncthreads_or(any);
 
         int32_t* Drow = a.D ? reinterpret_cast<int32_t*>(a.D + img * a.sD) + (int64_t)i * W : nullptr;
         float* Srow = a.S ? reinterpret_cast<float*>(a.S + img * a.sS) + (int64_t)i * W : nullptr;
         int32_t* Lrow = a.LB ? reinterpret_cast<int32_t*>(a.LB + img * a.sL) + (int64_t)i * W : nullptr;
         int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + img * a.sN) + (int64_t)i * W : nullptr;
 
-        if (lf < 0) {  // featureless row (CTA-uniform)
+        if (!any) {  // featureless row (CTA-uniform)
             for (int j = tid; j < W; j += 32 * NW) {
                 if (Drow) __stcs(Drow + j, DFC_INF_I32);
                 if (Srow) __stcs(Srow + j, __int_as_float(0x7f800000));
@@ -177,8 +198,8 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         }
 
         // ---- anchors owner(32 s), s < S: levels of a divide and conquer over
-        // [0, P] (index >= S stands for owner(W) := lf; index 0 comes last with
-        // lower bound ff).  A level with n >= NW anchors gives each warp whole
+        // [0, P] (index >= S stands for owner(W) := W - 1; index 0 comes last
+        // with lower bound 0).  A level with n >= NW anchors gives each warp whole
         // anchors; with fewer, each anchor's range is split over NW / n warps
         // (ascending parts) and the parts are combined with the tie rule. ----
         if (tid == 0) anc[S] = lf;
@@ -246,6 +267,12 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         }
         __syncthreads();
 
+        // nearest object row of column k (labels): the plane, or the bands
+        auto nr_of = [&](int k) -> uint32_t {
+            if (!a.bmask) return (uint32_t)__ldg(rowp + k);
+            return band_nr(__ldg(mrow + k), __ldg(arow + k), __ldg(brow + k));
+        };
+
         // ---- segments: lane = column, brute force over [owner(j0), owner(j0 + 32)] ----
         for (int s = warp; s < S; s += NW) {
             const int j = 32 * s + lane;
@@ -254,7 +281,7 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
                     if (Drow) __stcs(Drow + j, 0);
                     if (Srow) __stcs(Srow + j, 0.0f);
                     if (OWNERS) {
-                        if (Lrow) __stcs(Lrow + j, (int32_t)((uint32_t)__ldg(rowp + j) * (uint32_t)W + (uint32_t)j));
+                        if (Lrow) __stcs(Lrow + j, (int32_t)(nr_of(j) * (uint32_t)W + (uint32_t)j));
                         if (Nrow) __stcs(Nrow + j, j);
                     }
                 }
@@ -306,7 +333,7 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
                 if (Drow) __stcs(Drow + j, (int32_t)dval);
                 if (Srow) __stcs(Srow + j, dist_f32(dval));
                 if (OWNERS) {
-                    if (Lrow) __stcs(Lrow + j, (int32_t)((uint32_t)__ldg(rowp + bk) * (uint32_t)W + (uint32_t)bk));
+                    if (Lrow) __stcs(Lrow + j, (int32_t)(nr_of(bk) * (uint32_t)W + (uint32_t)bk));
                     if (Nrow) __stcs(Nrow + j, bk);
                 }
             }
