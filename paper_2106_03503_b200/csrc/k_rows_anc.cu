@@ -33,14 +33,17 @@ constexpr int kAncWarps = 4;               // warps per CTA (one row per CTA)
 constexpr int kAncMaxW = 16384;
 // Shared memory holds h_k = g_k + k^2 (int32), so that D_k(j) - j^2 = h_k - 2 j k
 // is one multiply-add (or, with 2 j k carried along, one 3-way add).  A column
-// without objects gets g = kAncInf: above every real D (rows <= 32768, columns
-// <= kAncMaxW: D <= 32767^2 + 16383^2 < 1.35e9), and h, h - 2jk stay inside int32.
-constexpr int32_t kAncInf = 0x60000000;
+// without objects gets g = kAncInf = kAncBig^2: above every real D (rows <= 32768,
+// columns <= kAncMaxW: D <= 32767^2 + 16383^2 < 1.35e9 < 1.6e9), and h,
+// h - 2jk stay inside int32.
+constexpr uint32_t kAncBig = 40000;  // vertical distance of a column without objects
+constexpr int32_t kAncInf = (int32_t)(kAncBig * kAncBig);
 
 __host__ __device__ __forceinline__ int anc_segs(int W) { return (W + 31) >> 5; }
-// words: g (W, 16-byte granules), anchors (S + 1), per-warp partial owners (2 NW), bounds (2 NW)
+// words: g (W, 16-byte granules), anchors (S + 1), per-warp partial owners (2 NW),
+// object-pixel bits of the row (S)
 __host__ __device__ __forceinline__ int anc_gwords(int W) { return (W + 3) & ~3; }
-inline int anc_smem_bytes(int W) { return (anc_gwords(W) + anc_segs(W) + 1 + 4 * kAncWarps) * 4; }
+inline int anc_smem_bytes(int W) { return (anc_gwords(W) + 2 * anc_segs(W) + 1 + 2 * kAncWarps) * 4; }
 
 // The rows this kernel owns in the default row pass: not a point plane; in a
 // sparse plane (k_rows_lr) only the rows that kernel flagged (2); elsewhere the
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
     int* anc = reinterpret_cast<int*>(g + anc_gwords(W));  // [S + 1]
     int32_t* pv = reinterpret_cast<int32_t*>(anc + S + 1);  // [NW] partial minima
     int* pk = reinterpret_cast<int*>(pv + NW);                // [NW] their columns
+    uint32_t* zb = reinterpret_cast<uint32_t*>(pk + NW);      // [S] bit = object pixel on the row
     int P = 1;                                                // power of two >= S
     while (P < S) P <<= 1;
 
@@ -113,68 +117,80 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
         const uint16_t* rowp = a.nr + img * a.nr_img_stride + (int64_t)i * a.Wp;
 
-        // ---- stage h = g + k^2 (and whether any column is finite) ----
-        bool any = false;
-        auto gval = [&](int j, uint32_t r) -> int32_t {
-            const uint32_t av = gi > r ? gi - r : r - gi;
-            any |= r != kNoRow;
-            return (r != kNoRow ? (int32_t)(av * av) : kAncInf) + j * j;
-        };
-        // band source: nearest object row of column k from the band's mask and
-        // carries (as K1c, k_columns.cu), without a nearest-row plane
+        // ---- stage h = g + k^2, the row's object-pixel bits, and whether any
+        // column is finite.  Thread = 4 consecutive columns; a column's vertical
+        // distance d (kAncBig: no object in the column) comes from the nearest-row
+        // plane or from the band's mask and carries (as K1c, k_columns.cu). ----
         const int bb = (int)(i >> 5), br = (int)(i & 31);
         const int slot = a.bmask ? img / a.n_img : 0;
         const int bpol = a.bpol0 + slot;
         const uint32_t bvalid = a.bmask && a.H - 32 * bb < 32 ? (1u << (a.H - 32 * bb)) - 1u : 0xffffffffu;
+        const uint32_t upmask = 0xffffffffu >> (31 - br);
         const uint32_t* mrow = a.bmask ? a.bmask + ((int64_t)(img - slot * a.n_img) * a.nb + bb) * a.Wp : nullptr;
         const uint16_t* arow = a.bmask ? a.babove + ((int64_t)img * a.nb + bb) * a.Wp : nullptr;
         const uint16_t* brow = a.bmask ? a.bbelow + ((int64_t)img * a.nb + bb) * a.Wp : nullptr;
+        // nearest object row (the upper one on a tie, exact_edt.cpp:351), for labels
         auto band_nr = [&](uint32_t m, uint32_t ca, uint32_t cb) -> uint32_t {
             const uint32_t mk = pol_mask(m, bpol, bvalid);
-            const uint32_t up = mk & (0xffffffffu >> (31 - br));  // rows 32 bb .. i
-            const uint32_t dn = mk >> br;                          // rows i ..
+            const uint32_t up = mk & upmask, dn = mk >> br;
             const uint32_t ra = up ? (uint32_t)(32 * bb + 31 - __clz(up)) : ca;
             const uint32_t rb = dn ? (uint32_t)(i + __ffs(dn) - 1) : cb;
             return pick_nearest(i, ra, rb);
         };
-        if (a.bmask) {
-            for (int q = tid; 4 * q < W; q += 32 * NW) {
-                const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(mrow) + q);
-                const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(arow) + q);
-                const uint2 b2 = __ldg(reinterpret_cast<const uint2*>(brow) + q);
-                const uint32_t mm[4] = {m4.x, m4.y, m4.z, m4.w};
-                const uint32_t ca[4] = {a2.x & 0xffffu, a2.x >> 16, a2.y & 0xffffu, a2.y >> 16};
-                const uint32_t cb[4] = {b2.x & 0xffffu, b2.x >> 16, b2.y & 0xffffu, b2.y >> 16};
-                int32_t o[4];
+        bool any = false;
+        for (int q0 = warp * 32; 4 * q0 < W; q0 += 32 * NW) {  // warp-uniform trip count
+            const int q = q0 + lane;
+            const bool live = 4 * q < W;
+            uint32_t d[4] = {kAncBig, kAncBig, kAncBig, kAncBig};
+            if (live) {
+                if (a.bmask) {
+                    const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(mrow) + q);
+                    const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(arow) + q);
+                    const uint2 b2 = __ldg(reinterpret_cast<const uint2*>(brow) + q);
+                    const uint32_t mm[4] = {m4.x, m4.y, m4.z, m4.w};
+                    const uint32_t ca[4] = {a2.x & 0xffffu, a2.x >> 16, a2.y & 0xffffu, a2.y >> 16};
+                    const uint32_t cb[4] = {b2.x & 0xffffu, b2.x >> 16, b2.y & 0xffffu, b2.y >> 16};
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int j = 4 * q + t;
-                    o[t] = j < W ? gval(j, band_nr(mm[t], ca[t], cb[t])) : kAncInf + j * j;
-                }
-                reinterpret_cast<int4*>(g)[q] = make_int4(o[0], o[1], o[2], o[3]);
-            }
-        } else if (a.vec_nr) {
-            const uint4* src = reinterpret_cast<const uint4*>(rowp);
-            const int nvec = (W + 7) >> 3;
-            for (int v = tid; v < nvec; v += 32 * NW) {
-                const uint4 q = __ldg(src + v);
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-                int32_t o[8];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int j = 8 * v + 2 * t;
-                    o[2 * t] = j < W ? gval(j, w[t] & 0xffffu) : kAncInf + j * j;
-                    o[2 * t + 1] = j + 1 < W ? gval(j + 1, w[t] >> 16) : kAncInf + (j + 1) * (j + 1);
-                }
-                if (8 * v + 7 < W || (W & 3) == 0) {
-                    reinterpret_cast<int4*>(g)[2 * v] = make_int4(o[0], o[1], o[2], o[3]);
-                    if (8 * v + 4 < W) reinterpret_cast<int4*>(g)[2 * v + 1] = make_int4(o[4], o[5], o[6], o[7]);
+                    for (int t = 0; t < 4; ++t) {
+                        const uint32_t mk = pol_mask(mm[t], bpol, bvalid);
+                        const uint32_t up = mk & upmask, dn = mk >> br;
+                        const uint32_t du = up ? (uint32_t)(br - 31) + __clz(up) : (ca[t] == kNoRow ? kAncBig : i - ca[t]);
+                        const uint32_t dd = dn ? (uint32_t)__ffs(dn) - 1u : (cb[t] == kNoRow ? kAncBig : cb[t] - i);
+                        d[t] = min(min(du, dd), kAncBig);
+                    }
                 } else {
-                    for (int t = 0; t < 8 && 8 * v + t < anc_gwords(W); ++t) g[8 * v + t] = o[t];
+                    uint32_t r[4];
+                    if (a.vec_nr) {
+                        const uint2 v = __ldg(reinterpret_cast<const uint2*>(rowp) + q);
+                        r[0] = v.x & 0xffffu; r[1] = v.x >> 16; r[2] = v.y & 0xffffu; r[3] = v.y >> 16;
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) r[t] = 4 * q + t < W ? (uint32_t)__ldg(rowp + 4 * q + t) : kNoRow;
+                    }
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        d[t] = r[t] == kNoRow ? kAncBig : (gi > r[t] ? gi - r[t] : r[t] - gi);
                 }
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (4 * q + t >= W) d[t] = kAncBig;  // padding past the row
             }
-        } else {
-            for (int j = tid; j < anc_gwords(W); j += 32 * NW) g[j] = j < W ? gval(j, __ldg(rowp + j)) : kAncInf + j * j;
+            int32_t o[4];
+            uint32_t z = 0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int j = 4 * q + t;
+                o[t] = (int32_t)(d[t] * d[t]) + j * j;
+                any |= d[t] < kAncBig;
+                z |= (uint32_t)(d[t] == 0 || j >= W) << t;
+            }
+            if (live) reinterpret_cast<int4*>(g)[q] = make_int4(o[0], o[1], o[2], o[3]);
+            // object-pixel bits: 8 lanes x 4 columns = one 32-column word
+            z <<= 4 * (lane & 7);
+            z |= __shfl_xor_sync(FULL, z, 1);
+            z |= __shfl_xor_sync(FULL, z, 2);
+            z |= __shfl_xor_sync(FULL, z, 4);
+            if ((lane & 7) == 0 && (q >> 3) < S) zb[q >> 3] = z;
         }
         // the owner search bounds are the row ends: a range containing columns
         // without objects still holds its finite owner, which beats them
@@ -214,7 +230,7 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
                 hi = last ? (S > 1 ? anc[1] : lf) : (s + step >= S ? lf : anc[s + step]);
             };
             // an object pixel on the row owns itself (g = 0: the unique minimum)
-            auto on_row = [&](int j) { return g[j] == j * j; };
+            auto on_row = [&](int j) { return (zb[j >> 5] >> (j & 31)) & 1u; };
             if (n >= NW) {
                 for (int t = warp; t < n; t += NW) {
                     const int s = s0 + t * ds;
@@ -276,7 +292,7 @@ __global__ void __launch_bounds__(32 * kAncWarps) k_rows_anc(RowArgs a) {
         // ---- segments: lane = column, brute force over [owner(j0), owner(j0 + 32)] ----
         for (int s = warp; s < S; s += NW) {
             const int j = 32 * s + lane;
-            if (__all_sync(FULL, j >= W || g[j] == j * j)) {  // every column an object pixel on the row
+            if (zb[s] == 0xffffffffu) {  // every column an object pixel on the row (warp-uniform)
                 if (j < W) {
                     if (Drow) __stcs(Drow + j, 0);
                     if (Srow) __stcs(Srow + j, 0.0f);
