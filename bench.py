@@ -43,9 +43,10 @@ HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 CONFIGS = {
     "c1": dict(desc="c1: 600x500 uint8 Bernoulli p=0.01 (reference generator), exact squared EDT "
-                    "int32 + float32 distances", bytes_alg=9, bytes_kernel=4 + 8),
+                    "int32 + float32 distances", bytes_alg=9, bytes_kernel=8 + 0.25),  # k_rows_anc: outputs + band masks/carries
     "c2": dict(desc="c2: 4096x4096 uint8, 200 seeded discs (r 8..64), exact squared EDT both "
-                    "polarities int32 + float32 distances", bytes_alg=17, bytes_kernel=4 + 16),
+                    "polarities int32 + float32 distances", bytes_alg=17,
+               bytes_kernel=16 + 0.375),  # k_rows_anc: 2 x 8 B outputs + band masks (shared) and carries / 32 rows
     "c3": dict(desc="c3: 1024 images 1024x1024 uint8, 30 seeded points each, exact squared EDT "
                     "int32 + int32 Voronoi labels", bytes_alg=9, bytes_kernel=8),  # point planes: no nr plane
     "c4": dict(desc="c4: 8192x8192 uint8, 2000 seeded discs/rectangles, city-block + chessboard + "
