@@ -124,7 +124,7 @@ RowGeom row_geom(int W) {
 int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
                 cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr,
-                uint32_t* pts = nullptr, uint32_t* bmask = nullptr) {
+                uint32_t* pts = nullptr, uint32_t* bmask = nullptr, bool skip_full = false) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -140,7 +140,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.pts = counts ? pts : nullptr;
     c.pcounts = counts;
     c.bmask = bmask;
-    c.skip_full = bmask != nullptr && counts != nullptr;
+    c.skip_full = skip_full && bmask != nullptr && counts != nullptr;
     const unsigned long long* skip = c.pts ? counts : nullptr;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
@@ -154,7 +154,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
         k_band_scan_serial<<<gs, 256, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last, skip);
     } else {           // tall columns: chunks of bands scanned in parallel
         const int nc = std::min(32, c.nb / 4);
-        dim3 gs((unsigned)((W + 31) / 32), (unsigned)(npol * n));
+        dim3 gs((unsigned)((W + 127) / 128), (unsigned)(npol * n));
         k_band_scan<<<gs, 32 * nc, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last, skip);
     }
     if (vsq)
@@ -526,7 +526,10 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     // (single images: K1a writes the masks before the point-plane test is known,
     // which would cost batches of point planes, C3, a mask write per pixel / 8)
     const bool band_on = mode == 6 && anc_dense_on() && W <= kAncMaxW && H <= 32768 && n == 1;
-    const size_t bmask_elems = band_on ? (size_t)(n * nb * Wp) : 0;
+    // band masks for every single image: K1c then builds the nearest-row plane
+    // from them instead of re-reading the image (C5: 1 B/px of reads less)
+    const bool masks_on = n == 1;
+    const size_t bmask_elems = masks_on ? (size_t)(n * nb * Wp) : 0;
     Scratch sc(st);
     cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 512 + (size_t)planes * 8 +
                              (pts_on ? (size_t)planes * kPtsCap * 4 : 0) + bmask_elems * 4 + 16);
@@ -536,13 +539,13 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry_elems), 16));
     auto* counts = reinterpret_cast<unsigned long long*>(round_up(reinterpret_cast<uintptr_t>(nr + nr_elems), 16));
     uint32_t* pts = pts_on ? reinterpret_cast<uint32_t*>(counts + planes) : nullptr;
-    uint32_t* bmask = band_on ? reinterpret_cast<uint32_t*>(round_up(
+    uint32_t* bmask = masks_on ? reinterpret_cast<uint32_t*>(round_up(
                                     reinterpret_cast<uintptr_t>(reinterpret_cast<char*>(counts + planes) +
                                                                 (pts_on ? (size_t)planes * kPtsCap * 4 : 0)), 16))
                               : nullptr;
     prof(0, st);
     int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts, pts,
-                         bmask);
+                         bmask, band_on);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -562,7 +565,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     if (uniform) {
         const int64_t nimg = planes;
         BandSrc bs;
-        bs.bmask = bmask;
+        bs.bmask = band_on ? bmask : nullptr;
         bs.above = last;
         bs.below = first;
         bs.nb = (int)nb;
@@ -583,7 +586,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
         for (int s = 0; s < npol; ++s) {
             const uint16_t* pl = nr + (int64_t)s * H * Wp;
             BandSrc bs;  // n == 1 here
-            bs.bmask = bmask;
+            bs.bmask = band_on ? bmask : nullptr;
             bs.above = last + (int64_t)s * nb * Wp;
             bs.below = first + (int64_t)s * nb * Wp;
             bs.nb = (int)nb;

@@ -19,9 +19,10 @@ struct ColArgs {
     uint32_t* pts;                           // [plane][kPtsCap] keys col << 16 | row, nullable
     const unsigned long long* pcounts;       // object pixels per plane (K1a), for the skip
     // band masks (bit r = row 32 b + r of the column is nonzero) [img][nb][Wp],
-    // written by K1a when non-null; with skip_full, K1c writes no nearest-row
-    // plane for planes the row pass reads from the bands (neither point nor
-    // sparse planes: k_rows_anc stages those rows from masks + carries)
+    // written by K1a when non-null and read by K1c instead of the image; with
+    // skip_full, K1c writes no nearest-row plane for planes the row pass reads
+    // from the bands (neither point nor sparse planes: k_rows_anc stages those
+    // rows from masks + carries)
     uint32_t* bmask;
     bool skip_full;
 };

@@ -162,47 +162,77 @@ __global__ void k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint
 // K1b: per column, in place: last[b] becomes the nearest object row ABOVE band
 // b (exclusive prefix-max over bands: rows grow with the band index, kNoRow =
 // absent), first[b] the nearest object row BELOW it (exclusive suffix-min).
-// CTA = 32 columns x nc band chunks (nc <= 32); a thread scans its chunk
-// twice (aggregate, then carry-in + write) -- coalesced across the columns,
-// and parallel over the chunks instead of a serial walk over all bands.
+// CTA = 128 columns (4 per thread, 8-byte accesses) x nc band chunks (nc <=
+// 32); a thread scans its chunk twice (aggregate, then carry-in + write) --
+// coalesced across the columns, and parallel over the chunks instead of a
+// serial walk over all bands.
 __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64_t n_planes,
                                                     uint16_t* __restrict__ first, uint16_t* __restrict__ last,
                                                     const unsigned long long* skip_counts) {
     if (skip_counts && blockIdx.y < n_planes && skip_counts[blockIdx.y] <= (unsigned long long)kPtsCap)
         return;  // point plane (CTA-uniform)
-    __shared__ int agg_last[32][33];
-    __shared__ int agg_first[32][33];
+    __shared__ int agg_last[32][129];
+    __shared__ int agg_first[32][129];
     const int cx = threadIdx.x & 31, ch = threadIdx.x >> 5, nc = blockDim.x >> 5;
-    const int j = blockIdx.x * 32 + cx;
+    const int j0 = blockIdx.x * 128 + 4 * cx;  // Wp % 8 == 0: the 4 columns are in the row
     const int64_t plane = blockIdx.y;
     const int per = (nb + nc - 1) / nc;
     const int b0 = ch * per, b1 = min(b0 + per, nb);
-    uint16_t* F = first + plane * nb * (int64_t)Wp + j;
-    uint16_t* Lp = last + plane * nb * (int64_t)Wp + j;
-    const bool ok = j < W && plane < n_planes;
-    int mx = -1, mn = 0x10000;
+    uint2* F = reinterpret_cast<uint2*>(first + plane * nb * (int64_t)Wp + j0);
+    uint2* Lp = reinterpret_cast<uint2*>(last + plane * nb * (int64_t)Wp + j0);
+    const int64_t step = Wp / 4;  // uint2 per row of bands
+    const bool ok = j0 < W && plane < n_planes;
+    auto split = [](uint2 v, int (&o)[4]) {
+        o[0] = (int)(v.x & 0xffffu); o[1] = (int)(v.x >> 16); o[2] = (int)(v.y & 0xffffu); o[3] = (int)(v.y >> 16);
+    };
+    int mx[4] = {-1, -1, -1, -1}, mn[4] = {0x10000, 0x10000, 0x10000, 0x10000};
     if (ok)
         for (int b = b0; b < b1; ++b) {
-            const int l = Lp[(int64_t)b * Wp], f = F[(int64_t)b * Wp];
-            if (l != kNoRow) mx = l;                 // rows increase with b: latest = max
-            if (f != kNoRow && mn == 0x10000) mn = f;  // earliest in the chunk = min
+            int l[4], f[4];
+            split(Lp[(int64_t)b * step], l);
+            split(F[(int64_t)b * step], f);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (l[t] != kNoRow) mx[t] = l[t];                   // rows increase with b: latest = max
+                if (f[t] != kNoRow && mn[t] == 0x10000) mn[t] = f[t];  // earliest in the chunk = min
+            }
         }
-    agg_last[ch][cx] = mx;
-    agg_first[ch][cx] = mn;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        agg_last[ch][4 * cx + t] = mx[t];
+        agg_first[ch][4 * cx + t] = mn[t];
+    }
     __syncthreads();
     if (!ok) return;
-    int above = -1, below = 0x10000;
-    for (int c = 0; c < ch; ++c) above = max(above, agg_last[c][cx]);
-    for (int c = nc - 1; c > ch; --c) below = min(below, agg_first[c][cx]);
+    int above[4], below[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        above[t] = -1;
+        below[t] = 0x10000;
+        for (int c = 0; c < ch; ++c) above[t] = max(above[t], agg_last[c][4 * cx + t]);
+        for (int c = nc - 1; c > ch; --c) below[t] = min(below[t], agg_first[c][4 * cx + t]);
+    }
+    auto pack = [](const int (&v)[4], int none) -> uint2 {
+        uint32_t w[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) w[t] = v[t] == none ? kNoRow : (uint32_t)v[t];
+        return make_uint2(w[0] | (w[1] << 16), w[2] | (w[3] << 16));
+    };
     for (int b = b0; b < b1; ++b) {  // exclusive prefix max
-        const int l = Lp[(int64_t)b * Wp];
-        Lp[(int64_t)b * Wp] = above < 0 ? kNoRow : (uint16_t)above;
-        if (l != kNoRow) above = l;
+        int l[4];
+        split(Lp[(int64_t)b * step], l);
+        Lp[(int64_t)b * step] = pack(above, -1);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (l[t] != kNoRow) above[t] = l[t];
     }
     for (int b = b1 - 1; b >= b0; --b) {  // exclusive suffix min
-        const int f = F[(int64_t)b * Wp];
-        F[(int64_t)b * Wp] = below == 0x10000 ? kNoRow : (uint16_t)below;
-        if (f != kNoRow) below = f;
+        int f[4];
+        split(F[(int64_t)b * step], f);
+        F[(int64_t)b * step] = pack(below, 0x10000);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (f[t] != kNoRow) below[t] = f[t];
     }
 }
 
@@ -232,7 +262,12 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
     const int nrows = min(kBand, a.H - r0);
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
     uint32_t m[4];
-    band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    if (a.bmask) {  // K1a's masks: 16 bytes instead of 32 image rows
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.bmask + ((int64_t)im * a.nb + b) * a.Wp + j0));
+        m[0] = q.x; m[1] = q.y; m[2] = q.z; m[3] = q.w;
+    } else {
+        band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
+    }
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
         if ((a.pts || a.skip_full) && skip_plane(s)) continue;
@@ -271,6 +306,27 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
                 }
             }
         };
+        if (!OUT_SQ && (mk[0] | mk[1] | mk[2] | mk[3]) == 0) {
+            // no object of this polarity in the band's 4 columns (sparse images):
+            // rows up to (ca + cb) / 2 take the carry above (the upper row on a
+            // tie), the others the carry below
+            int thr[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                thr[c] = ca[c] == kNoRow ? -1 : (cb[c] == kNoRow ? 0x7fffffff : (int)((ca[c] + cb[c]) >> 1));
+            const uint32_t lo0 = ca[0] | (ca[1] << 16), lo1 = ca[2] | (ca[3] << 16);
+            const uint32_t hi0 = cb[0] | (cb[1] << 16), hi1 = cb[2] | (cb[3] << 16);
+            uint16_t* dst = nr + (((int64_t)s * a.n_img + im) * a.H + r0) * a.Wp + j0;
+            for (int r = 0; r < nrows; ++r) {
+                const int i = r0 + r;
+                const uint32_t x0 = i <= thr[0] ? (lo0 & 0xffffu) : (hi0 & 0xffffu);
+                const uint32_t x1 = i <= thr[1] ? (lo0 & 0xffff0000u) : (hi0 & 0xffff0000u);
+                const uint32_t x2 = i <= thr[2] ? (lo1 & 0xffffu) : (hi1 & 0xffffu);
+                const uint32_t x3 = i <= thr[3] ? (lo1 & 0xffff0000u) : (hi1 & 0xffff0000u);
+                *reinterpret_cast<uint2*>(dst + (int64_t)r * a.Wp) = make_uint2(x0 | x1, x2 | x3);
+            }
+            continue;
+        }
         if (nrows == kBand) {  // full band: fully unrolled (masks, shifts constant-folded)
 #pragma unroll
             for (int r = 0; r < kBand; ++r) row_out(r);
