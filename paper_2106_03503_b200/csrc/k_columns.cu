@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64
 // K1c: per pixel nearest object row (OUT_SQ=false: uint16 plane [slot][img][H][Wp])
 // or the squared vertical distance (OUT_SQ=true: int32, dense [img][H][W]).
 template <bool OUT_SQ>
-__global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
+__global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
                             const uint16_t* __restrict__ above, uint16_t* __restrict__ nr,
                             int32_t* __restrict__ vsq) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -316,14 +316,16 @@ __global__ void k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
                 thr[c] = ca[c] == kNoRow ? -1 : (cb[c] == kNoRow ? 0x7fffffff : (int)((ca[c] + cb[c]) >> 1));
             const uint32_t lo0 = ca[0] | (ca[1] << 16), lo1 = ca[2] | (ca[3] << 16);
             const uint32_t hi0 = cb[0] | (cb[1] << 16), hi1 = cb[2] | (cb[3] << 16);
-            uint16_t* dst = nr + (((int64_t)s * a.n_img + im) * a.H + r0) * a.Wp + j0;
-            for (int r = 0; r < nrows; ++r) {
+            uint2* dst = reinterpret_cast<uint2*>(nr + (((int64_t)s * a.n_img + im) * a.H + r0) * a.Wp + j0);
+            const int rstep = a.Wp >> 2;  // uint2 per row
+#pragma unroll 4
+            for (int r = 0; r < nrows; ++r, dst += rstep) {
                 const int i = r0 + r;
                 const uint32_t x0 = i <= thr[0] ? (lo0 & 0xffffu) : (hi0 & 0xffffu);
                 const uint32_t x1 = i <= thr[1] ? (lo0 & 0xffff0000u) : (hi0 & 0xffff0000u);
                 const uint32_t x2 = i <= thr[2] ? (lo1 & 0xffffu) : (hi1 & 0xffffu);
                 const uint32_t x3 = i <= thr[3] ? (lo1 & 0xffff0000u) : (hi1 & 0xffff0000u);
-                *reinterpret_cast<uint2*>(dst + (int64_t)r * a.Wp) = make_uint2(x0 | x1, x2 | x3);
+                *dst = make_uint2(x0 | x1, x2 | x3);
             }
             continue;
         }
