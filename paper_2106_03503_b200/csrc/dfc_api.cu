@@ -446,7 +446,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         ra.row_count = rest_count;
         ra.row_done = nullptr;
         void* args[] = {&ra};
-        const int64_t sblocks = std::min<int64_t>(blocks, 148 * 64);
+        const int64_t sblocks = std::min<int64_t>(blocks, 148 * 8);  // grid-stride over the list (often empty)
         e = cudaLaunchKernel(fn, dim3((unsigned)sblocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
         if (e != cudaSuccess) return cuda_fail(e);
         ++g_launches;
