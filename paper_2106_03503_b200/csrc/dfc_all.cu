@@ -10,5 +10,6 @@
 #include "k_rows_pts.cu"
 #include "k_rows_anc.cu"
 #include "k_raster.cu"
+#include "k_raster_anc.cu"
 #include "k_render.cu"
 #include "dfc_api.cu"

@@ -724,11 +724,25 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
     r.city = d_cityblock;
     r.chess = d_chessboard;
     r.cham = d_chamfer34;
-    const int padW = (int)(cols + cols / r.L + 1);
-    const int smem = (2 * padW + 2 * r.T + 2) * 4;
-    e = cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_fail(e);
-    k_raster<<<(unsigned)rows, r.T, smem, st>>>(r);
+    // anchored segments (k_raster_anc.cu) up to kRaMaxW columns; DFC_RASTER=window
+    // keeps the outward window search (k_raster.cu) for A/B
+    static const bool window = [] {
+        const char* v = getenv("DFC_RASTER");
+        return v && strcmp(v, "window") == 0;
+    }();
+    if (!window && cols <= kRaMaxW) {
+        const int smem = ra_smem_bytes((int)cols);
+        e = cudaFuncSetAttribute(k_raster_anc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_fail(e);
+        const int64_t blocks = std::min<int64_t>(rows, 148 * 16);
+        k_raster_anc<<<(unsigned)blocks, 32 * kRaWarps, smem, st>>>(r);
+    } else {
+        const int padW = (int)(cols + cols / r.L + 1);
+        const int smem = (2 * padW + 2 * r.T + 2) * 4;
+        e = cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_fail(e);
+        k_raster<<<(unsigned)rows, r.T, smem, st>>>(r);
+    }
     ++g_launches;
     e = cudaGetLastError();
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);

@@ -179,6 +179,27 @@ def test_raster_argmin_monotone():
             assert (np.diff(kstar, axis=1) >= 0).all()
 
 
+def test_raster_argmin_monotone_synthetic():
+    """Same property on arbitrary vertical-distance rows (many ties, empty columns),
+    smallest and largest minimiser alike: k_raster_anc.cu brackets every segment's
+    minimisers by the owners at its two ends."""
+    rng = np.random.default_rng(5)
+    for _ in range(3000):
+        W = int(rng.integers(2, 120))
+        a = rng.integers(0, int(rng.choice([2, 5, 20, 100])), W).astype(np.int64)
+        none = rng.random(W) < rng.choice([0.0, 0.3, 0.8])
+        if none.all():
+            continue
+        h = np.abs(np.arange(W)[:, None] - np.arange(W)[None, :])
+        A = np.broadcast_to(a[None, :], h.shape)
+        mx, mn = np.maximum(A, h), np.minimum(A, h)
+        for f in (mx, 3 * mx + mn):
+            v = np.where(np.broadcast_to(none[None, :], h.shape), 1 << 40, f)
+            hit = v == v.min(axis=1, keepdims=True)
+            lo, hi = hit.argmax(axis=1), W - 1 - hit[:, ::-1].argmax(axis=1)
+            assert (np.diff(lo) >= 0).all() and (np.diff(hi) >= 0).all()
+
+
 def test_label_tie_rule_min_column_then_min_row():
     """voronoi_labels = (smallest minimizing column, then upper row); nearest_col =
     largest minimizing column (SURVEY finding 4)."""
