@@ -25,12 +25,12 @@
 //              same level loop; then lane = column scans its segment's range.
 //              An object pixel on the row (a = 0) owns itself (value 0), and a
 //              segment of object pixels is written directly.
-// One CTA (4 warps) per row, grid-stride; coalesced 4-byte stores.
+// One CTA (8 warps) per row, grid-stride; coalesced 4-byte stores.
 #include "dfc_kernels.cuh"
 
 namespace dfc {
 
-constexpr int kRaWarps = 4;
+constexpr int kRaWarps = 8;
 constexpr int kRaMaxW = 16384;
 constexpr int kRaBig = 0x1fffffff;   // a_k of a column without objects (3 kRaBig + h fits int32)
 constexpr int kRaNone = 0x7fffffff;
@@ -87,7 +87,7 @@ __device__ __forceinline__ void ra_scan2(const int* av, int j, int lo, int hi, i
     lch = bc;
 }
 
-__global__ void __launch_bounds__(32 * kRaWarps, 12) k_raster_anc(RasterArgs a) {
+__global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
     extern __shared__ uint4 rasm[];
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int NW = kRaWarps;
