@@ -170,8 +170,9 @@ def test_vertical_pass(dfc):
         np.testing.assert_array_equal(got.cpu().numpy(), oracle.to_i32(oracle.vertical_pass(img)))
 
 
-@pytest.mark.parametrize("shape", [(1, 1), (9, 10), (64, 64), (50, 1500), (3, 5000), (333, 77)])
-@pytest.mark.parametrize("density", [0.0, 0.003, 0.05, 0.5])
+@pytest.mark.parametrize("shape", [(1, 1), (9, 10), (64, 64), (50, 1500), (3, 5000), (333, 77), (5, 16384),
+                                   (3, 17000), (70, 33)])
+@pytest.mark.parametrize("density", [0.0, 0.003, 0.05, 0.5, 0.97])
 def test_raster_random(dfc, shape, density):
     img = oracle.random_image(shape[0], shape[1], density, 7 * shape[0] + shape[1])
     r = dfc.raster(_dev(img))
@@ -457,6 +458,17 @@ def test_merge_row_kernel(merge_kernel, shape, density):
     img = oracle.random_image(shape[0], shape[1], density, 5 * shape[0] + shape[1] + int(density * 1000))
     _check_edt(merge_kernel, img)
     _check_edt(merge_kernel, img, polarity=1)
+
+
+@pytest.mark.parametrize("shape", [(4, 17000), (33000, 3)])
+@pytest.mark.parametrize("density", [0.01, 0.3, 0.9])
+def test_default_path_outside_anc_limits(dfc, shape, density):
+    """Rows wider than 16384 columns or planes taller than 32768 rows leave the
+    anchored-segment kernel and the band staging: dense-row / merge-tree kernels
+    and the nearest-row plane take over."""
+    img = oracle.random_image(shape[0], shape[1], density, shape[0] + shape[1] + int(100 * density))
+    _check_edt(dfc, img)
+    _check_edt(dfc, img, polarity=1)
 
 
 def test_anc_ties_and_long_runs(anc_kernel):
