@@ -61,7 +61,7 @@ ROW_KERNELS = {
     "c1": "row pass (k_rows_anc: the plane is neither dense nor sparse)",
     "c2": "row pass (k_rows_anc, both planes)",
     "c3": "row pass (k_rows_pts: every image is a point plane, <= 32 object pixels)",
-    "c4": "k_band_* + k_raster (whole step)",
+    "c4": "k_band_* + k_raster_anc (whole step)",
     "c5": "row pass (k_rows_lr: a sparse plane)",
 }
 
