@@ -124,7 +124,8 @@ RowGeom row_geom(int W) {
 int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch, int64_t istride,
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
                 cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr,
-                uint32_t* pts = nullptr, uint32_t* bmask = nullptr, bool skip_full = false) {
+                uint32_t* pts = nullptr, uint32_t* bmask = nullptr, bool skip_full = false,
+                bool no_fill = false) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -156,6 +157,10 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
         const int nc = std::min(32, c.nb / 4);
         dim3 gs((unsigned)((W + 127) / 128), (unsigned)(npol * n));
         k_band_scan<<<gs, 32 * nc, 0, st>>>((int)W, Wp, c.nb, npol * n, first, last, skip);
+    }
+    if (no_fill) {  // the row pass stages from the bands: no nearest-row plane
+        g_launches += 2;
+        return DFC_OK;
     }
     if (vsq)
         k_band_fill<true><<<grid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
@@ -705,13 +710,23 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
     const int Wp = (int)round_up(cols, 8);
     const int64_t nb = (rows + kBand - 1) / kBand;
     const size_t carry = (size_t)nb * Wp, nre = (size_t)rows * Wp;
+    // anchored segments (k_raster_anc.cu) up to kRaMaxW columns, staging rows
+    // from the band masks and carries; DFC_RASTER=window keeps the outward
+    // window search (k_raster.cu) for A/B
+    static const bool window = [] {
+        const char* v = getenv("DFC_RASTER");
+        return v && strcmp(v, "window") == 0;
+    }();
+    const bool anc = !window && cols <= kRaMaxW;
     Scratch sc(st);
-    cudaError_t e = sc.alloc((2 * carry + nre) * sizeof(uint16_t) + 256);
+    cudaError_t e = sc.alloc((2 * carry + (anc ? 0 : nre)) * sizeof(uint16_t) + 256 + (anc ? carry * 4 + 16 : 0));
     if (e != cudaSuccess) return cuda_fail(e);
     uint16_t* first = static_cast<uint16_t*>(sc.p);
     uint16_t* last = first + carry;
     uint16_t* nr = reinterpret_cast<uint16_t*>(round_up(reinterpret_cast<uintptr_t>(last + carry), 16));
-    column_pass(d_img, 1, rows, cols, pitch_bytes, 0, 0, 1, nr, first, last, Wp, st);
+    uint32_t* bmask = anc ? reinterpret_cast<uint32_t*>(nr) : nullptr;  // [nb][Wp] in place of the plane
+    column_pass(d_img, 1, rows, cols, pitch_bytes, 0, 0, 1, anc ? nullptr : nr, first, last, Wp, st, nullptr,
+                nullptr, nullptr, bmask, false, anc);
     RasterArgs r;
     r.nr = nr;
     r.Wp = Wp;
@@ -724,13 +739,10 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
     r.city = d_cityblock;
     r.chess = d_chessboard;
     r.cham = d_chamfer34;
-    // anchored segments (k_raster_anc.cu) up to kRaMaxW columns; DFC_RASTER=window
-    // keeps the outward window search (k_raster.cu) for A/B
-    static const bool window = [] {
-        const char* v = getenv("DFC_RASTER");
-        return v && strcmp(v, "window") == 0;
-    }();
-    if (!window && cols <= kRaMaxW) {
+    r.bmask = bmask;
+    r.babove = last;
+    r.bbelow = first;
+    if (anc) {
         const int smem = ra_smem_bytes((int)cols);
         e = cudaFuncSetAttribute(k_raster_anc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e);

@@ -70,6 +70,11 @@ struct RasterArgs {
     int32_t* city;
     int32_t* chess;
     int32_t* cham;
+    // band source (k_raster_anc; nullable bmask = read nr): K1a's masks and
+    // K1b's carries above / below, [nb][Wp]
+    const uint32_t* bmask;
+    const uint16_t* babove;
+    const uint16_t* bbelow;
 };
 
 // Point plane: at most kPtsCap object pixels (C3's 30-point images).  With

@@ -110,13 +110,30 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
     for (int64_t i64 = blockIdx.x; i64 < a.H; i64 += gridDim.x) {
         const int i = (int)i64;
         const uint16_t* rowp = a.nr + (int64_t)i * a.Wp;
+        const int bb = i >> 5, br = i & 31;
+        const uint32_t upmask = 0xffffffffu >> (31 - br);
 
         // ---- stage a_k, the object bits and the segment minima of a_k -/+ k ----
         bool any = false;
         for (int q0 = warp * 32; 4 * q0 < W; q0 += 32 * NW) {  // warp-uniform trip count
             const int q = q0 + lane;
             int d[4] = {kRaBig, kRaBig, kRaBig, kRaBig};
-            if (4 * q < W) {
+            if (4 * q < W && a.bmask) {  // band source: the band's mask (object = nonzero) and carries
+                const int64_t off = (int64_t)bb * a.Wp;
+                const uint4 m4 = __ldg(reinterpret_cast<const uint4*>(a.bmask + off) + q);
+                const uint2 a2 = __ldg(reinterpret_cast<const uint2*>(a.babove + off) + q);
+                const uint2 b2 = __ldg(reinterpret_cast<const uint2*>(a.bbelow + off) + q);
+                const uint32_t mm[4] = {m4.x, m4.y, m4.z, m4.w};
+                const uint32_t ca[4] = {a2.x & 0xffffu, a2.x >> 16, a2.y & 0xffffu, a2.y >> 16};
+                const uint32_t cb[4] = {b2.x & 0xffffu, b2.x >> 16, b2.y & 0xffffu, b2.y >> 16};
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const uint32_t up = mm[t] & upmask, dn = mm[t] >> br;
+                    const int du = up ? br - 31 + (int)__clz(up) : (ca[t] == kNoRow ? kRaBig : i - (int)ca[t]);
+                    const int dd = dn ? __ffs(dn) - 1 : (cb[t] == kNoRow ? kRaBig : (int)cb[t] - i);
+                    if (4 * q + t < W) d[t] = min(du, dd);
+                }
+            } else if (4 * q < W) {
                 const uint2 v = __ldg(reinterpret_cast<const uint2*>(rowp) + q);
                 const uint32_t r[4] = {v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16};
 #pragma unroll
