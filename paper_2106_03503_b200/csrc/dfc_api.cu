@@ -743,11 +743,15 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
     r.babove = last;
     r.bbelow = first;
     if (anc) {
-        const int smem = ra_smem_bytes((int)cols);
-        e = cudaFuncSetAttribute(k_raster_anc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const bool p16 = rows <= kRa16MaxDim && cols <= kRa16MaxDim;
+        const void* fn = p16 ? (const void*)k_raster_anc<true> : (const void*)k_raster_anc<false>;
+        const int smem = ra_smem_bytes((int)cols, p16);
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e);
         const int64_t blocks = std::min<int64_t>(rows, 148 * 16);
-        k_raster_anc<<<(unsigned)blocks, 32 * kRaWarps, smem, st>>>(r);
+        void* args[] = {&r};
+        e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(32 * kRaWarps), args, (size_t)smem, st);
+        if (e != cudaSuccess) return cuda_fail(e);
     } else {
         const int padW = (int)(cols + cols / r.L + 1);
         const int smem = (2 * padW + 2 * r.T + 2) * 4;

@@ -26,6 +26,8 @@
 //              An object pixel on the row (a = 0) owns itself (value 0), and a
 //              segment of object pixels is written directly.
 // One CTA (8 warps) per row, grid-stride; coalesced 4-byte stores.
+#include <type_traits>
+
 #include "dfc_kernels.cuh"
 
 namespace dfc {
@@ -37,10 +39,17 @@ constexpr int kRaNone = 0x7fffffff;
 
 __host__ __device__ __forceinline__ int ra_segs(int W) { return (W + 31) >> 5; }
 __host__ __device__ __forceinline__ int ra_gwords(int W) { return (W + 3) & ~3; }
-// words: a (gw), owners of both families (2 (S+1)), object bits, segment minima / carries (4 S), parts (4 NW)
-inline int ra_smem_bytes(int W) {
+// 16-bit variant (rows and columns <= 8192): a_k as uint16 (kRa16Big for none),
+// so that two candidates share one SIMD instruction (VIMNMX.U16x2 / VIADD.16x2);
+// every value fits: chessboard <= 8191 < kRa16Big, chamfer <= 32764 <
+// 3 kRa16Big <= chamfer of a column without objects <= 57340 < 2^16.
+constexpr int kRa16Big = 16383;
+constexpr int kRa16MaxDim = 8192;
+// words: a (gw, or gw/2 + 4 for uint16), owners of both families (2 (S+1)),
+// object bits, segment minima / carries (4 S), parts (4 NW)
+inline int ra_smem_bytes(int W, bool p16) {
     const int S = ra_segs(W);
-    return (ra_gwords(W) + 2 * (S + 1) + 5 * S + 4 * kRaWarps) * 4;
+    return ((p16 ? ra_gwords(W) / 2 + 4 : ra_gwords(W)) + 2 * (S + 1) + 5 * S + 4 * kRaWarps) * 4;
 }
 
 struct RaInf {
@@ -52,11 +61,11 @@ struct RaCham {
 
 // Minimum of F over the candidates [lo, hi] (possibly empty: kRaNone) for
 // column j, and its smallest minimiser: lane = candidate, then REDUX minima.
-template <class F>
-__device__ __forceinline__ int ra_owner(const int* av, int j, int lo, int hi, int lane, int& col) {
+template <class F, class T>
+__device__ __forceinline__ int ra_owner(const T* av, int j, int lo, int hi, int lane, int& col) {
     int best = kRaNone, bk = lo;
     for (int k = lo + lane; k <= hi; k += 32) {
-        const int v = F::f(av[k], abs(j - k));
+        const int v = F::f((int)av[k], abs(j - k));
         if (v < best) {
             best = v;
             bk = k;
@@ -87,15 +96,39 @@ __device__ __forceinline__ void ra_scan2(const int* av, int j, int lo, int hi, i
     lch = bc;
 }
 
+// The same over uint16 a_k, two candidates per SIMD instruction: the superset
+// [lo & ~7, hi | 7], 16-byte loads of 8 candidates.
+__device__ __forceinline__ void ra_scan2_16(const uint16_t* av, int j, int lo, int hi, int& linf, int& lch) {
+    uint32_t bi = 0xffffffffu, bc = 0xffffffffu;
+    for (int k = lo & ~7; k <= hi; k += 8) {
+        const uint4 q = *reinterpret_cast<const uint4*>(av + k);
+        const uint32_t aa[4] = {q.x, q.y, q.z, q.w};
+        // (j - k, j - k - 1) as signed 16-bit halves, then 2 less per pair
+        uint32_t d2 = (uint32_t)((j - k) & 0xffff) | ((uint32_t)((j - k - 1) & 0xffff) << 16);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t h2 = __vmaxs2(d2, __vsub2(0u, d2));  // |j - k|
+            const uint32_t m = __vmaxu2(aa[t], h2);
+            bi = __vminu2(bi, m);
+            bc = __vminu2(bc, __vadd2(__vadd2(m, m), __vadd2(aa[t], h2)));  // 3 max + min
+            d2 = __vsub2(d2, 0x00020002u);
+        }
+    }
+    linf = (int)min(bi & 0xffffu, bi >> 16);
+    lch = (int)min(bc & 0xffffu, bc >> 16);
+}
+
+template <bool P16>
 __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
+    using T = typename std::conditional<P16, uint16_t, int>::type;
     extern __shared__ uint4 rasm[];
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int NW = kRaWarps;
     const int W = a.W;
     const int S = ra_segs(W);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    int* av = reinterpret_cast<int*>(rasm);
-    int* ancI = av + ra_gwords(W);  // [S + 1] chessboard owners
+    T* av = reinterpret_cast<T*>(rasm);
+    int* ancI = reinterpret_cast<int*>(rasm) + (P16 ? ra_gwords(W) / 2 + 4 : ra_gwords(W));  // [S + 1] chessboard owners
     int* ancC = ancI + S + 1;       // [S + 1] chamfer owners
     uint32_t* zb = reinterpret_cast<uint32_t*>(ancC + S + 1);  // [S] object pixels on the row
     int* m1 = reinterpret_cast<int*>(zb + S);  // [S] min (a_k - k) per segment -> exclusive prefix min
@@ -152,7 +185,16 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
                     x2 = min(x2, d[t] + j);
                 }
             }
-            if (4 * q < W) reinterpret_cast<int4*>(av)[q] = make_int4(d[0], d[1], d[2], d[3]);
+            if (4 * q < W) {
+                if (P16) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) d[t] = min(d[t], kRa16Big);
+                    reinterpret_cast<uint2*>(av)[q] = make_uint2((uint32_t)d[0] | ((uint32_t)d[1] << 16),
+                                                                 (uint32_t)d[2] | ((uint32_t)d[3] << 16));
+                } else {
+                    reinterpret_cast<int4*>(av)[q] = make_int4(d[0], d[1], d[2], d[3]);
+                }
+            }
             z <<= 4 * (lane & 7);
 #pragma unroll
             for (int o = 1; o < 8; o <<= 1) {
@@ -166,6 +208,7 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
                 m2[q >> 3] = x2;
             }
         }
+        if (P16 && tid < 8) av[ra_gwords(W) + tid] = (T)kRa16Big;  // the superset scan reads up to 8 past
         any = __syncthreads_or(any);
         int32_t* crow = a.city ? a.city + (int64_t)i * W : nullptr;
         int32_t* brow = a.chess ? a.chess + (int64_t)i * W : nullptr;
@@ -293,7 +336,7 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
             if (zb[s] == 0xffffffffu) {  // every column an object pixel on the row
                 l1 = linf = lch = 0;
             } else {
-                const int aj = in ? av[j] : kRaBig;
+                const int aj = in ? (int)av[j] : kRaBig;
                 int p = in ? aj - j : kRaNone, u = in ? aj + j : kRaNone;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -302,7 +345,11 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
                     if (lane + o < 32) u = min(u, dn);
                 }
                 l1 = min(min(p, c1[s]) + j, min(u, c2[s]) - j);
-                ra_scan2(av, j, min(ancI[s], ancC[s]), max(ancI[s + 1], ancC[s + 1]), linf, lch);
+                const int lo = min(ancI[s], ancC[s]), hi = max(ancI[s + 1], ancC[s + 1]);
+                if constexpr (P16)
+                    ra_scan2_16(av, j, lo, hi, linf, lch);
+                else
+                    ra_scan2(av, j, lo, hi, linf, lch);
             }
             if (in) {
                 if (crow) __stcs(crow + j, l1);
