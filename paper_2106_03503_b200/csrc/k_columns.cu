@@ -31,16 +31,20 @@ __device__ __forceinline__ void band_masks(const uint8_t* __restrict__ base, int
     m[0] = m[1] = m[2] = m[3] = 0u;
     if (vec && j0 + 3 < W) {
         uint32_t v[kBand];
+        const uint8_t* p = base + j0;
 #pragma unroll
-        for (int r = 0; r < kBand; ++r)
-            v[r] = r < nrows ? __ldg(reinterpret_cast<const uint32_t*>(base + r * pitch + j0)) : 0u;
+        for (int r = 0; r < kBand; ++r, p += pitch)
+            v[r] = r < nrows ? __ldg(reinterpret_cast<const uint32_t*>(p)) : 0u;
+        // 4 x 32 bit transpose: x[g] byte c bit b = row 8g + b of column c
+        // (one 0xff-per-nonzero-byte compare and one masked OR per row), then
+        // each column's word gathers byte c of x[0..3] with three byte permutes
+        uint32_t x[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int r = 0; r < kBand; ++r) {
-            const uint32_t nz = __vcmpne4(v[r], 0u);  // 0xff per nonzero byte
-            m[0] |= (nz & 1u) << r;
-            m[1] |= ((nz >> 8) & 1u) << r;
-            m[2] |= ((nz >> 16) & 1u) << r;
-            m[3] |= ((nz >> 24) & 1u) << r;
+        for (int r = 0; r < kBand; ++r) x[r >> 3] |= __vcmpne4(v[r], 0u) & (0x01010101u << (r & 7));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const uint32_t sel = (uint32_t)c | ((uint32_t)(c + 4) << 4);
+            m[c] = __byte_perm(__byte_perm(x[0], x[1], sel), __byte_perm(x[2], x[3], sel), 0x5410);
         }
     } else {
         for (int r = 0; r < nrows; ++r) {
