@@ -162,10 +162,11 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
         g_launches += 2;
         return DFC_OK;
     }
+    const dim3 fgrid(grid.x, (unsigned)(n > 1 ? (c.nb + kFillBands - 1) / kFillBands : c.nb), grid.z);
     if (vsq)
-        k_band_fill<true><<<grid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
+        k_band_fill<true><<<fgrid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
     else
-        k_band_fill<false><<<grid, tpb, 0, st>>>(c, first, last, nr, nullptr);
+        k_band_fill<false><<<fgrid, tpb, 0, st>>>(c, first, last, nr, nullptr);
     g_launches += 3;
     return DFC_OK;
 }

@@ -242,6 +242,8 @@ __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64
 
 // K1c: per pixel nearest object row (OUT_SQ=false: uint16 plane [slot][img][H][Wp])
 // or the squared vertical distance (OUT_SQ=true: int32, dense [img][H][W]).
+constexpr int kFillBands = 8;
+
 template <bool OUT_SQ>
 __global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t* __restrict__ below,
                             const uint16_t* __restrict__ above, uint16_t* __restrict__ nr,
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t*
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
     const int j0 = 4 * g;
     if (j0 >= a.W) return;
-    const int b = blockIdx.y, im = blockIdx.z;
+    const int im = blockIdx.z;
     // planes without a nearest-row plane: point planes (k_rows_pts) and, with
     // skip_full, planes k_rows_anc stages from the bands (CTA-uniform)
     auto skip_plane = [&](int s) {
@@ -262,6 +264,10 @@ __global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t*
         for (int s = 0; s < a.npol; ++s) all = all && skip_plane(s);
         if (all) return;
     }
+    // several bands per CTA for batches (a skipped plane costs few CTAs), one
+    // for single images (loads of consecutive bands overlap across CTAs)
+    const int bpc = (a.nb + (int)gridDim.y - 1) / (int)gridDim.y;
+    for (int b = blockIdx.y * bpc; b < min(a.nb, (int)(blockIdx.y + 1) * bpc); ++b) {
     const int r0 = b * kBand;
     const int nrows = min(kBand, a.H - r0);
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
@@ -340,6 +346,7 @@ __global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t*
             for (int r = 0; r < nrows; ++r) row_out(r);
         }
     }
+    }  // bands
 }
 
 // Per-direction vertical passes over an arbitrary squared-distance map
