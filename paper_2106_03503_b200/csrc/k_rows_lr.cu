@@ -63,7 +63,11 @@ __device__ __forceinline__ const uint16_t* lr_col_ptr(const RowArgs& a, const ui
 
 // Fill one row's columns [c0, c1) from its entry list (column | start << 16,
 // plus the column's nearest row), lane = column; shared by k_rows_lr and
-// k_rows_pts.  rE / rR are in shared memory.
+// k_rows_pts.  rE / rR are in shared memory.  DONLY: only Drow is written
+// (the caller checked S, LB and NC are null), so a block with few owners
+// needs no owner per column: D(j) is the minimum of the block's owners'
+// parabolas (each is >= the envelope, and j's owner is among them).
+template <bool DONLY = false>
 __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE, const uint16_t* rR, int nE,
                                             uint32_t giR, int32_t* Drow, float* Srow, int32_t* Lrow,
                                             int32_t* Nrow, int c0, int c1, int lane) {
@@ -93,7 +97,38 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
         const uint32_t wav = giR > wr ? giR - wr : wr - giR;
         const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
         const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
-        if (nin <= 3) {
+        if (DONLY && nin <= 3) {
+            // ---- D only, at most 3 owner changes: minimum over the block's
+            // owners' parabolas g + (j - k)^2 (uint32: every value of an owner
+            // of this block is < 2^31 + 2^24 at its columns) ----
+            const int j = b + 4 * lane;
+            const uint32_t g0 = __shfl_sync(FULL, wg, 0);
+            uint32_t d[4];
+            if (g0 == kInfU) {  // featureless row: its only entry
+#pragma unroll
+                for (int t = 0; t < 4; ++t) d[t] = (uint32_t)DFC_INF_I32;
+            } else {
+                const int dj0 = j - (int)__shfl_sync(FULL, wk, 0);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) d[t] = g0 + (uint32_t)((dj0 + t) * (dj0 + t));
+                for (int e = 1; e <= nin; ++e) {  // warp-uniform trip count
+                    const uint32_t ge = __shfl_sync(FULL, wg, e);
+                    const int dje = j - (int)__shfl_sync(FULL, wk, e);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) d[t] = min(d[t], ge + (uint32_t)((dje + t) * (dje + t)));
+                }
+            }
+            if (vec4 && j + 3 < c1) {
+                __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d[0], (int)d[1], (int)d[2], (int)d[3]));
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (j + t < c1) __stcs(Drow + j + t, (int32_t)d[t]);
+            }
+            const int sn = __shfl_sync(FULL, s, nin + 1);
+            base += nin + (sn == b + 128 ? 1 : 0);
+            b += 128;
+        } else if (nin <= 3) {
             // ---- 128-column block with at most 3 owner changes (sparse rows):
             // broadcast the block's owners, each column keeps the last one
             // starting at or before it ----
@@ -480,7 +515,10 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
             int32_t* Nrow = a.NC ? reinterpret_cast<int32_t*>(a.NC + imgR * a.sN) + iR * W : nullptr;
             const uint32_t* rE = sE + (rho - r0) * S;
             const uint16_t* rR = sR + (rho - r0) * S;
-            lr_fill_row(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+            if (Drow && !Srow && !Lrow && !Nrow)
+                lr_fill_row<true>(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+            else
+                lr_fill_row<false>(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
         }
     }
     // rows whose list exceeds the staging capacity (chunks wider than kStage

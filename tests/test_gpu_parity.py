@@ -35,6 +35,9 @@ def _check_edt(dfc, img, polarity=0):
     want = oracle.to_i32(oracle.edt(src))
     got = out["sqdist"].cpu().numpy()
     np.testing.assert_array_equal(got, want)
+    # squared distances alone: the row kernels' D-only fills (no owner per column)
+    only = dfc.edt(_dev(img), polarity=polarity, dist=False, label=False, nearest_col=False)
+    np.testing.assert_array_equal(only["sqdist"].cpu().numpy(), want)
     np.testing.assert_array_equal(out["dist"].cpu().numpy().view(np.uint32),
                                   oracle.sqrt_f32(want).view(np.uint32))
     lab = oracle.voronoi_labels(src, linear=True)
