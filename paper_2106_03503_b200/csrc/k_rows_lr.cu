@@ -96,6 +96,61 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
         const uint32_t wk = we & 0xffffu;
         const uint32_t wav = giR > wr ? giR - wr : wr - giR;
         const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
+        if (DONLY) {
+            // ---- D only, a 512-column block with at most 3 owner changes (the
+            // usual case on sparse planes): lane l owns columns b + 128 h + 4 l
+            // + t (coalesced 16-byte stores per h); D(j) is the minimum of the
+            // block's owners' parabolas g + (j - k)^2 (uint32: each of them is
+            // an owner of a column of this block, so its value at any column of
+            // the block is < 2^31 + 2^26) ----
+            constexpr int kH = 4;
+            const int nbig = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 128 * kH - 1));
+            if (nbig <= 3) {
+                const uint32_t g0 = __shfl_sync(FULL, wg, 0);
+                const int k0 = (int)__shfl_sync(FULL, wk, 0);
+                uint32_t d[kH][4];
+                if (g0 == kInfU) {  // featureless row: its only entry
+#pragma unroll
+                    for (int h = 0; h < kH; ++h)
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) d[h][t] = (uint32_t)DFC_INF_I32;
+                } else {
+#pragma unroll
+                    for (int h = 0; h < kH; ++h) {
+                        const int dj = b + 128 * h + 4 * lane - k0;
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) d[h][t] = g0 + (uint32_t)((dj + t) * (dj + t));
+                    }
+                    for (int e = 1; e <= nbig; ++e) {  // warp-uniform trip count
+                        const uint32_t ge = __shfl_sync(FULL, wg, e);
+                        const int ke = (int)__shfl_sync(FULL, wk, e);
+#pragma unroll
+                        for (int h = 0; h < kH; ++h) {
+                            const int dj = b + 128 * h + 4 * lane - ke;
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) d[h][t] = min(d[h][t], ge + (uint32_t)((dj + t) * (dj + t)));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < kH; ++h) {
+                    const int j = b + 128 * h + 4 * lane;
+                    if (vec4 && j + 3 < c1) {
+                        __stcs(reinterpret_cast<int4*>(Drow + j),
+                               make_int4((int)d[h][0], (int)d[h][1], (int)d[h][2], (int)d[h][3]));
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (j + t < c1) __stcs(Drow + j + t, (int32_t)d[h][t]);
+                    }
+                }
+                // the next block's first owner: the last entry starting <= b + 128 kH
+                const int sn = __shfl_sync(FULL, s, nbig + 1);
+                base += nbig + (sn == b + 128 * kH ? 1 : 0);
+                b += 128 * kH;
+                continue;
+            }
+        }
         const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
         if (DONLY && nin <= 3) {
             // ---- D only, at most 3 owner changes: minimum over the block's
