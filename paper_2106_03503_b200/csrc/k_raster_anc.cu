@@ -76,6 +76,33 @@ __device__ __forceinline__ int ra_owner(const T* av, int j, int lo, int hi, int 
     return m;
 }
 
+// Both families' owners for column j over the union of their ranges [lo, hi]
+// (uint16 a_k: rows and columns <= 8192), scanned as the even-aligned superset
+// [lo & ~1, hi | 1]: an extra candidate can neither go below the minimum nor
+// tie it (it would then be a smaller global minimiser than the owner, which
+// lies in the range).  Lane = a pair of candidates (one 4-byte load); a
+// candidate's key is value << 13 | k, so that one min keeps the smallest
+// minimiser and one REDUX yields value and column.  Empty range: kRaNone.
+__device__ __forceinline__ void ra_owner2_16(const uint16_t* av, int j, int lo, int hi, int lane, int& mi,
+                                             int& ci, int& mc, int& cc) {
+    uint32_t bi = 0xffffffffu, bc = 0xffffffffu;
+    for (int k = (lo & ~1) + 2 * lane; k <= hi; k += 64) {
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(av + k);
+        const int a0 = (int)(a2 & 0xffffu), a1 = (int)(a2 >> 16);
+        const int h0 = abs(j - k), h1 = abs(j - k - 1);
+        bi = min(bi, ((uint32_t)max(a0, h0) << 13) | (uint32_t)k);
+        bi = min(bi, ((uint32_t)max(a1, h1) << 13) | (uint32_t)(k + 1));
+        bc = min(bc, ((uint32_t)max(3 * a0 + h0, a0 + 3 * h0) << 13) | (uint32_t)k);
+        bc = min(bc, ((uint32_t)max(3 * a1 + h1, a1 + 3 * h1) << 13) | (uint32_t)(k + 1));
+    }
+    bi = __reduce_min_sync(0xffffffffu, bi);
+    bc = __reduce_min_sync(0xffffffffu, bc);
+    mi = bi == 0xffffffffu ? kRaNone : (int)(bi >> 13);
+    ci = (int)(bi & 8191u);
+    mc = bc == 0xffffffffu ? kRaNone : (int)(bc >> 13);
+    cc = (int)(bc & 8191u);
+}
+
 // Chessboard and chamfer minima for column j over the union of their ranges
 // [lo, hi], scanned as its aligned superset [lo & ~3, hi | 3] (extra
 // candidates cannot go below a minimum the range attains; the padding past W
@@ -272,10 +299,17 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
                     int ci = j, cc = j;
                     if (!on_row(j)) {
                         int lo, hi;
-                        bounds(ancI, s, lo, hi);
-                        ra_owner<RaInf>(av, j, lo, hi, lane, ci);
-                        bounds(ancC, s, lo, hi);
-                        ra_owner<RaCham>(av, j, lo, hi, lane, cc);
+                        if constexpr (P16) {
+                            int lo2, hi2, mi, mc;
+                            bounds(ancI, s, lo, hi);
+                            bounds(ancC, s, lo2, hi2);
+                            ra_owner2_16(av, j, min(lo, lo2), max(hi, hi2), lane, mi, ci, mc, cc);
+                        } else {
+                            bounds(ancI, s, lo, hi);
+                            ra_owner<RaInf>(av, j, lo, hi, lane, ci);
+                            bounds(ancC, s, lo, hi);
+                            ra_owner<RaCham>(av, j, lo, hi, lane, cc);
+                        }
                     }
                     if (lane == 0) {
                         ancI[s] = ci;
@@ -293,6 +327,14 @@ __global__ void __launch_bounds__(32 * kRaWarps, 6) k_raster_anc(RasterArgs a) {
                             mi = mc = 0;
                             ci = cc = j;
                         }
+                    } else if constexpr (P16) {
+                        int lo, hi, lo2, hi2;
+                        bounds(ancI, s, lo, hi);
+                        bounds(ancC, s, lo2, hi2);
+                        lo = min(lo, lo2);
+                        hi = max(hi, hi2);
+                        const int c = (hi - lo + q) / q, plo = lo + part * c;
+                        ra_owner2_16(av, j, plo, min(hi, plo + c - 1), lane, mi, ci, mc, cc);
                     } else {
                         int lo, hi;
                         bounds(ancI, s, lo, hi);
