@@ -426,7 +426,16 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
                 aa.row_list = rest_rows;
                 aa.row_count = rest_count;
             }
-            const int64_t ablocks = std::min<int64_t>(a.total_rows, 148 * 16);
+            // one CTA per row (the block scheduler balances rows of unequal cost;
+            // a grid-stride cap of 16 CTAs per SM left 27% of the slots idle on
+            // the last round of rows: C2 row pass 0.320 -> 0.287 ms).  A compact
+            // row list (count on the device) keeps the grid-stride cap.
+            static const int anc_cap = [] {  // DFC_ANC_CAP (tuning): CTAs per SM, 0 = one CTA per row
+                const char* v = getenv("DFC_ANC_CAP");
+                return v ? atoi(v) : 0;
+            }();
+            const int64_t ablocks =
+                (anc_cap <= 0 && !aa.row_list) ? a.total_rows : std::min<int64_t>(a.total_rows, 148 * (anc_cap > 0 ? anc_cap : 16));
             void* aargs[] = {&aa};
             e = cudaLaunchKernel(afn, dim3((unsigned)ablocks), dim3(32 * kAncWarps), aargs, (size_t)asm_bytes, st);
             if (e != cudaSuccess) return cuda_fail(e);
@@ -749,7 +758,11 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
         const int smem = ra_smem_bytes((int)cols, p16);
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return cuda_fail(e);
-        const int64_t blocks = std::min<int64_t>(rows, 148 * 16);
+        static const int ra_cap = [] {  // DFC_RA_CAP (tuning): CTAs per SM, 0 = one CTA per row
+            const char* v = getenv("DFC_RA_CAP");
+            return v ? atoi(v) : 0;
+        }();
+        const int64_t blocks = ra_cap <= 0 ? rows : std::min<int64_t>(rows, 148 * ra_cap);
         void* args[] = {&r};
         e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(32 * kRaWarps), args, (size_t)smem, st);
         if (e != cudaSuccess) return cuda_fail(e);
