@@ -586,3 +586,22 @@ def test_point_plane_dual_polarity(dfc):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
     np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+
+
+@pytest.mark.parametrize("density", [3e-5, 0.002])
+def test_tall_wide_single_image(dfc, density):
+    """One image taller than 8192 rows and wider than k_rows_anc's 16384 columns
+    (a sparse plane: k_rows_lr; a denser one: k_rows_dense / k_rows), objects on
+    both sides of the middle row: squared distances (with and without the other
+    outputs), float distances and labels as the oracle."""
+    img = oracle.random_image(8192, 16416, density, 77 + int(density * 1e6))
+    img[:, 5000] = 0
+    img[4095:4097, 9000:9100] = 1  # objects on both sides of the half boundary
+    out = dfc.edt(_dev(img), dist=True, label=True)
+    only = dfc.edt(_dev(img), dist=False)
+    torch.cuda.synchronize()
+    want = oracle.to_i32(oracle.edt(img))
+    np.testing.assert_array_equal(out["sqdist"].cpu().numpy(), want)
+    np.testing.assert_array_equal(only["sqdist"].cpu().numpy(), want)
+    np.testing.assert_array_equal(out["dist"].cpu().numpy().view(np.uint32), oracle.sqrt_f32(want).view(np.uint32))
+    np.testing.assert_array_equal(out["label"].cpu().numpy(), oracle.voronoi_labels(img, linear=True)[1])
