@@ -343,18 +343,22 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
     const uint32_t gi = a.vdist ? 0u : i + (uint32_t)a.row0;
     const uint16_t* rowp = a.nr + (active ? img * a.nr_img_stride + (int64_t)i * a.Wp : 0);
 
+    // 8 columns of the row (raw: columns past the row end are masked by fix8 at
+    // the point of use, so that a prefetch is not consumed as soon as it is
+    // issued -- the masking selects would wait on the load)
     auto load8 = [&](int m0) -> uint4 {
         uint4 v = make_uint4(FULL, FULL, FULL, FULL);
-        if (active && m0 < W) {
-            v = __ldg(reinterpret_cast<const uint4*>(lr_col_ptr(a, rowp, m0)));
-            if (m0 + 8 > W) {  // columns past the row end: no candidate
-                const int valid = W - m0;  // 1..7
-                uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+        if (active && m0 < W) v = __ldg(reinterpret_cast<const uint4*>(lr_col_ptr(a, rowp, m0)));
+        return v;
+    };
+    auto fix8 = [&](uint4 v, int m0) -> uint4 {
+        if (m0 + 8 > W) {  // columns past the row end: no candidate (warp-uniform)
+            const int valid = W - m0;  // <= 7 (m0 >= W: already FULL)
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if (2 * t >= valid) w[t] = FULL;
-                    else if (2 * t + 1 >= valid) w[t] |= 0xffff0000u;
-                }
+            for (int t = 0; t < 4; ++t) {
+                if (2 * t >= valid) w[t] = FULL;
+                else if (2 * t + 1 >= valid) w[t] |= 0xffff0000u;
             }
         }
         return v;
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
         };
         int lo = b & ~7, hi = lo + 8;  // examined columns [lo, hi)
         bool go = active;
-        uint4 v = load8(lo);
+        uint4 v = fix8(load8(lo), lo);
 #pragma unroll
         for (int t = 0; t < 8; ++t) consider(lo + t, (half(v, t >> 1) >> (16 * (t & 1))) & 0xffffu);
         for (;;) {
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
             if (!__any_sync(FULL, go)) break;
             uint4 vl = make_uint4(FULL, FULL, FULL, FULL), vr = vl;
             if (go && left) vl = load8(lo - 8);
-            if (go && right) vr = load8(hi);
+            if (go && right) vr = fix8(load8(hi), hi);
             if (go && left) {
 #pragma unroll
                 for (int t = 7; t >= 0; --t) consider(lo - 8 + t, (half(vl, t >> 1) >> (16 * (t & 1))) & 0xffffu);
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
         const bool more = mine && m0 + 8 <= kE;
         uint4 nxt = make_uint4(FULL, FULL, FULL, FULL);
         if (more) nxt = load8(m0 + 8);
+        cur = fix8(cur, m0);
         if (mine) {
             if ((cur.x & cur.y & cur.z & cur.w) != FULL) {  // any candidate among the 8 columns
                 if (n > kLrCap - 8) {  // no room for 8 pushes: the row goes to the merge-tree kernel
