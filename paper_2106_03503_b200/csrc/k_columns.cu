@@ -189,17 +189,31 @@ __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64
     auto split = [](uint2 v, int (&o)[4]) {
         o[0] = (int)(v.x & 0xffffu); o[1] = (int)(v.x >> 16); o[2] = (int)(v.y & 0xffffu); o[3] = (int)(v.y >> 16);
     };
+    // every pass loads kB bands before using any (independent loads in flight
+    // instead of one load latency per band)
+    constexpr int kB = 8;
     int mx[4] = {-1, -1, -1, -1}, mn[4] = {0x10000, 0x10000, 0x10000, 0x10000};
     if (ok)
-        for (int b = b0; b < b1; ++b) {
-            int l[4], f[4];
-            split(Lp[(int64_t)b * step], l);
-            split(F[(int64_t)b * step], f);
+        for (int bb = b0; bb < b1; bb += kB) {
+            uint2 lv[kB], fv[kB];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (l[t] != kNoRow) mx[t] = l[t];                   // rows increase with b: latest = max
-                if (f[t] != kNoRow && mn[t] == 0x10000) mn[t] = f[t];  // earliest in the chunk = min
-            }
+            for (int u = 0; u < kB; ++u)
+                if (bb + u < b1) {
+                    lv[u] = Lp[(int64_t)(bb + u) * step];
+                    fv[u] = F[(int64_t)(bb + u) * step];
+                }
+#pragma unroll
+            for (int u = 0; u < kB; ++u)
+                if (bb + u < b1) {
+                    int l[4], f[4];
+                    split(lv[u], l);
+                    split(fv[u], f);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (l[t] != kNoRow) mx[t] = l[t];                   // rows increase with b: latest = max
+                        if (f[t] != kNoRow && mn[t] == 0x10000) mn[t] = f[t];  // earliest in the chunk = min
+                    }
+                }
         }
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
@@ -207,14 +221,36 @@ __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64
         agg_first[ch][4 * cx + t] = mn[t];
     }
     __syncthreads();
+    // carries into each chunk: exclusive prefix max / suffix min over the nc
+    // chunk aggregates of every column, by warp scans (lane = chunk; warp w
+    // handles columns w, w + nc, ...), written back in place
+    for (int col = ch; col < 128; col += nc) {
+        const int c = cx;
+        int vl = c < nc ? agg_last[c][col] : -1;
+        int vf = c < nc ? agg_first[c][col] : 0x10000;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int ul = __shfl_up_sync(0xffffffffu, vl, o), df = __shfl_down_sync(0xffffffffu, vf, o);
+            if (c >= o) vl = max(vl, ul);
+            if (c + o < 32) vf = min(vf, df);
+        }
+        // inclusive -> exclusive
+        int el = __shfl_up_sync(0xffffffffu, vl, 1), ef = __shfl_down_sync(0xffffffffu, vf, 1);
+        if (c == 0) el = -1;
+        if (c + 1 >= nc) ef = 0x10000;
+        __syncwarp();
+        if (c < nc) {
+            agg_last[c][col] = el;
+            agg_first[c][col] = ef;
+        }
+    }
+    __syncthreads();
     if (!ok) return;
     int above[4], below[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-        above[t] = -1;
-        below[t] = 0x10000;
-        for (int c = 0; c < ch; ++c) above[t] = max(above[t], agg_last[c][4 * cx + t]);
-        for (int c = nc - 1; c > ch; --c) below[t] = min(below[t], agg_first[c][4 * cx + t]);
+        above[t] = agg_last[ch][4 * cx + t];
+        below[t] = agg_first[ch][4 * cx + t];
     }
     auto pack = [](const int (&v)[4], int none) -> uint2 {
         uint32_t w[4];
@@ -222,21 +258,37 @@ __global__ void __launch_bounds__(1024) k_band_scan(int W, int Wp, int nb, int64
         for (int t = 0; t < 4; ++t) w[t] = v[t] == none ? kNoRow : (uint32_t)v[t];
         return make_uint2(w[0] | (w[1] << 16), w[2] | (w[3] << 16));
     };
-    for (int b = b0; b < b1; ++b) {  // exclusive prefix max
-        int l[4];
-        split(Lp[(int64_t)b * step], l);
-        Lp[(int64_t)b * step] = pack(above, -1);
+    for (int bb = b0; bb < b1; bb += kB) {  // exclusive prefix max
+        uint2 lv[kB];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (l[t] != kNoRow) above[t] = l[t];
+        for (int u = 0; u < kB; ++u)
+            if (bb + u < b1) lv[u] = Lp[(int64_t)(bb + u) * step];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (bb + u < b1) {
+                int l[4];
+                split(lv[u], l);
+                Lp[(int64_t)(bb + u) * step] = pack(above, -1);
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (l[t] != kNoRow) above[t] = l[t];
+            }
     }
-    for (int b = b1 - 1; b >= b0; --b) {  // exclusive suffix min
-        int f[4];
-        split(F[(int64_t)b * step], f);
-        F[(int64_t)b * step] = pack(below, 0x10000);
+    for (int bb = b1 - 1; bb >= b0; bb -= kB) {  // exclusive suffix min
+        uint2 fv[kB];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (f[t] != kNoRow) below[t] = f[t];
+        for (int u = 0; u < kB; ++u)
+            if (bb - u >= b0) fv[u] = F[(int64_t)(bb - u) * step];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+            if (bb - u >= b0) {
+                int f[4];
+                split(fv[u], f);
+                F[(int64_t)(bb - u) * step] = pack(below, 0x10000);
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (f[t] != kNoRow) below[t] = f[t];
+            }
     }
 }
 
