@@ -605,3 +605,18 @@ def test_tall_wide_single_image(dfc, density):
     np.testing.assert_array_equal(only["sqdist"].cpu().numpy(), want)
     np.testing.assert_array_equal(out["dist"].cpu().numpy().view(np.uint32), oracle.sqrt_f32(want).view(np.uint32))
     np.testing.assert_array_equal(out["label"].cpu().numpy(), oracle.voronoi_labels(img, linear=True)[1])
+
+
+@pytest.mark.parametrize("shape", [(288, 200), (300, 77), (1000, 96), (2048, 64)])
+def test_band_scan_medium_heights(dfc, shape):
+    """9-64 bands of 32 rows (k_band_scan_serial; the chunked k_band_scan measured
+    slower there): single images of both polarities and a batch of non-point planes."""
+    img = oracle.random_image(shape[0], shape[1], 0.01, shape[0] + 7 * shape[1])
+    _check_edt(dfc, img)
+    _check_edt(dfc, img, polarity=1)
+    imgs = np.stack([oracle.random_image(shape[0], shape[1], 0.02, 100 + s) for s in range(3)])
+    out = dfc.edt_batched(_dev(imgs), dist=True, label=True)
+    torch.cuda.synchronize()
+    for b in range(3):
+        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
+        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
