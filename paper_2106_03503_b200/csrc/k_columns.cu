@@ -117,9 +117,9 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
 }
 
 // K1b (short columns, <= 64 bands): one thread per (column, plane), serial
-// over the bands with 4 independent loads in flight; same in-place result as
+// over the bands with 16 independent loads in flight; same in-place result as
 // the chunked scan below.
-__global__ void k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint16_t* __restrict__ first,
+__global__ void __launch_bounds__(256, 4) k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint16_t* __restrict__ first,
                                    uint16_t* __restrict__ last, const unsigned long long* skip_counts) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t plane = blockIdx.y;
@@ -127,39 +127,26 @@ __global__ void k_band_scan_serial(int W, int Wp, int nb, int64_t n_planes, uint
     if (skip_counts && skip_counts[plane] <= (unsigned long long)kPtsCap) return;  // point plane
     uint16_t* F = first + plane * nb * (int64_t)Wp + j;
     uint16_t* Lp = last + plane * nb * (int64_t)Wp + j;
-    uint16_t run = kNoRow;
-    int b = 0;
-    for (; b + 4 <= nb; b += 4) {
-        uint16_t t[4];
+    // both scans at once, 8 bands of each loaded before any is used: the
+    // exclusive prefix max of last (forward) and suffix min of first (backward)
+    constexpr int kB = 8;
+    uint16_t runL = kNoRow, runF = kNoRow;
+    for (int b = 0; b < nb; b += kB) {
+        uint16_t tl[kB], tf[kB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) t[u] = Lp[(int64_t)(b + u) * Wp];
+        for (int u = 0; u < kB; ++u)
+            if (b + u < nb) {
+                tl[u] = Lp[(int64_t)(b + u) * Wp];
+                tf[u] = F[(int64_t)(nb - 1 - b - u) * Wp];
+            }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            Lp[(int64_t)(b + u) * Wp] = run;
-            if (t[u] != kNoRow) run = t[u];
-        }
-    }
-    for (; b < nb; ++b) {
-        const uint16_t t = Lp[(int64_t)b * Wp];
-        Lp[(int64_t)b * Wp] = run;
-        if (t != kNoRow) run = t;
-    }
-    run = kNoRow;
-    b = nb - 1;
-    for (; b - 3 >= 0; b -= 4) {
-        uint16_t t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t[u] = F[(int64_t)(b - u) * Wp];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            F[(int64_t)(b - u) * Wp] = run;
-            if (t[u] != kNoRow) run = t[u];
-        }
-    }
-    for (; b >= 0; --b) {
-        const uint16_t t = F[(int64_t)b * Wp];
-        F[(int64_t)b * Wp] = run;
-        if (t != kNoRow) run = t;
+        for (int u = 0; u < kB; ++u)
+            if (b + u < nb) {
+                Lp[(int64_t)(b + u) * Wp] = runL;
+                if (tl[u] != kNoRow) runL = tl[u];
+                F[(int64_t)(nb - 1 - b - u) * Wp] = runF;
+                if (tf[u] != kNoRow) runF = tf[u];
+            }
     }
 }
 
