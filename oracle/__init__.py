@@ -99,9 +99,14 @@ def _bind_ref(lib):
     return lib
 
 
-if not os.path.exists(os.path.join(HERE, "build", "liborc.so")):
+_ORC = os.path.join(HERE, "build", "liborc.so")
+if os.path.exists(_ORC):
+    with open(_ORC, "rb") as _f:
+        if b"dfg_sparse_tiles" not in _f.read():  # built before the generators moved in
+            os.remove(_ORC)
+if not os.path.exists(_ORC):
     build()
-orc = _bind_orc(C.CDLL(os.path.join(HERE, "build", "liborc.so")))
+orc = _bind_orc(C.CDLL(_ORC))
 ref = _bind_ref(_load(os.path.join(HERE, "_ref", "libdfref.so")))
 
 
@@ -109,6 +114,26 @@ def _img(img):
     img = np.ascontiguousarray(img, dtype=np.uint8)
     assert img.ndim == 2
     return img, img.shape[0], img.shape[1]
+
+
+# ------------------------------------------------------------------ workloads
+def workload(name, scale=1, seed=None):
+    """The seeded input of config `name` (workloads.config) generated by the
+    oracle's own copy of workloads/gen.c: the reference arm of bench.py uses
+    this, so it maps no library of the product."""
+    import workloads
+    return workloads.config(name, scale=scale, seed=seed, lib=_wl_lib())
+
+
+_wl_bound = None
+
+
+def _wl_lib():
+    global _wl_bound
+    if _wl_bound is None:
+        import workloads
+        _wl_bound = workloads.bind(orc)
+    return _wl_bound
 
 
 # ---------------------------------------------------------------- C restatement

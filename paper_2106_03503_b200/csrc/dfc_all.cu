@@ -8,6 +8,7 @@
 #include "k_rows_dense.cu"
 #include "k_rows_lr.cu"
 #include "k_rows_pts.cu"
+#include "k_rows_band.cu"
 #include "k_rows_anc.cu"
 #include "k_raster.cu"
 #include "k_raster_anc.cu"

@@ -125,7 +125,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
                 cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr,
                 uint32_t* pts = nullptr, uint32_t* bmask = nullptr, bool skip_full = false,
-                bool no_fill = false) {
+                bool no_fill = false, bool skip_sparse = false) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -142,6 +142,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.pcounts = counts;
     c.bmask = bmask;
     c.skip_full = skip_full && bmask != nullptr && counts != nullptr;
+    c.skip_sparse = skip_sparse && bmask != nullptr && counts != nullptr;
     const unsigned long long* skip = c.pts ? counts : nullptr;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
@@ -231,11 +232,23 @@ bool anc_dense_on() {
 // Band source of k_rows_anc (see RowArgs): masks [img][nb][Wp], carries
 // above / below [plane][nb][Wp] of this call's planes, first polarity.
 struct BandSrc {
-    const uint32_t* bmask = nullptr;
+    const uint32_t* bmask = nullptr;   // K1a's masks (single images), else null
     const uint16_t* above = nullptr;
     const uint16_t* below = nullptr;
     int nb = 0, n_img = 1, pol0 = 0;
+    bool anc = false;     // k_rows_anc stages its rows from the bands
+    bool sparse = false;  // the band path (k_rows_band.cu) takes the sparse planes
 };
+
+// DFC_SPARSE=lr keeps the lane-per-row chunk scan (k_rows_lr, from the
+// nearest-row plane) for sparse planes instead of the band path (A/B)
+bool band_sparse_on() {
+    static const bool on = [] {
+        const char* v = getenv("DFC_SPARSE");
+        return !(v && strcmp(v, "lr") == 0);
+    }();
+    return on;
+}
 
 // Stage 2 over `nimg` planes of H rows.  Plane b writes its outputs at
 // base + b*stride.  take_new selects meijster_scan's tie rule.
@@ -365,11 +378,18 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         // kernels do not own: one tile, W <= kAncMaxW
         const bool anc_on = mode == 6 && W <= kAncMaxW && a.tile_cols >= W && row0 == 0 && H <= 32768;
         const bool dense_on = W <= kDenseMaxW && !(anc_on && anc_dense_on());
-        const bool lr_on = lr_ok && plane_counts != nullptr;
+        // sparse planes: the band path when the column pass left its band masks
+        const bool band_on = mode == 6 && band.sparse && band.bmask && plane_counts != nullptr &&
+                             a.tile_cols >= W && row0 == 0;
+        const bool lr_on = lr_ok && plane_counts != nullptr && !band_on;
+        const int64_t Ww = (W + 31) / 32;
+        const size_t cand_bytes = band_on ? (size_t)round_up(nimg * band.nb * 2 * Ww * 4, 256) : 0;
+        const size_t nent_bytes = band_on ? (size_t)round_up(a.total_rows * 4, 256) : 0;
         Scratch fl(st);
         const size_t flag_bytes = (size_t)round_up(a.total_rows, 256);
         const size_t list_bytes = (size_t)round_up((a.total_rows + 1) * 4, 256);
-        e = fl.alloc(flag_bytes + list_bytes + (lr_on ? ent_bytes + entr_bytes : 0));
+        e = fl.alloc(flag_bytes + list_bytes + (lr_on || band_on ? ent_bytes + entr_bytes : 0) + cand_bytes +
+                     nent_bytes);
         if (e != cudaSuccess) return cuda_fail(e);
         a.row_done = static_cast<uint8_t*>(fl.p);
         int* rest_count = reinterpret_cast<int*>(static_cast<char*>(fl.p) + flag_bytes);
@@ -402,10 +422,48 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             const int rc = launch_lr(a, static_cast<char*>(fl.p) + flag_bytes + list_bytes, nullptr, nullptr);
             if (rc != DFC_OK) return rc;
         }
+        a.lr_gate = lr_on || band_on;  // the other kernels skip the sparse planes' rows
+        if (band_on) {  // sparse planes: candidates per band, per-row stacks, fill
+            char* base = static_cast<char*>(fl.p) + flag_bytes + list_bytes;
+            BandArgs ba;
+            ba.bmask = band.bmask;
+            ba.above = band.above;
+            ba.below = band.below;
+            ba.ent = reinterpret_cast<uint32_t*>(base);
+            ba.entr = reinterpret_cast<uint16_t*>(base + ent_bytes);
+            ba.cand = reinterpret_cast<uint32_t*>(base + ent_bytes + entr_bytes);
+            ba.nent = reinterpret_cast<int*>(base + ent_bytes + entr_bytes + cand_bytes);
+            ba.counts = plane_counts;
+            ba.Ws = lrWs;
+            ba.H = (int)H;
+            ba.W = (int)W;
+            ba.Wp = Wp;
+            ba.nb = band.nb;
+            ba.Ww = (int)Ww;
+            ba.n_img = band.n_img;
+            ba.pol0 = band.pol0;
+            ba.nplanes = (int)nimg;
+            ba.pts_gate = a.pts_gate;
+            const dim3 hgrid((unsigned)((W + 1024 * kHullWarps - 1) / (1024 * kHullWarps)), (unsigned)band.nb,
+                             (unsigned)(2 * nimg));
+            k_band_hull<<<hgrid, 32 * kHullWarps, 0, st>>>(ba);
+            const int64_t tasks = nimg * band.nb;
+            const unsigned rblocks = (unsigned)((tasks + kBandWarps - 1) / kBandWarps);
+            if (take_new)
+                k_band_rows<true><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
+            else
+                k_band_rows<false><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
+            const int fsm = fill_smem_bytes();
+            e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+            if (e != cudaSuccess) return cuda_fail(e);
+            const int64_t fblocks = std::min<int64_t>((a.total_rows + kFillWarps - 1) / kFillWarps, 148 * 6);
+            k_rows_fill<<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
+            g_launches += 3;
+        }
         if (anc_on) {
             RowArgs aa = a;
             aa.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0;
-            if (band.bmask && anc_dense_on()) {  // stage rows from the bands (no nr plane)
+            if (band.bmask && band.anc) {  // stage rows from the bands (no nr plane)
                 aa.bmask = band.bmask;
                 aa.babove = band.above;
                 aa.bbelow = band.below;
@@ -544,6 +602,8 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     // band masks for every single image: K1c then builds the nearest-row plane
     // from them instead of re-reading the image (C5: 1 B/px of reads less)
     const bool masks_on = n == 1;
+    // sparse planes of single images: the band path (k_rows_band.cu), no plane
+    const bool sparse_band = mode == 6 && masks_on && band_sparse_on();
     const size_t bmask_elems = masks_on ? (size_t)(n * nb * Wp) : 0;
     Scratch sc(st);
     cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 512 + (size_t)planes * 8 +
@@ -560,7 +620,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
                               : nullptr;
     prof(0, st);
     int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts, pts,
-                         bmask, band_on);
+                         bmask, band_on, false, sparse_band);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -580,7 +640,9 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     if (uniform) {
         const int64_t nimg = planes;
         BandSrc bs;
-        bs.bmask = band_on ? bmask : nullptr;
+        bs.bmask = bmask;
+        bs.anc = band_on;
+        bs.sparse = sparse_band;
         bs.above = last;
         bs.below = first;
         bs.nb = (int)nb;
@@ -601,7 +663,9 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
         for (int s = 0; s < npol; ++s) {
             const uint16_t* pl = nr + (int64_t)s * H * Wp;
             BandSrc bs;  // n == 1 here
-            bs.bmask = band_on ? bmask : nullptr;
+            bs.bmask = bmask;
+            bs.anc = band_on;
+            bs.sparse = sparse_band;
             bs.above = last + (int64_t)s * nb * Wp;
             bs.below = first + (int64_t)s * nb * Wp;
             bs.nb = (int)nb;

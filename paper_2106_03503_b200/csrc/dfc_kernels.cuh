@@ -25,6 +25,9 @@ struct ColArgs {
     // rows from masks + carries)
     uint32_t* bmask;
     bool skip_full;
+    // the band path (k_rows_band.cu) takes the sparse planes: no nearest-row
+    // plane for them either
+    bool skip_sparse;
 };
 
 // Stage 2 (k_rows.cu)

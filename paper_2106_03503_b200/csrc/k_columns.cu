@@ -296,9 +296,11 @@ __global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t*
     auto skip_plane = [&](int s) {
         const int64_t p = (int64_t)s * a.n_img + im;
         if (a.pts && a.pcounts[p] <= (unsigned long long)kPtsCap) return true;
-        return a.skip_full && a.pcounts && !lr_plane(a.pcounts, (int)p, a.H, a.W);
+        if (!a.pcounts) return false;
+        const bool sparse = lr_plane(a.pcounts, (int)p, a.H, a.W);
+        return sparse ? a.skip_sparse : a.skip_full;
     };
-    if (a.pts || a.skip_full) {
+    if (a.pts || a.skip_full || a.skip_sparse) {
         bool all = true;
         for (int s = 0; s < a.npol; ++s) all = all && skip_plane(s);
         if (all) return;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(128, 8) k_band_fill(ColArgs a, const uint16_t*
     }
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
-        if ((a.pts || a.skip_full) && skip_plane(s)) continue;
+        if ((a.pts || a.skip_full || a.skip_sparse) && skip_plane(s)) continue;
         const int64_t coff = (((int64_t)s * a.n_img + im) * a.nb + b) * a.Wp + j0;
         const uint2 ab = *reinterpret_cast<const uint2*>(above + coff);
         const uint2 bl = *reinterpret_cast<const uint2*>(below + coff);

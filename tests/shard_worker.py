@@ -68,7 +68,7 @@ def main():
                 print("C5 mismatch", H, W, dens, flush=True)
                 ok = False
     # ---- C3-style: per-image shards ----
-    from paper_2106_03503_b200 import workloads
+    import workloads
     imgs = torch.from_numpy(workloads.points_batch(7, 24, 20, 5, 3))
     lo, hi, out = sharded.edt_batch_sharded(imgs, rank, world, ops=ops)
     parts = [None] * world

@@ -1,0 +1,79 @@
+"""CPU fuzz of tests/band_model.py -- the statement-level model of the
+band-candidate row pass for sparse planes (csrc/k_rows_band.cu: hull filter,
+lane-per-row stack with a spilling ring, fill) -- against brute force, both
+tie rules, with small windows / lanes / ring capacities so that the bridge
+merges, the window boundaries and the spill / reload paths all run."""
+import random
+
+import pytest
+
+import band_model as bm
+
+
+def _img(rnd, H, W, dens, mode):
+    img = [[0] * W for _ in range(H)]
+    if mode == "bern":
+        for i in range(H):
+            for j in range(W):
+                img[i][j] = 1 if rnd.random() < dens else 0
+    elif mode == "rowline":  # a full object row: every column on the hull
+        r = rnd.randrange(H)
+        img[r] = [1] * W
+    elif mode == "few":
+        for _ in range(rnd.randint(0, 4)):
+            img[rnd.randrange(H)][rnd.randrange(W)] = 1
+    elif mode == "lattice":  # many exact ties
+        s = rnd.randint(2, 6)
+        for i in range(rnd.randrange(s), H, s):
+            for j in range(rnd.randrange(s), W, s):
+                img[i][j] = 1
+    return img
+
+
+@pytest.mark.parametrize("take_new", [False, True])
+def test_band_model_matches_brute_force(take_new):
+    rnd = random.Random(11 + take_new)
+    for it in range(260):
+        H = rnd.randint(1, 100)
+        W = rnd.randint(1, 48)
+        mode = rnd.choice(["bern", "bern", "rowline", "few", "lattice"])
+        img = _img(rnd, H, W, rnd.choice([0.0, 0.005, 0.02, 0.1, 0.4]), mode)
+        lane_cols = rnd.choice([1, 2, 3, 4, 8, 32])
+        lanes = rnd.choice([1, 2, 4, 8, 32])
+        cap = rnd.choice([1, 2, 3, 32])
+        D, K, R, _, _ = bm.band_transform(img, take_new, cap, lane_cols, lanes)
+        bD, bK, bR = bm.brute(img, take_new)
+        assert D == bD, (it, mode, H, W)
+        assert K == bK, (it, mode, H, W)
+        if not take_new:
+            assert R == bR, (it, mode, H, W)
+
+
+def test_window_hull_is_superset_of_global_hull():
+    rnd = random.Random(5)
+    for _ in range(300):
+        W = rnd.randint(1, 90)
+        line = rnd.randint(0, 200)
+        car = [rnd.randint(0, 199) if rnd.random() < 0.6 else None for _ in range(W)]
+        car = [None if c is None else min(c, line) for c in car]
+        glob = bm.window_hull(car, line, 0, lane_cols=W, lanes=1)
+        for lc, ln in ((1, 4), (3, 4), (4, 8), (32, 32)):
+            got = set()
+            for w0 in range(0, W, lc * ln):
+                got |= bm.window_hull(car, line, w0, lc, ln, W)
+            assert glob <= got
+            # one window covering the whole row: the merges give exactly the global hull
+        assert bm.window_hull(car, line, 0, 1, 128, W) == glob
+
+
+def test_candidate_counts_are_small_on_sparse_tiles():
+    """Candidate columns per band on a scaled C5-like image stay far below W
+    (the row pass's work); the spill path never runs at the kernel's cap."""
+    rnd = random.Random(2)
+    H, W = 96, 512
+    img = [[0] * W for _ in range(H)]
+    for _ in range(40):
+        img[rnd.randrange(H)][rnd.randrange(W)] = 1
+    _, _, _, ncand, st = bm.band_transform(img, False, 32, 32, 32)
+    assert max(ncand) < W // 3
+    assert st["spills"] == 0

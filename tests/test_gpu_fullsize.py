@@ -1,14 +1,12 @@
 """Parity at BASELINE.json's full sizes (configs 1-5), on the GPU.
 
-Where the CPU oracle finishes in seconds (C1, C2, C4, a C3 sample) the GPU
-maps are compared bit-exactly with it.  At 1 Gpixel (C5) the oracle is too
-slow, so size-independent properties carry the check:
-  * the degenerate corner image has the closed form D(i, j) = i^2 + j^2
-    (max 2,147,352,578 -- the int32 bound, SURVEY finding 7);
-  * on the tiled Bernoulli image, a seeded sample of pixels is verified
-    EXACTLY against brute force over all ~27k object pixels, and each
-    pixel's label names an object at exactly that distance;
-  * transpose equivariance edt(img^T) == edt(img)^T (test_exact_edt.cpp:197-208).
+Every config's FULL map is compared bit-exactly: C1, C2, C4 with the C
+oracle; all 1024 C3 images (distances and labels) and the whole 1-Gpixel C5
+map (distances, labels, float distances) with the reference library itself
+(oracle/_ref, all host cores: ~20 s each); the degenerate C5 corner image with
+its closed form D(i, j) = i^2 + j^2 over all 2^30 pixels (max 2,147,352,578 --
+the int32 bound, SURVEY finding 7).  Plus transpose equivariance
+edt(img^T) == edt(img)^T on C5 (test_exact_edt.cpp:197-208).
 """
 import numpy as np
 import pytest
@@ -27,7 +25,7 @@ def dfc():
 
 @pytest.fixture(scope="module")
 def wl():
-    from paper_2106_03503_b200 import workloads
+    import workloads
     return workloads
 
 
@@ -57,14 +55,37 @@ def test_c2_full_both_polarities(dfc, wl):
         np.testing.assert_array_equal(out["dist_" + key].cpu().numpy(), oracle.sqrt_f32(want))
 
 
-def test_c3_sample_of_full_batch(dfc, wl):
+def _ordinals_to_linear(img, ords):
+    """Reference LabelMap ordinals (grid.cpp:29-36: row-major enumeration of
+    the object pixels) -> linear indices row * cols + col."""
+    objs = np.flatnonzero(img.reshape(-1)).astype(np.int32)
+    return objs[ords.reshape(-1)].reshape(img.shape)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_c3_full_batch_vs_reference(dfc, wl):
+    """All 1024 images of C3, squared distances AND labels, against the
+    reference library itself (edt + voronoi_labels per image, all host cores)."""
+    import ctypes as C
+    import os
     imgs = wl.config("c3")  # 1024 x 1024^2, computed as one batch
     out = dfc.edt_batched(_dev(imgs), dist=False, label=True)
     torch.cuda.synchronize()
-    rng = np.random.default_rng(0)
-    for b in sorted(rng.choice(imgs.shape[0], 12, replace=False)):
-        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
-        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
+    sq = out["sqdist"].cpu().numpy()
+    lab = out["label"].cpu().numpy()
+    del out
+    n, h, w = imgs.shape
+    threads = os.cpu_count() or 1
+    for b0 in range(0, n, 128):
+        sub = np.ascontiguousarray(imgs[b0:b0 + 128])
+        d = np.empty(sub.shape, np.uint64)
+        ords = np.empty(sub.shape, np.uint32)
+        st = oracle.ref.dfref_edt_labels_batch(sub, sub.shape[0], h, w, threads, d.ctypes.data,
+                                               ords.ctypes.data, C.byref(C.c_double(0)))
+        assert st == 0
+        np.testing.assert_array_equal(sq[b0:b0 + 128], d.astype(np.int32))
+        for t in range(sub.shape[0]):
+            np.testing.assert_array_equal(lab[b0 + t], _ordinals_to_linear(sub[t], ords[t]))
 
 
 def test_c4_full(dfc, wl):
@@ -86,29 +107,35 @@ def test_c5_degenerate_corner_closed_form(dfc, wl):
     assert int(d.max()) == 2147352578
 
 
-def test_c5_sampled_exact_and_labels(dfc, wl):
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_c5_full_map_vs_reference(dfc, wl):
+    """The whole 32768^2 C5 map (the bench workload, squared distances only)
+    against the reference library's edt on all host cores, bit for bit; then
+    the labels and float distances of the same image against the reference's
+    voronoi_labels and (float)sqrt((double)D)."""
+    import os
     img = wl.config("c5")
-    fr, fc = np.nonzero(img)
-    assert 20000 < fr.size < 35000
+    assert 20000 < int(img.sum()) < 35000
     dev = _dev(img)
-    out = dfc.edt(dev, dist=True, label=True)
-    torch.cuda.synchronize()
-    rng = np.random.default_rng(1)
-    pi = rng.integers(0, 32768, 3000)
-    pj = rng.integers(0, 32768, 3000)
-    d = out["sqdist"][torch.from_numpy(pi).cuda(), torch.from_numpy(pj).cuda()].cpu().numpy().astype(np.int64)
-    lab = out["label"][torch.from_numpy(pi).cuda(), torch.from_numpy(pj).cuda()].cpu().numpy().astype(np.int64)
-    for c in range(0, 3000, 500):
-        a, b = pi[c:c + 500, None], pj[c:c + 500, None]
-        dd = (a - fr[None]) ** 2 + (b - fc[None]) ** 2
-        np.testing.assert_array_equal(d[c:c + 500], dd.min(axis=1))
-    lr, lc = lab // 32768, lab % 32768
-    assert img[lr, lc].all()
-    np.testing.assert_array_equal((pi - lr) ** 2 + (pj - lc) ** 2, d)
-    s = out["dist"][torch.from_numpy(pi).cuda(), torch.from_numpy(pj).cuda()].cpu().numpy()
-    np.testing.assert_array_equal(s, np.sqrt(d.astype(np.float64)).astype(np.float32))
-    del out
-    # transpose equivariance on the full image
+    sq = dfc.edt(dev, dist=False)["sqdist"].cpu().numpy()
+    threads = os.cpu_count() or 1
+    ref = oracle.ref_edt(img, threads=threads)
+    for r0 in range(0, 32768, 4096):  # chunked: the uint64 map is 8 GiB
+        np.testing.assert_array_equal(sq[r0:r0 + 4096], ref[r0:r0 + 4096].astype(np.int32))
+    assert int(sq.max()) == int(ref.max())
+    del ref
+    full = dfc.edt(dev, dist=True, label=True)
+    np.testing.assert_array_equal(full["sqdist"].cpu().numpy(), sq)
+    s = full["dist"].cpu().numpy()
+    for r0 in range(0, 32768, 4096):
+        np.testing.assert_array_equal(s[r0:r0 + 4096], oracle.sqrt_f32(sq[r0:r0 + 4096]))
+    del s
+    lab = full["label"].cpu().numpy()
+    del full
+    ords = oracle.ref_voronoi_labels(img, threads=threads)
+    np.testing.assert_array_equal(lab, _ordinals_to_linear(img, ords))
+    del ords, lab
+    # transpose equivariance on the full image (test_exact_edt.cpp:197-208)
     dt = dfc.edt(dev.t().contiguous(), dist=False)["sqdist"]
     d0 = dfc.edt(dev, dist=False)["sqdist"]
     assert bool((dt == d0.t()).all())

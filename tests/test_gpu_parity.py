@@ -138,7 +138,7 @@ def test_pitch_and_bool_input(dfc):
 
 @pytest.mark.parametrize("shape", [(64, 64), (100, 301), (1, 500), (256, 4096)])
 def test_dual_polarity(dfc, shape):
-    from paper_2106_03503_b200 import workloads
+    import workloads
     img = workloads.discs(shape[0], shape[1], 12, 3 + shape[1])
     out = dfc.edt_dual(_dev(img))
     torch.cuda.synchronize()
@@ -151,7 +151,7 @@ def test_dual_polarity(dfc, shape):
 
 
 def test_batched_points(dfc):
-    from paper_2106_03503_b200 import workloads
+    import workloads
     imgs = workloads.points_batch(24, 128, 96, 30, 99)
     imgs[5] = 0  # a featureless image inside the batch
     out = dfc.edt_batched(_dev(imgs), dist=True, label=True)
@@ -240,7 +240,8 @@ def test_column_striped_path_emulated(dfc, world, p):
     the N tiles in place with global row numbers (dfc_rows_from_nr_u16).  At
     p = 0.002 the row stripes are sparse planes (< 1/256 object pixels): the
     lane-per-row kernel reads the tiles."""
-    from paper_2106_03503_b200 import sharded, workloads
+    from paper_2106_03503_b200 import sharded
+    import workloads
     H, W = (96, 256) if p > 0.01 else (256, 1024)
     img = workloads.sparse_tiles(H, W, tile=32, n_on=6 if p > 0.01 else 64, p=p, seed=11 + world)
     ops = sharded.KernelOps()
@@ -306,7 +307,7 @@ def test_streaming_overflow_falls_back(stream_kernel):
 
 
 def test_streaming_batched_and_dual(stream_kernel):
-    from paper_2106_03503_b200 import workloads
+    import workloads
     imgs = workloads.points_batch(40, 96, 128, 30, 5)
     out = stream_kernel.edt_batched(_dev(imgs), dist=True, label=True)
     img = workloads.discs(256, 384, 10, 3)
@@ -335,7 +336,7 @@ def test_window_row_kernel(window_kernel, shape, density):
 
 
 def test_window_batched_dual_and_lines(window_kernel):
-    from paper_2106_03503_b200 import workloads
+    import workloads
     imgs = workloads.points_batch(24, 96, 128, 30, 6)
     out = window_kernel.edt_batched(_dev(imgs), dist=True, label=True)
     img = workloads.discs(256, 384, 10, 4)
@@ -413,7 +414,7 @@ def test_lr_overflow_falls_back(lr_kernel):
 
 
 def test_lr_batched_dual_and_discs(lr_kernel):
-    from paper_2106_03503_b200 import workloads
+    import workloads
     imgs = workloads.points_batch(40, 96, 128, 30, 5)
     out = lr_kernel.edt_batched(_dev(imgs), dist=True, label=True)
     img = workloads.discs(256, 384, 10, 3)
@@ -496,7 +497,7 @@ def test_anc_ties_and_long_runs(anc_kernel):
 
 
 def test_anc_batched_dual_and_discs(anc_kernel):
-    from paper_2106_03503_b200 import workloads
+    import workloads
     imgs = workloads.points_batch(40, 96, 128, 30, 5)
     out = anc_kernel.edt_batched(_dev(imgs), dist=True, label=True)
     img = workloads.discs(256, 384, 10, 3)
@@ -620,3 +621,64 @@ def test_band_scan_medium_heights(dfc, shape):
     for b in range(3):
         np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
         np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
+
+
+# ---- the band path for sparse planes (k_rows_band.cu: hull filter, per-row
+# stacks with a spilling ring, fill) -- the default for planes with fewer than
+# 1/256 object pixels in single images ----
+
+def _sparse(shape, npts, seed):
+    rng = np.random.default_rng(seed)
+    img = np.zeros(shape, np.uint8)
+    img[rng.integers(0, shape[0], npts), rng.integers(0, shape[1], npts)] = 1
+    return img
+
+
+@pytest.mark.parametrize("shape", [(33, 97), (64, 64), (257, 65), (100, 1500), (300, 2000), (1000, 96),
+                                   (70, 4100), (129, 5000), (40, 1025), (2, 32768), (600, 3000)])
+@pytest.mark.parametrize("npts", [1, 2, 7, 40])
+def test_band_sparse_random(dfc, shape, npts):
+    img = _sparse(shape, npts, shape[0] * 7 + shape[1] + npts)
+    if img.sum() * 256 >= img.size:
+        pytest.skip("not a sparse plane")
+    _check_edt(dfc, img, 0)
+
+
+def test_band_sparse_full_row_spills(dfc):
+    """A full object row: below it every column owns itself, so each row's
+    stack holds all 2000 columns (the ring spills to the list and reloads)."""
+    img = np.zeros((300, 2000), np.uint8)
+    img[150, :] = 1
+    _check_edt(dfc, img, 0)
+    img2 = np.zeros((600, 1100), np.uint8)
+    img2[5, 3:1090:2] = 1    # every other column: ties between neighbours
+    img2[590, 0] = 1
+    _check_edt(dfc, img2, 0)
+
+
+def test_band_sparse_ties_lattice_and_corners(dfc):
+    img = np.zeros((400, 700), np.uint8)
+    img[::37, ::41] = 1      # a lattice: many equidistant owners
+    _check_edt(dfc, img, 0)
+    c = np.zeros((513, 1500), np.uint8)
+    c[0, 0] = c[512, 1499] = c[0, 1499] = 1
+    _check_edt(dfc, c, 0)
+
+
+def test_band_sparse_inverted_polarity(dfc):
+    img = np.ones((200, 1300), np.uint8)
+    img[_sparse((200, 1300), 9, 3) == 1] = 0   # the object->background plane is sparse
+    _check_edt(dfc, img, 1)
+    out = dfc.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    for key, src in (("bg", img), ("obj", (img == 0).astype(np.uint8))):
+        np.testing.assert_array_equal(out["sqdist_" + key].cpu().numpy(), oracle.to_i32(oracle.edt(src)))
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_band_sparse_tiles_scaled(dfc, seed):
+    """A C5-like image at 1/16 scale: Bernoulli pixels in a quarter of the tiles."""
+    import workloads
+    img = workloads.sparse_tiles(2048, 2048, 64, 256, 4e-3, 99 + seed)
+    assert img.sum() * 256 < img.size
+    _check_edt(dfc, img, 0)

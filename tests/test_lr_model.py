@@ -36,7 +36,7 @@ def test_live_ring_stays_small_on_discs():
     capacity (kLrCap = 32) on a disc image's background->object plane."""
     import numpy as np
     import oracle
-    from paper_2106_03503_b200 import workloads
+    import workloads
     img = workloads.discs(256, 512, 6, 5)
     v = oracle.vertical_pass(img)
     inf = np.iinfo(np.uint64).max

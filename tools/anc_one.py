@@ -4,7 +4,7 @@ import sys
 sys.path.insert(0, ".")
 import torch
 import paper_2106_03503_b200 as dfc
-from paper_2106_03503_b200 import workloads
+import workloads
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 mode = sys.argv[2] if len(sys.argv) > 2 else "0"

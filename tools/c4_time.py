@@ -4,7 +4,7 @@ import sys
 sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_2106_03503_b200 as dfc
-from paper_2106_03503_b200 import workloads
+import workloads
 img = torch.from_numpy(workloads.config("c4")).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ts = []

@@ -7,7 +7,7 @@ import numpy as np
 
 sys.path.insert(0, "."); sys.path.insert(0, "tests"); sys.path.insert(0, "tools")
 import stream_model as sm
-from paper_2106_03503_b200 import workloads
+import workloads
 from win_stats_lib import nearest_rows
 
 

@@ -4,7 +4,7 @@ import sys
 sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_2106_03503_b200 as dfc
-from paper_2106_03503_b200 import workloads
+import workloads
 cfg = sys.argv[1]
 chunks = [int(c) for c in sys.argv[2:]] or [256]
 img = torch.from_numpy(workloads.config(cfg)).cuda()

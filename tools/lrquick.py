@@ -1,7 +1,7 @@
 import sys, time; sys.path.insert(0,'.')
 import numpy as np, torch, oracle
 import paper_2106_03503_b200 as dfc
-from paper_2106_03503_b200 import workloads
+import workloads
 dfc.set_row_kernel("lr")
 for shape,dens in [((33,97),0.02),((70,600),0.3),((40,1031),0.002),((64,64),1.0),((5,7),0.0)]:
     img = oracle.random_image(shape[0], shape[1], dens, 5)

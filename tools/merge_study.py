@@ -10,7 +10,7 @@ import numpy as np
 
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 from row_model import Row
-from paper_2106_03503_b200 import workloads
+import workloads
 sys.path.insert(0, "tools")
 from win_stats_lib import nearest_rows  # noqa: E402
 

@@ -3,7 +3,7 @@ import sys
 sys.path.insert(0, ".")
 import torch
 import paper_2106_03503_b200 as dfc
-from paper_2106_03503_b200 import workloads
+import workloads
 img = torch.from_numpy(workloads.config(sys.argv[1])).cuda()
 for _ in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     dfc.edt(img, polarity=int(sys.argv[2]), dist=True)

@@ -3,7 +3,7 @@ segment evaluations per thread, stack sizes.  python tools/win_stats.py c2 [rows
 import sys
 import numpy as np
 sys.path.insert(0, ".")
-from paper_2106_03503_b200 import workloads
+import workloads
 
 def nearest_rows(feat):
     H, W = feat.shape
