@@ -210,6 +210,52 @@ int dfc_labels_gray(const uint32_t* d_ordinal, int64_t n, int64_t feature_count,
                     dfc_stream_t stream);
 
 /*
+ * ONE image over `world` GPUs (config 5): column stripes
+ * for the column pass, an all-to-all of the compact column-pass products
+ * (per band of 32 rows and column: the 32-bit object mask and the nearest
+ * object rows above / below the band -- 8 B per 32 pixels), row stripes for
+ * the row pass.  Replaces the `parallel_for` fan-out of edt
+ * (exact_edt.cpp:53-154, parallel.hpp:13-30) across devices; the result is
+ * bit-identical to dfc_edt_u8 on the whole image.
+ *
+ * Rank r owns columns [dfc_shard_cols(cols, world, r)) of the input and rows
+ * [dfc_shard_rows(rows, world, r)) of the output (row stripes are whole bands
+ * of 32 rows).  Each dfc_shard describes one LOCAL rank; n_local may be 1
+ * (one process per GPU: comm from dfc_comm_init_rank) up to world (one process
+ * driving every GPU: comms from dfc_comm_init_all, or all comm NULL -- then
+ * the exchange is stream-ordered peer copies inside this process, and every
+ * rank must be local).  The exchange is NCCL grouped send/recv on each shard's
+ * stream; NCCL (libnccl.so.2) is opened at the first call that needs it.
+ * Returns DFC_ERR_NCCL (see dfc_last_nccl_error) when it is unavailable.
+ */
+typedef struct dfc_shard {
+    int device;              /* CUDA device of this rank                          */
+    int rank;                /* 0 .. world-1                                      */
+    const uint8_t* d_img;    /* its column stripe: rows x ncols, row pitch below  */
+    int64_t pitch_bytes;
+    int32_t* d_sqdist;       /* its row stripe of the result: nrows x cols         */
+    float* d_dist;           /* optional float distances of the row stripe          */
+    int32_t* d_label;        /* optional labels (global linear index, keep_old)    */
+    void* comm;              /* ncclComm_t, or NULL (in-process exchange)          */
+    dfc_stream_t stream;
+} dfc_shard;
+
+int dfc_edt_u8_sharded(const dfc_shard* shards, int n_local, int world, int64_t rows, int64_t cols,
+                       int polarity);
+/* The partition: column stripe and row stripe of `rank`. */
+int dfc_shard_cols(int64_t cols, int world, int rank, int64_t* col0, int64_t* ncols);
+int dfc_shard_rows(int64_t rows, int world, int rank, int64_t* row0, int64_t* nrows);
+/* Communicators: a 128-byte NCCL unique id (rank 0 makes it, the caller
+ * broadcasts it), one rank's communicator on the CURRENT device, or one per
+ * listed device for a single process; opaque ncclComm_t handles. */
+int dfc_comm_unique_id(uint8_t* id128);
+int dfc_comm_init_rank(void** comm, int world, int rank, const uint8_t* id128);
+int dfc_comm_init_all(void** comms, int ndev, const int* devices);
+int dfc_comm_destroy(void* comm);
+/* The ncclResult_t behind the last DFC_ERR_NCCL on this thread. */
+int dfc_last_nccl_error(void);
+
+/*
  * Measurement hook (bench.py): cudaEvent_t handles recorded on the call's
  * stream by the next dfc_edt_u8* calls on this thread -- ev_col_begin before
  * the column pass, ev_row_begin between column and row pass, ev_row_end

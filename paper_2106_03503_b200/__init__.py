@@ -62,12 +62,30 @@ _lib.dfc_count_objects_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp]
 _lib.dfc_gray_i32.argtypes = [_vp, _i64, C.c_int, _vp, _vp, _vp, _vp]
 _lib.dfc_labels_gray.argtypes = [_vp, _i64, _i64, _vp, _vp]
 
+
+class Shard(C.Structure):
+    """struct dfc_shard (include/distfield_cuda.h): one local rank of dfc_edt_u8_sharded."""
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("d_img", _vp), ("pitch_bytes", _i64),
+                ("d_sqdist", _vp), ("d_dist", _vp), ("d_label", _vp), ("comm", _vp), ("stream", _vp)]
+
+
+_lib.dfc_edt_u8_sharded.argtypes = [C.POINTER(Shard), C.c_int, C.c_int, _i64, _i64, C.c_int]
+_lib.dfc_shard_cols.argtypes = [_i64, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_i64)]
+_lib.dfc_shard_rows.argtypes = [_i64, C.c_int, C.c_int, C.POINTER(_i64), C.POINTER(_i64)]
+_lib.dfc_comm_unique_id.argtypes = [C.c_char_p]
+_lib.dfc_comm_init_rank.argtypes = [C.POINTER(_vp), C.c_int, C.c_int, C.c_char_p]
+_lib.dfc_comm_init_all.argtypes = [C.POINTER(_vp), C.c_int, C.POINTER(C.c_int)]
+_lib.dfc_comm_destroy.argtypes = [_vp]
+_lib.dfc_last_nccl_error.restype = C.c_int
+
 EXPORTED_SYMBOLS = (
     "dfc_edt_u8", "dfc_edt_u8_dual", "dfc_edt_u8_batched", "dfc_vertical_u8", "dfc_raster_u8",
     "dfc_vertical_down_pass_u64", "dfc_vertical_up_pass_u64",
     "dfc_label_ordinals", "dfc_last_launch_count", "dfc_status_string", "dfc_last_cuda_error",
     "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel", "dfc_set_lr_chunk",
     "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
+    "dfc_edt_u8_sharded", "dfc_shard_cols", "dfc_shard_rows", "dfc_comm_unique_id", "dfc_comm_init_rank",
+    "dfc_comm_init_all", "dfc_comm_destroy", "dfc_last_nccl_error",
 )
 
 
@@ -76,6 +94,8 @@ class DfcError(RuntimeError):
         msg = _lib.dfc_status_string(status).decode()
         if status == 3:
             msg += f" (cudaError {_lib.dfc_last_cuda_error()})"
+        if status == 4:
+            msg += f" (ncclResult {_lib.dfc_last_nccl_error()})"
         super().__init__(msg)
         self.status = status
 
@@ -354,6 +374,59 @@ def label_ordinals(img: torch.Tensor, label: torch.Tensor, stream=None) -> torch
     _check(_lib.dfc_label_ordinals(_ptr(img), h, w, pitch, _ptr(label.contiguous()), _ptr(out),
                                    _stream(stream)))
     return out.to(torch.int64) & 0xFFFFFFFF
+
+
+# ---------------------------------------------------------- multi-GPU (config 5)
+def shard_cols(cols: int, world: int, rank: int):
+    """[col0, col0 + ncols): the column stripe rank `rank` holds (dfc_shard_cols)."""
+    a, b = _i64(), _i64()
+    _check(_lib.dfc_shard_cols(cols, world, rank, C.byref(a), C.byref(b)))
+    return a.value, a.value + b.value
+
+
+def shard_rows(rows: int, world: int, rank: int):
+    """[row0, row1): the row stripe of the result rank `rank` gets (whole 32-row bands)."""
+    a, b = _i64(), _i64()
+    _check(_lib.dfc_shard_rows(rows, world, rank, C.byref(a), C.byref(b)))
+    return a.value, a.value + b.value
+
+
+def comm_unique_id() -> bytes:
+    """A 128-byte NCCL unique id (rank 0 makes it; the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.dfc_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init_rank(world: int, rank: int, uid: bytes) -> int:
+    """This rank's NCCL communicator on the current CUDA device (opaque handle)."""
+    h = _vp()
+    _check(_lib.dfc_comm_init_rank(C.byref(h), world, rank, uid))
+    return h.value
+
+
+def comm_destroy(handle: int) -> None:
+    _check(_lib.dfc_comm_destroy(handle))
+
+
+def edt_sharded(shards, world: int, rows: int, cols: int, polarity: int = 0) -> None:
+    """dfc_edt_u8_sharded over local ranks.  `shards`: dicts with keys rank,
+    img (CUDA uint8 [rows, ncols] column stripe), sqdist (CUDA int32 [nrows, cols]
+    row stripe), optional dist / label, comm (handle or None), stream."""
+    arr = (Shard * len(shards))()
+    for s, d in zip(arr, shards):
+        img, _, _, pitch = _img2d(d["img"])
+        s.device = img.device.index
+        s.rank = d["rank"]
+        s.d_img = img.data_ptr()
+        s.pitch_bytes = pitch
+        s.d_sqdist = d["sqdist"].data_ptr()
+        s.d_dist = d["dist"].data_ptr() if d.get("dist") is not None else None
+        s.d_label = d["label"].data_ptr() if d.get("label") is not None else None
+        s.comm = d.get("comm")
+        st = d.get("stream") or torch.cuda.current_stream(img.device)
+        s.stream = st.cuda_stream
+    _check(_lib.dfc_edt_u8_sharded(arr, len(shards), world, rows, cols, polarity))
 
 
 from . import distfield  # noqa: E402,F401  (reference-shaped host API)

@@ -14,3 +14,4 @@
 #include "k_raster_anc.cu"
 #include "k_render.cu"
 #include "dfc_api.cu"
+#include "dfc_shard.cu"

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "dfc_kernels.cuh"
 
@@ -59,19 +60,21 @@ bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a)
 
 int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// Keep freed scratch in the pool: after the first call no cudaMalloc happens.
+// Keep freed scratch in the pool: after the first call on a device no
+// cudaMalloc happens.  Once per device, thread-safe (a single process may
+// drive several GPUs, dfc_edt_u8_sharded).
 void init_pool_once() {
-    static bool done = false;
-    if (done) return;
+    constexpr int kMaxDev = 64;
+    static std::once_flag flags[kMaxDev];
     int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) {
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return;
+    std::call_once(flags[dev], [dev] {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-    }
-    done = true;
+    });
 }
 
 struct Scratch {
@@ -248,6 +251,28 @@ bool band_sparse_on() {
         return !(v && strcmp(v, "lr") == 0);
     }();
     return on;
+}
+
+// The band path (k_rows_band.cu) over the sparse planes of `ba`: hull filter,
+// per-row stacks, fill into a's outputs.
+int launch_band_path(const RowArgs& a, const BandArgs& ba, bool take_new, cudaStream_t st) {
+    const dim3 hgrid((unsigned)((ba.W + 1024 * kHullWarps - 1) / (1024 * kHullWarps)), (unsigned)ba.nb,
+                     (unsigned)(2 * ba.nplanes));
+    k_band_hull<<<hgrid, 32 * kHullWarps, 0, st>>>(ba);
+    const int64_t tasks = (int64_t)ba.nplanes * ba.nb;
+    const unsigned rblocks = (unsigned)((tasks + kBandWarps - 1) / kBandWarps);
+    if (take_new)
+        k_band_rows<true><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
+    else
+        k_band_rows<false><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
+    const int fsm = fill_smem_bytes();
+    cudaError_t e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int64_t rows = (int64_t)ba.nplanes * ba.H;
+    const int64_t fblocks = std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * 6);
+    k_rows_fill<<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
+    g_launches += 3;
+    return DFC_OK;
 }
 
 // Stage 2 over `nimg` planes of H rows.  Plane b writes its outputs at
@@ -443,22 +468,12 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             ba.n_img = band.n_img;
             ba.pol0 = band.pol0;
             ba.nplanes = (int)nimg;
+            ba.band0 = 0;
+            ba.Hg = (int)H;
             ba.pts_gate = a.pts_gate;
-            const dim3 hgrid((unsigned)((W + 1024 * kHullWarps - 1) / (1024 * kHullWarps)), (unsigned)band.nb,
-                             (unsigned)(2 * nimg));
-            k_band_hull<<<hgrid, 32 * kHullWarps, 0, st>>>(ba);
-            const int64_t tasks = nimg * band.nb;
-            const unsigned rblocks = (unsigned)((tasks + kBandWarps - 1) / kBandWarps);
-            if (take_new)
-                k_band_rows<true><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
-            else
-                k_band_rows<false><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
-            const int fsm = fill_smem_bytes();
-            e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
-            if (e != cudaSuccess) return cuda_fail(e);
-            const int64_t fblocks = std::min<int64_t>((a.total_rows + kFillWarps - 1) / kFillWarps, 148 * 6);
-            k_rows_fill<<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
-            g_launches += 3;
+            ba.all_planes = false;
+            const int rc = launch_band_path(a, ba, take_new, st);
+            if (rc != DFC_OK) return rc;
         }
         if (anc_on) {
             RowArgs aa = a;

@@ -63,12 +63,17 @@ struct BandArgs {
     int* nent;               // entries per row
     int64_t Ws;              // list stride per row (entries)
     int H, W, Wp, nb, Ww, n_img, pol0, nplanes;
+    // row stripes (the sharded path): local band b is global band band0 + b of
+    // an image of Hg rows; plane p's local rows are [0, H).  Single images:
+    // band0 = 0, Hg = H.
+    int band0, Hg;
     bool pts_gate;           // point planes belong to k_rows_pts
+    bool all_planes;         // every plane (the sharded path), not only the sparse ones
 };
 
 // The planes this path owns: sparse, not a point plane.
 __device__ __forceinline__ bool band_plane(const BandArgs& a, int p) {
-    return lr_plane(a.counts, p, a.H, a.W) && !pts_plane(a.counts, p, a.pts_gate);
+    return a.all_planes || (lr_plane(a.counts, p, a.Hg, a.W) && !pts_plane(a.counts, p, a.pts_gate));
 }
 
 // ---------------------------------------------------------------- hull filter
@@ -83,7 +88,8 @@ __global__ void __launch_bounds__(32 * kHullWarps) k_band_hull(BandArgs a) {
     if (win * 1024 >= a.W) return;                 // warp-uniform
     if (!band_plane(a, p)) return;                 // CTA-uniform
     const int w0 = win * 1024, c0 = w0 + 32 * lane;
-    const int line = side ? min(32 * b + 31, a.H - 1) : 32 * b;
+    const int gb = a.band0 + b;  // global band
+    const int line = side ? min(32 * gb + 31, a.Hg - 1) : 32 * gb;
     uint32_t (&D)[32][33] = dsm[warp];
 
     // ---- the lane's 32 carries -> distance to the line (kHullNone: none) ----
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(32 * kHullWarps) k_band_hull(BandArgs a) {
     if (side == 0) {
         const int s = p / a.n_img, im = p - s * a.n_img;
         const int pol = a.pol0 + s;
-        const int nrows = min(32, a.H - 32 * b);
+        const int nrows = min(32, a.Hg - 32 * gb);
         const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
         const uint32_t* mrow = a.bmask + ((int64_t)im * a.nb + b) * a.Wp;
         uint32_t z = 0;
@@ -251,12 +257,13 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
     if (!band_plane(a, p)) return;  // warp-uniform
     const int s = p / a.n_img, im = p - s * a.n_img;
     const int pol = a.pol0 + s;
-    const int nrows = min(32, a.H - 32 * b);
+    const int gb = a.band0 + b;  // global band; rows of the image [32 gb, 32 gb + nrows)
+    const int nrows = min(32, a.Hg - 32 * gb);
     const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
     const bool active = lane < nrows;
-    const uint32_t i = (uint32_t)(32 * b + lane);
+    const uint32_t i = (uint32_t)(32 * gb + lane);  // global row
     const uint32_t upmask = 0xffffffffu >> (31 - lane);
-    const int64_t row = (int64_t)p * a.H + i;
+    const int64_t row = (int64_t)p * a.H + 32 * b + lane;  // local row
     uint32_t* gE = a.ent + (active ? row * a.Ws : 0);
     uint16_t* gR = a.entr + (active ? row * a.Ws : 0);
     const uint32_t* cA = a.cand + ((int64_t)p * a.nb + b) * 2 * a.Ww;
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
                 const uint32_t c2 = __shfl_sync(FULL, cc, u);
                 if (!active) continue;
                 const uint32_t up = mk & upmask, dn = mk >> lane;
-                const uint32_t ra = up ? (uint32_t)(32 * b + 31 - __clz(up)) : (c2 & 0xffffu);
+                const uint32_t ra = up ? (uint32_t)(32 * gb + 31 - __clz(up)) : (c2 & 0xffffu);
                 const uint32_t rb = dn ? (uint32_t)(i + __ffs(dn) - 1) : (c2 >> 16);
                 const uint32_t r = pick_nearest(i, ra, rb);
                 if (r != kNoRow) cand(m, r);
@@ -404,7 +411,7 @@ __global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandA
         const int p = (int)(row / a.H);
         if (!band_plane(a, p)) continue;  // warp-uniform
         const int64_t iR = row - (int64_t)p * a.H;
-        const uint32_t gi = (uint32_t)iR;
+        const uint32_t gi = (uint32_t)(iR + 32 * a.band0);  // global row
         const int nE = __ldcg(a.nent + row);
         const uint32_t* gE = a.ent + row * a.Ws;
         const uint16_t* gR = a.entr + row * a.Ws;

@@ -5,17 +5,25 @@ One process per GPU (torchrun), ``torch.distributed`` for the plumbing.
 * C3 (a batch of independent images): rank r owns images
   [r*n/N, (r+1)*n/N); no data-path collective.
 * C5 (one giant image, north_star): rank r owns the column stripe
-  [r*W/N, (r+1)*W/N).  Stage 1 (per-column nearest-object scan) is exact on a
-  stripe because columns are independent.  The uint16 nearest-row plane of the
-  stripe is row-major, so the block destined for rank q -- rows
-  [q*H/N, (q+1)*H/N) -- is contiguous: ONE all-to-all over the raw bytes
-  (NCCL has no 16-bit integer type) turns column stripes into row stripes.  The
-  received buffer holds N column tiles of (H/N x W/N); stage 2 reads them in
-  place (``dfc_rows_from_nr_u16`` tile addressing) with global row numbers, so
-  no transpose pass exists.  Each rank ends with its row stripe of the result.
+  ``shard_cols(W, N, r)``.  Stage 1 (the per-column nearest-object scan) is
+  exact on a stripe because columns are independent.
 
-The two stages are pluggable (``KernelOps`` on the GPU; the CPU tests pass a
-numpy stand-in) so the partition/exchange logic is tested with ``gloo``.
+  - ``compact`` (default, ``StripedEDT``): the library call
+    ``dfc_edt_u8_sharded`` -- column pass on the stripe, an NCCL all-to-all of
+    the compact band data (per 32-row band and column: object mask, nearest
+    object rows above / below the band; 0.25 B/px), the band-path row pass on
+    the row stripe ``shard_rows(H, N, r)``.  The communicator is the
+    library's own (``dfc_comm_init_rank``; rank 0's unique id is broadcast
+    over ``torch.distributed``).
+  - ``dense`` (``edt_column_striped_dense``, reported for comparison): the
+    uint16 nearest-row plane of the stripe (2 B/px) goes through
+    ``all_to_all_single``; stage 2 reads the N received tiles in place
+    (``dfc_rows_from_nr_u16``).
+
+``edt_column_striped_compact_py`` is the compact exchange's data flow in
+Python over ``torch.distributed`` with pluggable column/row stages -- the
+host-side protocol the CPU (gloo) tests check with numpy stand-ins; on the GPU
+the same flow runs inside ``dfc_edt_u8_sharded``.
 """
 from __future__ import annotations
 
@@ -26,6 +34,11 @@ import torch.distributed as dist
 def shard_range(n: int, rank: int, world: int):
     """[lo, hi) of n units owned by rank (contiguous, sizes differ by <= 1)."""
     return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def band_range(rows: int, rank: int, world: int):
+    """[b0, b1) of the 32-row bands of the row stripe of `rank` (dfc_shard_rows)."""
+    return shard_range((rows + 31) // 32, rank, world)
 
 
 class KernelOps:
@@ -46,6 +59,40 @@ class KernelOps:
 
     def batch(self, imgs: torch.Tensor, label: bool = True):
         return self.dfc.edt_batched(imgs, dist=False, label=label)
+
+
+class StripedEDT:
+    """C5 over torch.distributed ranks through ``dfc_edt_u8_sharded`` (compact
+    exchange, NCCL inside libdfc).  Build once per (H, W, world); call with
+    this rank's column stripe; returns (row0, row1, sqdist of the row stripe)."""
+
+    def __init__(self, H: int, W: int, rank: int, world: int, device=None, group=None, dist_out=False):
+        import paper_2106_03503_b200 as dfc
+        self.dfc, self.H, self.W, self.rank, self.world = dfc, H, W, rank, world
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.c0, self.c1 = dfc.shard_cols(W, world, rank)
+        self.r0, self.r1 = dfc.shard_rows(H, world, rank)
+        self.comm = None
+        if world > 1:
+            uid = torch.zeros(128, dtype=torch.uint8, device=self.device)
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(dfc.comm_unique_id()), dtype=torch.uint8))
+            dist.broadcast(uid, 0, group=group)
+            self.comm = dfc.comm_init_rank(world, rank, bytes(uid.cpu().numpy().tobytes()))
+        self.sq = torch.empty((self.r1 - self.r0, W), dtype=torch.int32, device=self.device)
+        self.dist = torch.empty_like(self.sq, dtype=torch.float32) if dist_out else None
+
+    def __call__(self, img_stripe: torch.Tensor, polarity: int = 0, stream=None):
+        if img_stripe.shape != (self.H, self.c1 - self.c0):
+            raise ValueError(f"rank {self.rank} holds columns [{self.c0}, {self.c1}) of all {self.H} rows")
+        self.dfc.edt_sharded([{"rank": self.rank, "img": img_stripe, "sqdist": self.sq, "dist": self.dist,
+                               "comm": self.comm, "stream": stream}], self.world, self.H, self.W, polarity)
+        return self.r0, self.r1, self.sq
+
+    def close(self):
+        if self.comm is not None:
+            self.dfc.comm_destroy(self.comm)
+            self.comm = None
 
 
 def edt_batch_sharded(imgs_all, rank: int, world: int, ops=None, device=None):
@@ -77,9 +124,10 @@ def exchange_column_to_row(nr_stripe: torch.Tensor, H: int, rank: int, world: in
     return recv, my0, my1
 
 
-def edt_column_striped(img_stripe: torch.Tensor, H: int, W: int, rank: int, world: int, ops=None, group=None):
-    """C5: exact squared EDT of an H x W image whose column stripe
-    [rank*W/N, (rank+1)*W/N) this rank holds (img_stripe: [H, W/N] uint8).
+def edt_column_striped_dense(img_stripe: torch.Tensor, H: int, W: int, rank: int, world: int, ops=None,
+                             group=None):
+    """C5, dense exchange: the stripe's uint16 nearest-row plane (2 B/px)
+    through all_to_all_single.  img_stripe: [H, W/N] uint8, equal even stripes.
     Returns (row0, row1, sqdist [row1-row0, W]) -- this rank's row stripe."""
     ops = ops or KernelOps()
     if W % world != 0 or (W // world) % 2 != 0:
@@ -89,4 +137,42 @@ def edt_column_striped(img_stripe: torch.Tensor, H: int, W: int, rank: int, worl
     nr = ops.column_nr(img_stripe)                      # stage 1 on the stripe
     tiles, r0, r1 = exchange_column_to_row(nr, H, rank, world, group)
     sq = ops.rows_from_tiles(tiles, r1 - r0, W, r0, Ws)  # stage 2 on the row stripe
+    return r0, r1, sq
+
+
+def edt_column_striped_compact_py(img_stripe: torch.Tensor, H: int, W: int, rank: int, world: int, ops,
+                                  group=None):
+    """The compact exchange of dfc_edt_u8_sharded, in Python (tests): `ops`
+    provides band_data(stripe) -> (masks [nb, Ws] int64 bit masks, above, below
+    [nb, Ws] int64 rows, -1 = none, count) and rows_from_bands(masks, above,
+    below, row0, nrows, W, count) -> sqdist of the row stripe.  Column stripes
+    from shard_range(W), row stripes from band_range(H); the band slices for
+    rank q are contiguous, as in the C implementation."""
+    c0, c1 = shard_range(W, rank, world)
+    assert img_stripe.shape == (H, c1 - c0)
+    masks, above, below, count = ops.band_data(img_stripe)
+    nb = (H + 31) // 32
+    assert masks.shape == (nb, c1 - c0)
+    packed = torch.stack([masks, above, below]).to(torch.int64)  # [3, nb, Ws]
+    b_my0, b_my1 = band_range(H, rank, world)
+    send = [packed[:, slice(*band_range(H, q, world))].reshape(-1) for q in range(world)]
+    widths = [shard_range(W, q, world)[1] - shard_range(W, q, world)[0] for q in range(world)]
+    rsz = [3 * (b_my1 - b_my0) * widths[q] for q in range(world)]
+    flat = torch.empty(sum(rsz), dtype=torch.int64)
+    counts = torch.empty(world, dtype=torch.int64)
+    if world == 1:
+        flat.copy_(send[0])
+        counts.fill_(count)
+    else:  # one all_to_all_single per message kind (gloo has no list all_to_all)
+        dist.all_to_all_single(flat, torch.cat(send), output_split_sizes=rsz,
+                               input_split_sizes=[t.numel() for t in send], group=group)
+        dist.all_to_all_single(counts, torch.full((world,), count, dtype=torch.int64), group=group)
+    recv = list(torch.split(flat, rsz))
+    full = torch.empty((3, b_my1 - b_my0, W), dtype=torch.int64)
+    for q in range(world):
+        q0, q1 = shard_range(W, q, world)
+        full[:, :, q0:q1] = recv[q].view(3, b_my1 - b_my0, q1 - q0)
+    r0, r1 = min(H, 32 * b_my0), min(H, 32 * b_my1)
+    total = int(counts.sum())
+    sq = ops.rows_from_bands(full[0], full[1], full[2], r0, r1 - r0, W, total)
     return r0, r1, sq

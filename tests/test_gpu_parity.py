@@ -239,7 +239,8 @@ def test_column_striped_path_emulated(dfc, world, p):
     stripe; the all-to-all is emulated by slicing; the real stage-2 kernel reads
     the N tiles in place with global row numbers (dfc_rows_from_nr_u16).  At
     p = 0.002 the row stripes are sparse planes (< 1/256 object pixels): the
-    lane-per-row kernel reads the tiles."""
+    lane-per-row kernel reads the tiles.  (The dense-exchange variant,
+    sharded.edt_column_striped_dense.)"""
     from paper_2106_03503_b200 import sharded
     import workloads
     H, W = (96, 256) if p > 0.01 else (256, 1024)
@@ -273,10 +274,98 @@ def test_column_nr_plane(dfc):
 def test_sharded_driver_single_rank(dfc):
     from paper_2106_03503_b200 import sharded
     img = oracle.random_image(64, 128, 0.01, 4)
-    r0, r1, sq = sharded.edt_column_striped(_dev(img), 64, 128, 0, 1)
+    r0, r1, sq = sharded.edt_column_striped_dense(_dev(img), 64, 128, 0, 1)
     torch.cuda.synchronize()
     assert (r0, r1) == (0, 64)
     np.testing.assert_array_equal(sq.cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+
+
+# ---- dfc_edt_u8_sharded: column stripes -> compact band exchange -> row stripes ----
+
+def _sharded_in_process(dfc, img, world, polarity=0, dist=False, label=False):
+    """All `world` ranks as shards of ONE call on this GPU, without
+    communicators: the exchange is stream-ordered device copies, every other
+    step is the library's real multi-GPU path."""
+    H, W = img.shape
+    shards, outs = [], []
+    for r in range(world):
+        c0, c1 = dfc.shard_cols(W, world, r)
+        r0, r1 = dfc.shard_rows(H, world, r)
+        o = {"sqdist": torch.full((r1 - r0, W), -7, dtype=torch.int32, device="cuda")}
+        if dist:
+            o["dist"] = torch.empty((r1 - r0, W), dtype=torch.float32, device="cuda")
+        if label:
+            o["label"] = torch.empty((r1 - r0, W), dtype=torch.int32, device="cuda")
+        shards.append(dict(rank=r, img=_dev(np.ascontiguousarray(img[:, c0:c1])), comm=None, **o))
+        outs.append((r0, r1, o))
+    dfc.edt_sharded(shards, world, H, W, polarity)
+    torch.cuda.synchronize()
+    full = {k: np.zeros((H, W), np.float32 if k == "dist" else np.int32) for k in outs[0][2]}
+    for r0, r1, o in outs:
+        for k, v in o.items():
+            full[k][r0:r1] = v.cpu().numpy()
+    return full
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("kind", ["tiles", "bern", "discs", "corner", "empty"])
+def test_sharded_library_in_process(dfc, world, kind):
+    import workloads
+    if kind == "tiles":
+        img = workloads.sparse_tiles(512, 1024, tile=32, n_on=64, p=0.004, seed=3 + world)
+    elif kind == "bern":
+        img = oracle.random_image(301, 517, 0.02, 40 + world)   # uneven stripes, partial last band
+    elif kind == "discs":
+        img = workloads.discs(256, 384, 10, 4)               # a dense plane through the band path
+    elif kind == "corner":
+        img = np.zeros((200, 333), np.uint8)
+        img[199, 0] = 1
+    else:
+        img = np.zeros((70, 90), np.uint8)
+    got = _sharded_in_process(dfc, img, world, dist=True, label=True)
+    want = oracle.to_i32(oracle.edt(img))
+    np.testing.assert_array_equal(got["sqdist"], want)
+    np.testing.assert_array_equal(got["dist"].view(np.uint32), oracle.sqrt_f32(want).view(np.uint32))
+    lab = oracle.voronoi_labels(img, linear=True)
+    np.testing.assert_array_equal(got["label"], np.full(img.shape, -1, np.int32) if lab is None else lab[1])
+
+
+def test_sharded_library_inverted_polarity(dfc):
+    img = np.ones((256, 300), np.uint8)
+    img[[5, 100, 200], [7, 150, 299]] = 0
+    got = _sharded_in_process(dfc, img, 4, polarity=1)
+    np.testing.assert_array_equal(got["sqdist"], oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
+
+
+def test_sharded_library_nccl_single_rank(dfc):
+    """The NCCL exchange itself (grouped send/recv through libnccl) with a
+    one-rank communicator -- the one-GPU box cannot host more ranks."""
+    from paper_2106_03503_b200 import sharded
+    img = oracle.random_image(130, 257, 0.003, 12)
+    uid = dfc.comm_unique_id()
+    comm = dfc.comm_init_rank(1, 0, uid)
+    try:
+        sq = torch.empty((130, 257), dtype=torch.int32, device="cuda")
+        dfc.edt_sharded([dict(rank=0, img=_dev(img), sqdist=sq, comm=comm)], 1, 130, 257)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(sq.cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+    finally:
+        dfc.comm_destroy(comm)
+    st = sharded.StripedEDT(130, 257, 0, 1)
+    r0, r1, sq2 = st(_dev(img))
+    torch.cuda.synchronize()
+    assert (r0, r1) == (0, 130)
+    np.testing.assert_array_equal(sq2.cpu().numpy(), oracle.to_i32(oracle.edt(img)))
+
+
+def test_sharded_library_argument_errors(dfc):
+    img = _dev(np.zeros((64, 64), np.uint8))
+    sq = torch.empty((64, 64), dtype=torch.int32, device="cuda")
+    with pytest.raises(dfc.DfcError):   # two shards claim rank 0
+        dfc.edt_sharded([dict(rank=0, img=img[:, :32], sqdist=sq), dict(rank=0, img=img[:, 32:], sqdist=sq)],
+                        2, 64, 64)
+    with pytest.raises(dfc.DfcError):   # in-process exchange needs every rank
+        dfc.edt_sharded([dict(rank=0, img=img[:, :32], sqdist=sq)], 2, 64, 64)
 
 
 @pytest.fixture
