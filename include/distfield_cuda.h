@@ -265,17 +265,15 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 
 /*
  * Stage-2 kernel selection for the calls of this thread: 0 = library
- * default, 1 = segment/merge kernel (k_rows), 2 = streaming lane-per-row
- * kernel (k_rows_stream, with k_rows as its overflow fallback), 3 = window
- * kernel (k_rows_win: per-segment stacks + bounded outward search, rows up to
- * 16384 columns; wider rows use k_rows), 4 = dense-row kernel (k_rows_dense)
- * for rows with only short runs between object pixels and k_rows for the rest,
- * 5 = lane-per-row chunk scan (k_rows_lr, with k_rows as its overflow
- * fallback), 6 = the default: as 4, but anchored segments (k_rows_anc: one
- * CTA per row, one lane per column of a 32-column segment, rows up to 16384
- * columns) instead of k_rows for every row the point-plane, dense-row and
- * sparse-plane kernels do not take.  Results are identical; this is a
- * performance/testing knob.
+ * default, 1 = segment/merge kernel (k_rows) for every row, 4 = dense-row
+ * kernel (k_rows_dense) for rows with only short runs between object pixels,
+ * the lane-per-row chunk scan (k_rows_lr) for sparse planes and k_rows for
+ * the rest, 5 = k_rows_lr for every row (k_rows as its overflow fallback),
+ * 6 = the default: point planes by k_rows_pts, sparse planes of single
+ * images by the band path (k_rows_band.cu), every other row by anchored
+ * segments (k_rows_anc, rows up to 16384 columns; wider rows by k_rows).
+ * Modes 2 and 3 (retired kernels) return DFC_ERR_ARG.  Results are identical
+ * in every mode; this is a performance/testing knob.
  */
 int dfc_set_row_kernel(int mode);
 

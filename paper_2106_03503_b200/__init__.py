@@ -123,13 +123,12 @@ def set_lr_chunk(cols: int) -> None:
 
 def set_row_kernel(mode: str) -> None:
     """Stage-2 kernel for this thread's calls: "default" (= "anc" unless
-    DFC_ROWS says otherwise), "segment", "stream", "window" (k_rows_win.cu,
-    rows up to 16384 columns), "dense" (point planes, dense rows, sparse
-    planes, the merge-tree kernel k_rows for the rest), "lr" (k_rows_lr.cu,
-    lane-per-row chunk scan) or "anc" (as "dense" but k_rows_anc.cu, anchored
-    segments, for the rest)."""
-    _check(_lib.dfc_set_row_kernel(
-        {"default": 0, "segment": 1, "stream": 2, "window": 3, "dense": 4, "lr": 5, "anc": 6}[mode]))
+    DFC_ROWS says otherwise), "segment" (the merge-tree kernel k_rows for
+    every row), "dense" (point planes, dense rows, sparse planes, k_rows for
+    the rest), "lr" (k_rows_lr.cu, lane-per-row chunk scan for every row) or
+    "anc" (point planes, sparse planes by the band path, k_rows_anc.cu for the
+    rest).  Results are identical in every mode."""
+    _check(_lib.dfc_set_row_kernel({"default": 0, "segment": 1, "dense": 4, "lr": 5, "anc": 6}[mode]))
 
 
 def last_launch_count() -> int:

@@ -3,8 +3,6 @@
 // code), so kernel host stubs, templates and registrations live in one unit.
 #include "k_columns.cu"
 #include "k_rows.cu"
-#include "k_rows_stream.cu"
-#include "k_rows_win.cu"
 #include "k_rows_dense.cu"
 #include "k_rows_lr.cu"
 #include "k_rows_pts.cu"

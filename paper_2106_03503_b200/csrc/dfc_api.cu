@@ -19,15 +19,13 @@ thread_local int g_last_cuda = 0;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
 thread_local int g_lr_chunk = 0;  // k_rows_lr columns per warp chunk (0: default)
-thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 2: streaming, 3: window,
-                                  // 4: dense rows first, the rest by the segment kernel (default)
+thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 4: dense rows first, the
+                                  // rest by the segment kernel, 5: lane-per-row, 6: anchored (default)
 
 // DFC_ROWS=segment|stream overrides the default stage-2 kernel (tuning/A-B).
 int env_row_mode() {
     static const int m = [] {
         const char* v = getenv("DFC_ROWS");
-        if (v && strcmp(v, "stream") == 0) return 2;
-        if (v && strcmp(v, "win") == 0) return 3;
         if (v && strcmp(v, "segment") == 0) return 1;
         if (v && strcmp(v, "dense") == 0) return 4;
         if (v && strcmp(v, "lr") == 0) return 5;
@@ -166,7 +164,13 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
         g_launches += 2;
         return DFC_OK;
     }
-    const dim3 fgrid(grid.x, (unsigned)(n > 1 ? (c.nb + kFillBands - 1) / kFillBands : c.nb), grid.z);
+    // several bands per CTA for batches (a skipped plane costs few CTAs); for a
+    // single image ~8 CTAs per SM in all (each CTA walks nb / grid.y bands), so
+    // a plane the row pass reads from the bands costs ~1k early exits, not
+    // one per (band, 512 columns)
+    const unsigned fy = n > 1 ? (unsigned)((c.nb + kFillBands - 1) / kFillBands)
+                              : (unsigned)std::max<int64_t>(1, std::min<int64_t>(c.nb, (148 * 8 + grid.x - 1) / grid.x));
+    const dim3 fgrid(grid.x, fy, grid.z);
     if (vsq)
         k_band_fill<true><<<fgrid, tpb, 0, st>>>(c, first, last, nullptr, vsq);
     else
@@ -184,42 +188,6 @@ struct OutSet {
 
 bool out_vec_ok(const void* p, int64_t stride) {
     return p == nullptr || (aligned(p, 16) && stride % 16 == 0);
-}
-
-// Window kernel (k_rows_win.cu): 32-column segments, a power-of-two count per
-// row; 256 threads per CTA, each row's segments spread over the CTA.
-int row_pass_win(RowArgs a, bool take_new, cudaStream_t st) {
-    constexpr int Lw = 32;
-    const int W = a.W;
-    WinLayout wl;
-    wl.nseg = 1;
-    while (wl.nseg * Lw < W) wl.nseg <<= 1;
-    wl.spt = 1;
-    wl.lg = 0;
-    while ((1 << wl.lg) < wl.nseg) ++wl.lg;
-    a.L = Lw;
-    a.R = std::max(1, 256 / wl.nseg);
-    a.T = std::min(wl.nseg, 256);
-    a.row_smem_words = win_row_words(wl.nseg, Lw);
-    a.vec_nr = aligned(a.nr, 16) && a.Wp % 8 == 0 && a.nr_img_stride % 8 == 0 &&
-               (a.tile_cols >= W || (a.tile_cols % Lw == 0 && a.tile_stride % 8 == 0));
-    int smem = a.R * a.row_smem_words * 4;
-    while (a.R > 1 && smem > 227 * 1024) {
-        a.R >>= 1;
-        smem = a.R * a.row_smem_words * 4;
-    }
-    if (smem > 227 * 1024) return DFC_ERR_SHAPE;
-    const int threads = std::min(256, std::max(32, a.R * wl.nseg));
-    const void* fn = take_new ? win_kernel_ptr<true>() : win_kernel_ptr<false>();
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_fail(e);
-    const int64_t blocks = (a.total_rows + a.R - 1) / a.R;
-    if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
-    void* args[] = {&a, &wl};
-    e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(threads), args, (size_t)smem, st);
-    if (e != cudaSuccess) return cuda_fail(e);
-    ++g_launches;
-    return DFC_OK;
 }
 
 // dense planes by k_rows_anc too (all-object segments and anchors on object
@@ -256,21 +224,22 @@ bool band_sparse_on() {
 // The band path (k_rows_band.cu) over the sparse planes of `ba`: hull filter,
 // per-row stacks, fill into a's outputs.
 int launch_band_path(const RowArgs& a, const BandArgs& ba, bool take_new, cudaStream_t st) {
-    const dim3 hgrid((unsigned)((ba.W + 1024 * kHullWarps - 1) / (1024 * kHullWarps)), (unsigned)ba.nb,
-                     (unsigned)(2 * ba.nplanes));
-    k_band_hull<<<hgrid, 32 * kHullWarps, 0, st>>>(ba);
+    BandArgs hb = ba;
+    hb.win = (int)round_up((ba.W + 31) / 32, 32);
+    const int64_t htasks = (int64_t)ba.nplanes * ba.nb * 2;
+    k_band_hull<<<(unsigned)((htasks + kHullWarps - 1) / kHullWarps), 32 * kHullWarps, 0, st>>>(hb);
     const int64_t tasks = (int64_t)ba.nplanes * ba.nb;
     const unsigned rblocks = (unsigned)((tasks + kBandWarps - 1) / kBandWarps);
     if (take_new)
-        k_band_rows<true><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
+        k_band_rows<true><<<rblocks, 32 * kBandWarps, 0, st>>>(hb);
     else
-        k_band_rows<false><<<rblocks, 32 * kBandWarps, 0, st>>>(ba);
+        k_band_rows<false><<<rblocks, 32 * kBandWarps, 0, st>>>(hb);
     const int fsm = fill_smem_bytes();
     cudaError_t e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
     if (e != cudaSuccess) return cuda_fail(e);
     const int64_t rows = (int64_t)ba.nplanes * ba.H;
     const int64_t fblocks = std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * 6);
-    k_rows_fill<<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
+    k_rows_fill<<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
     g_launches += 3;
     return DFC_OK;
 }
@@ -321,7 +290,6 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     a.n_img = band.n_img;
     a.bpol0 = band.pol0;
     const int mode = g_row_mode != 0 ? g_row_mode : env_row_mode();
-    if (mode == 3 && W <= 16384) return row_pass_win(a, take_new, st);
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
@@ -368,20 +336,27 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         return DFC_OK;
     };
 
-    // Mode 5: every row by k_rows_lr; rows whose live stack overflows go to k_rows.
+    // Mode 5: every row by k_rows_lr; rows whose live stack overflows (flagged
+    // 2 in row_done -- once per row, however many of its chunks overflow) are
+    // compacted into a list and recomputed by k_rows.
     if (mode == 5 && lr_ok) {
         Scratch fl(st);
-        e = fl.alloc(ent_bytes + entr_bytes + (size_t)(a.total_rows + 1) * sizeof(int));
+        const size_t flag_bytes = (size_t)round_up(a.total_rows, 256);
+        e = fl.alloc(ent_bytes + entr_bytes + flag_bytes + (size_t)(a.total_rows + 1) * sizeof(int));
         if (e != cudaSuccess) return cuda_fail(e);
-        int* fail_count = reinterpret_cast<int*>(static_cast<char*>(fl.p) + ent_bytes + entr_bytes);
+        uint8_t* flags = reinterpret_cast<uint8_t*>(static_cast<char*>(fl.p) + ent_bytes + entr_bytes);
+        int* fail_count = reinterpret_cast<int*>(flags + flag_bytes);
         int* fail_rows = fail_count + 1;
-        e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
+        e = cudaMemsetAsync(flags, 0, flag_bytes + sizeof(int), st);
         if (e != cudaSuccess) return cuda_fail(e);
         RowArgs la = a;
         la.lr_gate = false;
-        la.row_done = nullptr;
-        int rc = launch_lr(la, fl.p, fail_rows, fail_count);
+        la.row_done = flags;
+        int rc = launch_lr(la, fl.p, nullptr, nullptr);
         if (rc != DFC_OK) return rc;
+        const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
+        k_rows_failed<<<(unsigned)rblocks, 256, 0, st>>>(flags, a.total_rows, fail_rows, fail_count);
+        ++g_launches;
         RowArgs fb = a;  // fallback: the segment kernel over the overflowed rows
         fb.row_list = fail_rows;
         fb.row_count = fail_count;
@@ -541,50 +516,9 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         return DFC_OK;
     }
 
-    // Streaming kernel (one lane = one row) when the nr plane allows coalesced
-    // 16-byte tile loads; rows whose live stack overflows go to k_rows.
-    const bool stream_ok = mode == 2 && aligned(nr, 16) && Wp % 8 == 0 && a.tile_cols % 8 == 0 &&
-                           a.tile_stride % 8 == 0 && a.nr_img_stride % 8 == 0;
-    if (stream_ok) {
-        Scratch fl(st);
-        e = fl.alloc((size_t)(a.total_rows + 1) * sizeof(int));
-        if (e != cudaSuccess) return cuda_fail(e);
-        int* fail_count = static_cast<int*>(fl.p);
-        int* fail_rows = fail_count + 1;
-        e = cudaMemsetAsync(fail_count, 0, sizeof(int), st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        const int outs = (D ? kOutD : 0) | (S ? kOutS : 0) | (LB ? kOutL : 0) | (NC ? kOutN : 0);
-        const void* sfn = take_new ? stream_kernel_ptr<true>(outs) : stream_kernel_ptr<false>(outs);
-        const int ssm = stream_smem_bytes();
-        e = cudaFuncSetAttribute(sfn, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
-        if (e != cudaSuccess) return cuda_fail(e);
-        const int64_t sblocks = (a.total_rows + 32 * kSWarps - 1) / (32 * kSWarps);
-        static const int chunk_env = [] {  // DFC_CHUNK (tuning): columns per warp chunk
-            const char* v = getenv("DFC_CHUNK");
-            const int c = v ? atoi(v) : 0;
-            return c >= 32 ? c & ~31 : 256;
-        }();
-        int chunk = (int)std::min<int64_t>(W, chunk_env);
-        chunk = (chunk + 31) & ~31;
-        const int nchunks = (int)((W + chunk - 1) / chunk);
-        if (sblocks > 0x7fffffff || nchunks > 65535) return DFC_ERR_SHAPE;
-        void* sargs[] = {&a, &fail_rows, &fail_count, &chunk};
-        e = cudaLaunchKernel(sfn, dim3((unsigned)sblocks, (unsigned)nchunks), dim3(32 * kSWarps), sargs,
-                             (size_t)ssm, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-        ++g_launches;
-        RowArgs fb = a;  // fallback: the segment kernel over the overflowed rows
-        fb.row_list = fail_rows;
-        fb.row_count = fail_count;
-        void* fargs[] = {&fb};
-        const int64_t fblocks = std::min<int64_t>(blocks, 148 * 4);
-        e = cudaLaunchKernel(fn, dim3((unsigned)fblocks), dim3(g.R * g.T), fargs, (size_t)g.smem_bytes, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-    } else {
-        void* args[] = {&a};
-        e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
-        if (e != cudaSuccess) return cuda_fail(e);
-    }
+    void* args[] = {&a};
+    e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e);
     ++g_launches;
     return DFC_OK;
 }
@@ -1045,7 +979,7 @@ int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_
 }
 
 int dfc_set_row_kernel(int mode) {
-    if (mode < 0 || mode > 6) return DFC_ERR_ARG;
+    if (mode < 0 || mode > 6 || mode == 2 || mode == 3) return DFC_ERR_ARG;  // 2, 3: retired kernels
     g_row_mode = mode;
     return DFC_OK;
 }

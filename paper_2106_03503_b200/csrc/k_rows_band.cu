@@ -45,12 +45,12 @@
 
 namespace dfc {
 
-constexpr int kHullWarps = 4;
+constexpr int kHullWarps = 2;
+constexpr int kHullCap = 64;        // stack entries per hull window
 constexpr int kBandWarps = 2;       // k_band_rows: bands per CTA
 constexpr int kBandCap = 32;        // ring entries per lane (power of two)
 constexpr int kFillWarps = 4;
 constexpr int kFillCap = 1536;      // list entries staged per warp (k_rows_fill)
-constexpr uint32_t kHullNone = 0xFFFFFFFFu;
 
 struct BandArgs {
     const uint32_t* bmask;   // [img][nb][Wp] bit r = row 32 b + r nonzero
@@ -67,6 +67,7 @@ struct BandArgs {
     // an image of Hg rows; plane p's local rows are [0, H).  Single images:
     // band0 = 0, Hg = H.
     int band0, Hg;
+    int win;                 // k_band_hull window: ceil(W / 32) rounded up to 32 (<= 1024)
     bool pts_gate;           // point planes belong to k_rows_pts
     bool all_planes;         // every plane (the sharded path), not only the sparse ones
 };
@@ -77,128 +78,137 @@ __device__ __forceinline__ bool band_plane(const BandArgs& a, int p) {
 }
 
 // ---------------------------------------------------------------- hull filter
+// warp = (plane, band, side); lane = a window of `win` columns (the 32 windows
+// cover the row).  Each lane runs the monotone chain over its window (stack in
+// shared memory, top two entries cached in registers); then 5 levels of bridge
+// merges join the windows' hulls into the row's hull: a merge walks the lower
+// common tangent from the left group's last and the right group's first
+// vertex, trimming each window's surviving range [lo, hi) of its stack.  A
+// window whose stack would exceed kHullCap entries contributes every valid
+// column instead and sits out the merges (still a superset).
+struct HullSmem {
+    int32_t h[kHullCap][32];    // H of the stack entries (< 2^31, see below)
+    uint16_t c[kHullCap][32];   // their column offsets in the window
+    int lo[32], hi[32];         // surviving range of each window's stack
+};
+
 __global__ void __launch_bounds__(32 * kHullWarps) k_band_hull(BandArgs a) {
-    __shared__ uint32_t dsm[kHullWarps][32][33];  // line distance per (column-in-lane, lane)
-    __shared__ uint32_t hm[kHullWarps][32];       // hull bits per lane
-    constexpr unsigned FULL = 0xffffffffu;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int win = blockIdx.x * kHullWarps + warp;
-    const int b = blockIdx.y;
-    const int p = blockIdx.z >> 1, side = blockIdx.z & 1;
-    if (win * 1024 >= a.W) return;                 // warp-uniform
-    if (!band_plane(a, p)) return;                 // CTA-uniform
-    const int w0 = win * 1024, c0 = w0 + 32 * lane;
-    const int gb = a.band0 + b;  // global band
+    __shared__ HullSmem smem[kHullWarps];
+    HullSmem& sm = smem[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31;
+    const int64_t task = (int64_t)blockIdx.x * kHullWarps + (threadIdx.x >> 5);
+    if (task >= (int64_t)a.nplanes * a.nb * 2) return;
+    const int side = (int)(task & 1);
+    const int64_t pb = task >> 1;
+    const int p = (int)(pb / a.nb), b = (int)(pb - (int64_t)p * a.nb);
+    if (!band_plane(a, p)) return;  // warp-uniform
+    const int gb = a.band0 + b;      // global band
     const int line = side ? min(32 * gb + 31, a.Hg - 1) : 32 * gb;
-    uint32_t (&D)[32][33] = dsm[warp];
-
-    // ---- the lane's 32 carries -> distance to the line (kHullNone: none) ----
+    const int WIN = a.win;
+    const int k0 = lane * WIN, k1 = min(a.W, k0 + WIN);
     const uint16_t* car = (side ? a.below : a.above) + ((int64_t)p * a.nb + b) * a.Wp;
-    if (c0 + 32 <= a.Wp) {
-        const uint4* q = reinterpret_cast<const uint4*>(car + c0);
+    // H_k = d^2 + k^2 <= (rows-1)^2 + (cols-1)^2 <= DFC_MAX_SQDIST < 2^31: int32;
+    // differences fit int32, times column differences (< 2^15): one IMAD.WIDE
+    auto above_seg = [](int ka, int Ha, int kb, int Hb, int kc, int Hc) {
+        return (long long)(Hb - Ha) * (kc - kb) > (long long)(Hc - Hb) * (kb - ka);
+    };
+    // 32 carries of columns [c0, c0 + 32) (kNoRow past the row end)
+    auto load32 = [&](int c0, uint32_t (&w)[16]) {
+        if (c0 + 32 <= a.Wp) {
+            const uint4* q = reinterpret_cast<const uint4*>(car + c0);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const uint4 x = __ldg(q + v);
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+            for (int v = 0; v < 4; ++v) {
+                const uint4 x = __ldg(q + v);
+                w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
+            }
+        } else {
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const int c = 8 * v + t;
-                const uint32_t r = (w[t >> 1] >> (16 * (t & 1))) & 0xffffu;
-                D[c][lane] = (r == kNoRow || c0 + c >= a.W) ? kHullNone
-                                                             : (side ? r - (uint32_t)line : (uint32_t)line - r);
+            for (int t = 0; t < 16; ++t) {
+                const uint32_t lo = c0 + 2 * t < a.W ? (uint32_t)__ldg(car + c0 + 2 * t) : kNoRow;
+                const uint32_t hi = c0 + 2 * t + 1 < a.W ? (uint32_t)__ldg(car + c0 + 2 * t + 1) : kNoRow;
+                w[t] = lo | (hi << 16);
             }
         }
-    } else {
-        for (int c = 0; c < 32; ++c) {
-            const uint32_t r = c0 + c < a.W ? (uint32_t)__ldg(car + c0 + c) : kNoRow;
-            D[c][lane] = r == kNoRow ? kHullNone : (side ? r - (uint32_t)line : (uint32_t)line - r);
-        }
-    }
-    __syncwarp();
-    auto Hof = [&](int x) -> int64_t {  // H of window column x (a valid one)
-        const int o = x - w0;
-        const int64_t d = D[o & 31][o >> 5];
-        return d * d + (int64_t)x * x;
-    };
-    // b strictly above the segment a-c (ka < kb < kc): b is not on the lower hull
-    auto above_seg = [](int ka, int64_t Ha, int kb, int64_t Hb, int kc, int64_t Hc) {
-        return (Hb - Ha) * (int64_t)(kc - kb) > (Hc - Hb) * (int64_t)(kb - ka);
     };
 
-    // ---- lane-local lower hull (monotone chain), the stack as a bit mask ----
-    uint32_t st = 0;
-    int tc = -1;        // top (column offset in the lane)
-    int64_t tH = 0;
-    for (int c = 0; c < 32; ++c) {
-        const uint32_t dv = D[c][lane];
-        if (dv == kHullNone) continue;
-        const int k = c0 + c;
-        const int64_t Hk = (int64_t)dv * dv + (int64_t)k * k;
-        while (st & (st - 1)) {  // at least two entries
-            const int sc = 31 - __clz(st & ((1u << tc) - 1u));
-            const int64_t sH = Hof(c0 + sc);
-            if (above_seg(c0 + sc, sH, c0 + tc, tH, k, Hk)) {
-                st ^= 1u << tc;
-                tc = sc;
+    // ---- monotone chain over the window ----
+    int n = 0;
+    bool overflow = false;
+    int tk = 0, tH = 0, sk = 0, sH = 0;  // top and second entries
+    for (int c0 = k0; c0 < k1; c0 += 32) {
+        uint32_t w[16];
+        load32(c0, w);
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const uint32_t r = (w[t >> 1] >> (16 * (t & 1))) & 0xffffu;
+            const int k = c0 + t;
+            if (r == kNoRow || k >= k1 || overflow) continue;
+            const int d = side ? (int)r - line : line - (int)r;
+            const int H = d * d + k * k;
+            while (n >= 2 && above_seg(sk, sH, tk, tH, k, H)) {
+                --n;
+                tk = sk;
                 tH = sH;
-            } else {
-                break;
+                if (n >= 2) {
+                    sk = k0 + sm.c[n - 2][lane];
+                    sH = sm.h[n - 2][lane];
+                }
             }
+            if (n == kHullCap) {
+                overflow = true;
+                continue;
+            }
+            sm.h[n][lane] = H;
+            sm.c[n][lane] = (uint16_t)(k - k0);
+            ++n;
+            sk = tk;
+            sH = tH;
+            tk = k;
+            tH = H;
         }
-        st |= 1u << c;
-        tc = c;
-        tH = Hk;
     }
-    uint32_t* M = hm[warp];
-    M[lane] = st;
+    sm.lo[lane] = 0;
+    sm.hi[lane] = overflow ? 0 : n;
     __syncwarp();
 
-    // ---- bridge merges: groups of g lanes, leaders at multiples of 2g ----
-    auto col_of = [&](int l, int c) { return w0 + 32 * l + c; };
+    // ---- bridge merges: groups of g windows, leaders at multiples of 2g ----
     for (int g = 1; g < 32; g <<= 1) {
         if ((lane & (2 * g - 1)) == 0) {
             const int lead = lane, mid = lane + g, end = lane + 2 * g;
-            int xa = -1, xb = -1;
+            int wa = -1, ia = 0, wb = -1, ib = 0;
             for (int l = mid - 1; l >= lead; --l)
-                if (M[l]) {
-                    xa = col_of(l, 31 - __clz(M[l]));
-                    break;
-                }
+                if (sm.hi[l] > sm.lo[l]) { wa = l; ia = sm.hi[l] - 1; break; }
             for (int l = mid; l < end; ++l)
-                if (M[l]) {
-                    xb = col_of(l, __ffs(M[l]) - 1);
-                    break;
-                }
-            if (xa >= 0 && xb >= 0) {
-                int64_t Ha = Hof(xa), Hb = Hof(xb);
+                if (sm.hi[l] > sm.lo[l]) { wb = l; ib = sm.lo[l]; break; }
+            if (wa >= 0 && wb >= 0) {
+                int ka = wa * WIN + sm.c[ia][wa], Ha = sm.h[ia][wa];
+                int kb = wb * WIN + sm.c[ib][wb], Hb = sm.h[ib][wb];
                 for (;;) {
                     bool moved = false;
-                    for (;;) {  // predecessor of xa in the left group
-                        const int o = xa - w0;
-                        int l = o >> 5;
-                        uint32_t m = M[l] & ((1u << (o & 31)) - 1u);
-                        while (!m && l > lead) m = M[--l];
-                        if (!m) break;
-                        const int xp = col_of(l, 31 - __clz(m));
-                        const int64_t Hp = Hof(xp);
-                        if (!above_seg(xp, Hp, xa, Ha, xb, Hb)) break;
-                        M[o >> 5] &= ~(1u << (o & 31));
-                        xa = xp;
-                        Ha = Hp;
+                    for (;;) {  // the predecessor of a in the left group
+                        int wp = wa, ip = ia - 1;
+                        if (ip < sm.lo[wp]) {
+                            for (wp = wa - 1; wp >= lead && sm.hi[wp] <= sm.lo[wp]; --wp) {}
+                            if (wp < lead) break;
+                            ip = sm.hi[wp] - 1;
+                        }
+                        const int kp = wp * WIN + sm.c[ip][wp], Hp = sm.h[ip][wp];
+                        if (!above_seg(kp, Hp, ka, Ha, kb, Hb)) break;
+                        sm.hi[wa] = ia;  // a is the left group's last vertex
+                        wa = wp; ia = ip; ka = kp; Ha = Hp;
                         moved = true;
                     }
-                    for (;;) {  // successor of xb in the right group
-                        const int o = xb - w0;
-                        int l = o >> 5;
-                        uint32_t m = (o & 31) == 31 ? 0u : M[l] & ~((2u << (o & 31)) - 1u);
-                        while (!m && l < end - 1) m = M[++l];
-                        if (!m) break;
-                        const int xs = col_of(l, __ffs(m) - 1);
-                        const int64_t Hs = Hof(xs);
-                        if (!above_seg(xa, Ha, xb, Hb, xs, Hs)) break;
-                        M[o >> 5] &= ~(1u << (o & 31));
-                        xb = xs;
-                        Hb = Hs;
+                    for (;;) {  // the successor of b in the right group
+                        int ws = wb, is = ib + 1;
+                        if (is >= sm.hi[ws]) {
+                            for (ws = wb + 1; ws < end && sm.hi[ws] <= sm.lo[ws]; ++ws) {}
+                            if (ws >= end) break;
+                            is = sm.lo[ws];
+                        }
+                        const int ks = ws * WIN + sm.c[is][ws], Hs = sm.h[is][ws];
+                        if (!above_seg(ka, Ha, kb, Hb, ks, Hs)) break;
+                        sm.lo[wb] = ib + 1;  // b is the right group's first vertex
+                        wb = ws; ib = is; kb = ks; Hb = Hs;
                         moved = true;
                     }
                     if (!moved) break;
@@ -207,34 +217,48 @@ __global__ void __launch_bounds__(32 * kHullWarps) k_band_hull(BandArgs a) {
         }
         __syncwarp();
     }
-    uint32_t word = M[lane];
 
-    // ---- side 0 also carries the columns with an object pixel in the band ----
-    if (side == 0) {
-        const int s = p / a.n_img, im = p - s * a.n_img;
-        const int pol = a.pol0 + s;
-        const int nrows = min(32, a.Hg - 32 * gb);
-        const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
-        const uint32_t* mrow = a.bmask + ((int64_t)im * a.nb + b) * a.Wp;
+    // ---- the window's candidate words (side 0 adds the band's object columns) ----
+    const int s = p / a.n_img, im = p - s * a.n_img;
+    const int pol = a.pol0 + s;
+    const int nrows = min(32, a.Hg - 32 * gb);
+    const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
+    const uint32_t* mrow = a.bmask + ((int64_t)im * a.nb + b) * a.Wp;
+    uint32_t* out = a.cand + (((int64_t)p * a.nb + b) * 2 + side) * a.Ww;
+    int idx = sm.lo[lane];
+    const int ihi = sm.hi[lane];
+    for (int c0 = k0; c0 < k1; c0 += 32) {
         uint32_t z = 0;
-        if (c0 + 32 <= a.Wp) {
-            const uint4* q = reinterpret_cast<const uint4*>(mrow + c0);
-#pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                const uint4 x = __ldg(q + v);
-                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) z |= (uint32_t)(pol_mask(w[t], pol, valid) != 0u) << (4 * v + t);
-            }
-        } else {
-            for (int c = 0; c < 32 && c0 + c < a.Wp; ++c) z |= (uint32_t)(pol_mask(__ldg(mrow + c0 + c), pol, valid) != 0u) << c;
+        while (idx < ihi && k0 + sm.c[idx][lane] < c0 + 32) {
+            z |= 1u << ((k0 + sm.c[idx][lane]) & 31);
+            ++idx;
         }
-        if (a.W - c0 < 32) z &= a.W - c0 <= 0 ? 0u : ((1u << (a.W - c0)) - 1u);
-        word |= z;
+        if (overflow) {  // every valid column of the window
+            uint32_t w[16];
+            load32(c0, w);
+#pragma unroll
+            for (int t = 0; t < 32; ++t)
+                z |= (uint32_t)(((w[t >> 1] >> (16 * (t & 1))) & 0xffffu) != kNoRow) << t;
+        }
+        if (side == 0) {
+            if (c0 + 32 <= a.Wp) {
+                const uint4* q = reinterpret_cast<const uint4*>(mrow + c0);
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const uint4 x = __ldg(q + v);
+                    z |= (uint32_t)(pol_mask(x.x, pol, valid) != 0u) << (4 * v);
+                    z |= (uint32_t)(pol_mask(x.y, pol, valid) != 0u) << (4 * v + 1);
+                    z |= (uint32_t)(pol_mask(x.z, pol, valid) != 0u) << (4 * v + 2);
+                    z |= (uint32_t)(pol_mask(x.w, pol, valid) != 0u) << (4 * v + 3);
+                }
+            } else {
+                for (int c = 0; c < 32 && c0 + c < a.Wp; ++c)
+                    z |= (uint32_t)(pol_mask(__ldg(mrow + c0 + c), pol, valid) != 0u) << c;
+            }
+        }
+        if (k1 - c0 < 32) z &= (1u << (k1 - c0)) - 1u;  // columns past the row end
+        out[c0 >> 5] = z;
     }
-    const int wi = w0 / 32 + lane;
-    if (wi < a.Ww) a.cand[(((int64_t)p * a.nb + b) * 2 + side) * a.Ww + wi] = word;
-    (void)FULL;
 }
 
 // ------------------------------------------------------------ per-row stacks

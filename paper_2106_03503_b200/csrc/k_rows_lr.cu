@@ -647,6 +647,22 @@ __global__ void k_rows_rest(const uint8_t* row_done, const unsigned long long* c
     }
 }
 
+// Rows k_rows_lr flagged as overflowed (row_done == 2), appended to a list
+// once each (mode 5's fallback list: at most total_rows entries).
+__global__ void k_rows_failed(const uint8_t* row_done, int64_t total_rows, int* list, int* count) {
+    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < total_rows;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const bool mine = row_done[row] == 2;
+        const unsigned m = __ballot_sync(__activemask(), mine);
+        if (m == 0) continue;
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(count, __popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (mine) list[base + __popc(m & ((1u << lane) - 1u))] = (int)row;
+    }
+}
+
 // Object pixels of a (possibly column-tiled) nearest-row plane: cells whose
 // nearest object row is their own row (the sparse-plane gate of
 // dfc_rows_from_nr_u16, where no column pass of the whole image ran here).

@@ -78,10 +78,13 @@ def _strictly_above(ka, Ha, kb, Hb, kc, Hc):
     return (Hb - Ha) * (kc - kb) > (Hc - Hb) * (kb - ka)
 
 
-def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None):
-    """Candidate bits of one window [w0, w0 + lanes*lane_cols): the kernel's
-    per-lane monotone chains + log2(lanes) levels of bridge merges.  Returns
-    the set of hull columns."""
+def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None, cap=None):
+    """Candidate columns of one group of `lanes` lanes x `lane_cols` columns
+    starting at w0 (k_band_hull: lane = a window of the row, the group = the
+    whole row): per-lane monotone chains, then log2(lanes) levels of bridge
+    merges.  A lane whose stack would exceed `cap` entries contributes all its
+    valid columns and sits out the merges (a superset: a hull point of the row
+    is a hull point of every subset holding it)."""
     W = len(car) if W is None else W
 
     def Hof(k):
@@ -93,6 +96,7 @@ def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None):
 
     # lane-local hulls: bit c of hm[l] = column w0 + lane_cols*l + c
     hm = [0] * lanes
+    overflow = set()
     for l in range(lanes):
         st = []
         for c in range(lane_cols):
@@ -105,6 +109,12 @@ def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None):
                     st.pop()
                 else:
                     break
+            if cap is not None and len(st) == cap:
+                for c2 in range(lane_cols):
+                    if valid(w0 + lane_cols * l + c2):
+                        overflow.add(w0 + lane_cols * l + c2)
+                st = []
+                break
             st.append(k)
         for k in st:
             hm[l] |= 1 << (k - w0 - lane_cols * l)
@@ -170,7 +180,7 @@ def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None):
                 if not moved:
                     break
         g *= 2
-    out = set()
+    out = set(overflow)
     for l in range(lanes):
         for c in range(lane_cols):
             if (hm[l] >> c) & 1:
@@ -178,13 +188,13 @@ def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None):
     return out
 
 
-def band_candidates(above, below, masks, b, H, W, lane_cols=32, lanes=32):
+def band_candidates(above, below, masks, b, H, W, lane_cols=32, lanes=32, hcap=None):
     i0, i1 = 32 * b, min(32 * b + 31, H - 1)
     cand = set(k for k in range(W) if masks[b][k])
     win = lane_cols * lanes
     for w0 in range(0, W, win):
-        cand |= window_hull(above[b], i0, w0, lane_cols, lanes, W)
-        cand |= window_hull(below[b], i1, w0, lane_cols, lanes, W)
+        cand |= window_hull(above[b], i0, w0, lane_cols, lanes, W, hcap)
+        cand |= window_hull(below[b], i1, w0, lane_cols, lanes, W, hcap)
     return sorted(cand)
 
 
@@ -264,7 +274,7 @@ def fill(lst, i, W):
     return D, K, R
 
 
-def band_transform(img, take_new=False, cap=32, lane_cols=32, lanes=32):
+def band_transform(img, take_new=False, cap=32, lane_cols=32, lanes=32, hcap=None):
     """(D, K, R) maps of a plane via the band path; stats per row."""
     H, W = len(img), len(img[0])
     above, below, masks = carries(img, H, W)
@@ -272,7 +282,7 @@ def band_transform(img, take_new=False, cap=32, lane_cols=32, lanes=32):
     ncand = []
     st_all = {"spills": 0, "reloads": 0}
     for b in range((H + 31) // 32):
-        cand = band_candidates(above, below, masks, b, H, W, lane_cols, lanes)
+        cand = band_candidates(above, below, masks, b, H, W, lane_cols, lanes, hcap)
         ncand.append(len(cand))
         for i in range(32 * b, min(32 * b + 32, H)):
             lst, st = row_stack(i, b, cand, above, below, masks, W, take_new, cap)

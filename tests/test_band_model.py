@@ -41,7 +41,8 @@ def test_band_model_matches_brute_force(take_new):
         lane_cols = rnd.choice([1, 2, 3, 4, 8, 32])
         lanes = rnd.choice([1, 2, 4, 8, 32])
         cap = rnd.choice([1, 2, 3, 32])
-        D, K, R, _, _ = bm.band_transform(img, take_new, cap, lane_cols, lanes)
+        hcap = rnd.choice([None, 2, 3, 5])   # hull stacks that overflow: all valid columns
+        D, K, R, _, _ = bm.band_transform(img, take_new, cap, lane_cols, lanes, hcap)
         bD, bK, bR = bm.brute(img, take_new)
         assert D == bD, (it, mode, H, W)
         assert K == bK, (it, mode, H, W)

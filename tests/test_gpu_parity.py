@@ -368,80 +368,6 @@ def test_sharded_library_argument_errors(dfc):
         dfc.edt_sharded([dict(rank=0, img=img[:, :32], sqdist=sq)], 2, 64, 64)
 
 
-@pytest.fixture
-def stream_kernel(dfc):
-    dfc.set_row_kernel("stream")
-    yield dfc
-    dfc.set_row_kernel("default")
-
-
-@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (33, 97), (64, 64), (40, 1031), (70, 600), (3, 4100), (100, 33)])
-@pytest.mark.parametrize("density", [0.0, 0.002, 0.02, 0.3, 1.0])
-def test_streaming_row_kernel(stream_kernel, shape, density):
-    """The lane-per-row streaming stage 2 gives the same maps, labels, columns."""
-    img = oracle.random_image(shape[0], shape[1], density, 31 * shape[0] + shape[1] + int(density * 1000))
-    _check_edt(stream_kernel, img)
-
-
-def test_streaming_overflow_falls_back(stream_kernel):
-    """A horizontal object line far above equal-height parabolas keeps ~i entries
-    alive per row: rows beyond the ring capacity must be recomputed exactly."""
-    img = np.zeros((300, 257), np.uint8)
-    img[0, :] = 1
-    img[299, 100] = 1
-    _check_edt(stream_kernel, img)
-    img2 = np.zeros((200, 512), np.uint8)
-    img2[0, ::2] = 1
-    _check_edt(stream_kernel, img2)
-
-
-def test_streaming_batched_and_dual(stream_kernel):
-    import workloads
-    imgs = workloads.points_batch(40, 96, 128, 30, 5)
-    out = stream_kernel.edt_batched(_dev(imgs), dist=True, label=True)
-    img = workloads.discs(256, 384, 10, 3)
-    dual = stream_kernel.edt_dual(_dev(img))
-    torch.cuda.synchronize()
-    for b in range(0, 40, 7):
-        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
-        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
-    np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
-    np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
-
-
-@pytest.fixture
-def window_kernel(dfc):
-    dfc.set_row_kernel("window")
-    yield dfc
-    dfc.set_row_kernel("default")
-
-
-@pytest.mark.parametrize("shape", [(1, 1), (5, 7), (33, 97), (64, 64), (40, 1031), (70, 600), (3, 4100), (100, 33)])
-@pytest.mark.parametrize("density", [0.0, 0.002, 0.02, 0.3, 1.0])
-def test_window_row_kernel(window_kernel, shape, density):
-    """The outward-search stage 2 (k_rows_win.cu) gives the same maps, labels, columns."""
-    img = oracle.random_image(shape[0], shape[1], density, 17 * shape[0] + shape[1] + int(density * 1000))
-    _check_edt(window_kernel, img)
-
-
-def test_window_batched_dual_and_lines(window_kernel):
-    import workloads
-    imgs = workloads.points_batch(24, 96, 128, 30, 6)
-    out = window_kernel.edt_batched(_dev(imgs), dist=True, label=True)
-    img = workloads.discs(256, 384, 10, 4)
-    dual = window_kernel.edt_dual(_dev(img))
-    torch.cuda.synchronize()
-    for b in range(0, 24, 5):
-        np.testing.assert_array_equal(out["sqdist"][b].cpu().numpy(), oracle.to_i32(oracle.edt(imgs[b])))
-        np.testing.assert_array_equal(out["label"][b].cpu().numpy(), oracle.voronoi_labels(imgs[b], linear=True)[1])
-    np.testing.assert_array_equal(dual["sqdist_bg"].cpu().numpy(), oracle.to_i32(oracle.edt(img)))
-    np.testing.assert_array_equal(dual["sqdist_obj"].cpu().numpy(), oracle.to_i32(oracle.edt((img == 0).astype(np.uint8))))
-    lines = np.zeros((300, 257), np.uint8)
-    lines[0, :] = 1
-    lines[299, 100] = 1
-    _check_edt(window_kernel, lines)
-
-
 @pytest.mark.parametrize("gap", [1, 2, 17, 255, 256, 257, 600])
 def test_dense_rows_zero_split(dfc, gap):
     """Dense planes (most pixels are objects) with gaps of many lengths, next to
