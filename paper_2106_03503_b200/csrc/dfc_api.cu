@@ -211,6 +211,17 @@ struct BandSrc {
     bool sparse = false;  // the band path (k_rows_band.cu) takes the sparse planes
 };
 
+// Bands per candidate group of the band path (k_band_hull): DFC_BAND_GROUP
+// (tuning), default 4.
+int band_group() {
+    static const int g = [] {
+        const char* v = getenv("DFC_BAND_GROUP");
+        const int x = v ? atoi(v) : 0;
+        return x >= 1 && x <= 64 ? x : 4;
+    }();
+    return g;
+}
+
 // DFC_SPARSE=lr keeps the lane-per-row chunk scan (k_rows_lr, from the
 // nearest-row plane) for sparse planes instead of the band path (A/B)
 bool band_sparse_on() {
@@ -225,17 +236,21 @@ bool band_sparse_on() {
 // per-row stacks, fill into a's outputs.
 int launch_band_path(const RowArgs& a, const BandArgs& ba, bool take_new, cudaStream_t st) {
     BandArgs hb = ba;
-    hb.win = (int)round_up((ba.W + 31) / 32, 32);
-    const int64_t htasks = (int64_t)ba.nplanes * ba.nb * 2;
-    k_band_hull<<<(unsigned)((htasks + kHullWarps - 1) / kHullWarps), 32 * kHullWarps, 0, st>>>(hb);
+    const int hsm = hull_smem_bytes(ba.W);
+    cudaError_t e = cudaFuncSetAttribute(k_band_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+    if (e != cudaSuccess) return cuda_fail(e);
+    k_band_hull<<<dim3((unsigned)ba.ngroups, (unsigned)(2 * ba.nplanes)), hull_threads(ba.W), hsm, st>>>(hb);
     const int64_t tasks = (int64_t)ba.nplanes * ba.nb;
-    const unsigned rblocks = (unsigned)((tasks + kBandWarps - 1) / kBandWarps);
+    const int rsm = band_rows_smem_bytes();
+    const void* rfn = take_new ? (const void*)k_band_rows<true> : (const void*)k_band_rows<false>;
+    e = cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
+    if (e != cudaSuccess) return cuda_fail(e);
     if (take_new)
-        k_band_rows<true><<<rblocks, 32 * kBandWarps, 0, st>>>(hb);
+        k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(hb);
     else
-        k_band_rows<false><<<rblocks, 32 * kBandWarps, 0, st>>>(hb);
+        k_band_rows<false><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(hb);
     const int fsm = fill_smem_bytes();
-    cudaError_t e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+    e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
     if (e != cudaSuccess) return cuda_fail(e);
     const int64_t rows = (int64_t)ba.nplanes * ba.H;
     const int64_t fblocks = std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * 6);
@@ -383,8 +398,12 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
                              a.tile_cols >= W && row0 == 0;
         const bool lr_on = lr_ok && plane_counts != nullptr && !band_on;
         const int64_t Ww = (W + 31) / 32;
-        const size_t cand_bytes = band_on ? (size_t)round_up(nimg * band.nb * 2 * Ww * 4, 256) : 0;
-        const size_t nent_bytes = band_on ? (size_t)round_up(a.total_rows * 4, 256) : 0;
+        const int bgroup = band_group();
+        const int64_t ngroups = (band.nb + bgroup - 1) / bgroup;
+        const size_t cand_bytes = band_on ? (size_t)round_up(nimg * ngroups * 2 * Ww * 4, 256) : 0;
+        const size_t nent_bytes = band_on ? (size_t)round_up(a.total_rows * kBandWarps * 4, 256) +
+                                                (size_t)round_up(nimg * band.nb * (kBandWarps + 1) * 4, 256)
+                                          : 0;
         Scratch fl(st);
         const size_t flag_bytes = (size_t)round_up(a.total_rows, 256);
         const size_t list_bytes = (size_t)round_up((a.total_rows + 1) * 4, 256);
@@ -433,6 +452,8 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             ba.entr = reinterpret_cast<uint16_t*>(base + ent_bytes);
             ba.cand = reinterpret_cast<uint32_t*>(base + ent_bytes + entr_bytes);
             ba.nent = reinterpret_cast<int*>(base + ent_bytes + entr_bytes + cand_bytes);
+            ba.cbound = reinterpret_cast<int*>(base + ent_bytes + entr_bytes + cand_bytes +
+                                               (size_t)round_up(a.total_rows * kBandWarps * 4, 256));
             ba.counts = plane_counts;
             ba.Ws = lrWs;
             ba.H = (int)H;
@@ -445,6 +466,8 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             ba.nplanes = (int)nimg;
             ba.band0 = 0;
             ba.Hg = (int)H;
+            ba.group = bgroup;
+            ba.ngroups = (int)ngroups;
             ba.pts_gate = a.pts_gate;
             ba.all_planes = false;
             const int rc = launch_band_path(a, ba, take_new, st);

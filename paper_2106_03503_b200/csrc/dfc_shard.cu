@@ -127,6 +127,7 @@ struct ShardWork {
     uint32_t *cand, *ent;
     uint16_t* entr;
     int* nent;
+    int* cbound;
     cudaEvent_t colpass_done = nullptr, copies_done = nullptr;
 };
 
@@ -280,8 +281,10 @@ int dfc_edt_u8_sharded(const dfc_shard* shards, int n_local, int world, int64_t 
         const size_t o_rcnt = take((size_t)world * 8);
         const size_t o_fm = take((size_t)(w.nbq * Wp) * 4), o_fa = take((size_t)(w.nbq * Wp) * 2),
                      o_fb = take((size_t)(w.nbq * Wp) * 2), o_gc = take(8);
-        const size_t o_cand = take((size_t)(w.nbq * 2 * Ww) * 4), o_ent = take((size_t)(w.Hq * Ws) * 4),
-                     o_entr = take((size_t)(w.Hq * Ws) * 2), o_nent = take((size_t)w.Hq * 4);
+        const int64_t ngroups = (w.nbq + band_group() - 1) / band_group();
+        const size_t o_cand = take((size_t)(ngroups * 2 * Ww) * 4), o_ent = take((size_t)(w.Hq * Ws) * 4),
+                     o_entr = take((size_t)(w.Hq * Ws) * 2), o_nent = take((size_t)w.Hq * kBandWarps * 4),
+                     o_cb = take((size_t)(w.nbq * (kBandWarps + 1)) * 4);
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&w.mem), off, st);
         if (e != cudaSuccess) return fail(e);
         w.first = reinterpret_cast<uint16_t*>(w.mem + o_first);
@@ -297,6 +300,7 @@ int dfc_edt_u8_sharded(const dfc_shard* shards, int n_local, int world, int64_t 
         w.ent = reinterpret_cast<uint32_t*>(w.mem + o_ent);
         w.entr = reinterpret_cast<uint16_t*>(w.mem + o_entr);
         w.nent = reinterpret_cast<int*>(w.mem + o_nent);
+        w.cbound = reinterpret_cast<int*>(w.mem + o_cb);
         const int gl0 = g_launches;
         const int r = column_pass(h.d_img, 1, H, w.Wg, h.pitch_bytes, 0, polarity, 1, nullptr, w.first, w.last,
                                   (int)w.Wpg, st, nullptr, w.count, nullptr, w.bmask, false, true);
@@ -435,6 +439,7 @@ int dfc_edt_u8_sharded(const dfc_shard* shards, int n_local, int world, int64_t 
             ba.ent = w.ent;
             ba.entr = w.entr;
             ba.nent = w.nent;
+            ba.cbound = w.cbound;
             ba.Ws = Ws;
             ba.H = (int)w.Hq;
             ba.W = (int)W;
@@ -446,6 +451,8 @@ int dfc_edt_u8_sharded(const dfc_shard* shards, int n_local, int world, int64_t 
             ba.nplanes = 1;
             ba.band0 = (int)w.b0;
             ba.Hg = (int)H;
+            ba.group = band_group();
+            ba.ngroups = (int)((w.nbq + ba.group - 1) / ba.group);
             ba.pts_gate = false;
             ba.all_planes = true;
             const int r = launch_band_path(a, ba, false, st);

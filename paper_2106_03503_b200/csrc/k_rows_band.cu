@@ -45,10 +45,9 @@
 
 namespace dfc {
 
-constexpr int kHullWarps = 2;
-constexpr int kHullCap = 64;        // stack entries per hull window
-constexpr int kBandWarps = 2;       // k_band_rows: bands per CTA
-constexpr int kBandCap = 32;        // ring entries per lane (power of two)
+constexpr int kBandWarps = 8;       // k_band_rows: warps (column chunks) per band
+constexpr int kBandCap = 16;        // ring entries per lane (power of two)
+constexpr int kCandCap = 2048;      // candidates of a band listed in shared memory
 constexpr int kFillWarps = 4;
 constexpr int kFillCap = 1536;      // list entries staged per warp (k_rows_fill)
 
@@ -56,18 +55,19 @@ struct BandArgs {
     const uint32_t* bmask;   // [img][nb][Wp] bit r = row 32 b + r nonzero
     const uint16_t* above;   // [plane][nb][Wp] nearest object row above the band (kNoRow: none)
     const uint16_t* below;   // [plane][nb][Wp] nearest object row below the band
-    uint32_t* cand;          // [plane][nb][2][Ww] candidate columns (side 0 above + band, 1 below)
+    uint32_t* cand;          // [plane][group][2][Ww] candidate columns (side 0: above + the group's bands)
     const unsigned long long* counts;  // object pixels per plane
     uint32_t* ent;           // per row list: column | start << 16, at row * Ws
     uint16_t* entr;          // the entries' nearest object rows
-    int* nent;               // entries per row
+    int* nent;               // entries per (row, chunk)
+    int* cbound;             // per (plane, band): the chunks' first columns, then W
     int64_t Ws;              // list stride per row (entries)
     int H, W, Wp, nb, Ww, n_img, pol0, nplanes;
     // row stripes (the sharded path): local band b is global band band0 + b of
     // an image of Hg rows; plane p's local rows are [0, H).  Single images:
     // band0 = 0, Hg = H.
     int band0, Hg;
-    int win;                 // k_band_hull window: ceil(W / 32) rounded up to 32 (<= 1024)
+    int group, ngroups;      // bands per candidate group (k_band_hull), groups per plane
     bool pts_gate;           // point planes belong to k_rows_pts
     bool all_planes;         // every plane (the sharded path), not only the sparse ones
 };
@@ -78,207 +78,198 @@ __device__ __forceinline__ bool band_plane(const BandArgs& a, int p) {
 }
 
 // ---------------------------------------------------------------- hull filter
-// warp = (plane, band, side); lane = a window of `win` columns (the 32 windows
-// cover the row).  Each lane runs the monotone chain over its window (stack in
-// shared memory, top two entries cached in registers); then 5 levels of bridge
-// merges join the windows' hulls into the row's hull: a merge walks the lower
-// common tangent from the left group's last and the right group's first
-// vertex, trimming each window's surviving range [lo, hi) of its stack.  A
-// window whose stack would exceed kHullCap entries contributes every valid
-// column instead and sits out the merges (still a superset).
-struct HullSmem {
-    int32_t h[kHullCap][32];    // H of the stack entries (< 2^31, see below)
-    uint16_t c[kHullCap][32];   // their column offsets in the window
-    int lo[32], hi[32];         // surviving range of each window's stack
-};
-
-__global__ void __launch_bounds__(32 * kHullWarps) k_band_hull(BandArgs a) {
-    __shared__ HullSmem smem[kHullWarps];
-    HullSmem& sm = smem[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    const int64_t task = (int64_t)blockIdx.x * kHullWarps + (threadIdx.x >> 5);
-    if (task >= (int64_t)a.nplanes * a.nb * 2) return;
-    const int side = (int)(task & 1);
-    const int64_t pb = task >> 1;
-    const int p = (int)(pb / a.nb), b = (int)(pb - (int64_t)p * a.nb);
-    if (!band_plane(a, p)) return;  // warp-uniform
-    const int gb = a.band0 + b;      // global band
+// Bands come in groups of G (a.group).  For band b of group [b0, b0 + G):
+//   A-candidates(b) <= hullA(b0) + {columns with an object in bands b0 .. b-1}
+// because an object above b0 whose cell (among the objects above b) crosses
+// the line 32 b also crosses the nearer line 32 b0 (convexity, the same
+// argument as above); symmetrically below with the group's last band.  So the
+// group's candidates = hullA(first band) + hullB(last band) + every column
+// with an object in the group, and one CTA per (group, side) builds one hull:
+// thread = 32 columns, a monotone chain with the stack as a 32-bit mask, then
+// log2(threads) levels of bridge merges (walk the lower common tangent) over
+// the mask words in shared memory.  C5, G = 4: ~340 candidates per band.
+__global__ void __launch_bounds__(1024) k_band_hull(BandArgs a) {
+    extern __shared__ uint32_t hsm[];
+    uint32_t* M = hsm;                                      // hull bits per thread [T]
+    uint16_t* D = reinterpret_cast<uint16_t*>(hsm + blockDim.x);  // distance to the line per column [T*32]
+    const int T = blockDim.x, tid = threadIdx.x;
+    const int grp = blockIdx.x, p = blockIdx.y >> 1, side = blockIdx.y & 1;
+    if (!band_plane(a, p)) return;  // CTA-uniform
+    const int nb = a.nb;
+    const int bfirst = grp * a.group, blast = min(nb - 1, bfirst + a.group - 1);
+    const int kb = side ? blast : bfirst;  // the key band of this side
+    const int gb = a.band0 + kb;
     const int line = side ? min(32 * gb + 31, a.Hg - 1) : 32 * gb;
-    const int WIN = a.win;
-    const int k0 = lane * WIN, k1 = min(a.W, k0 + WIN);
-    const uint16_t* car = (side ? a.below : a.above) + ((int64_t)p * a.nb + b) * a.Wp;
-    // H_k = d^2 + k^2 <= (rows-1)^2 + (cols-1)^2 <= DFC_MAX_SQDIST < 2^31: int32;
-    // differences fit int32, times column differences (< 2^15): one IMAD.WIDE
+    constexpr uint16_t kNone = 0xFFFF;      // d <= rows - 1 <= 65534
+    // ---- distances to the line, coalesced (8 columns per 16-byte load) ----
+    const uint16_t* car = (side ? a.below : a.above) + ((int64_t)p * nb + kb) * a.Wp;
+    for (int q = tid; 8 * q < 32 * T; q += T) {
+        uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+        if (8 * q + 8 <= a.Wp) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(car) + q);
+            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            uint32_t lo = w[t] & 0xffffu, hi = w[t] >> 16;
+            const int k = 8 * q + 2 * t;
+            lo = (lo == kNoRow || k >= a.W) ? kNone : (side ? lo - line : line - lo);
+            hi = (hi == kNoRow || k + 1 >= a.W) ? kNone : (side ? hi - line : line - hi);
+            o[t] = lo | (hi << 16);
+        }
+        *reinterpret_cast<uint4*>(D + 8 * q) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    __syncthreads();
+    auto Hof = [&](int x) -> int {  // H_x = d^2 + x^2 < 2^31 (see below)
+        const int d = D[x];
+        return d * d + x * x;
+    };
+    // H <= (rows-1)^2 + (cols-1)^2 <= DFC_MAX_SQDIST < 2^31; differences fit
+    // int32, times column differences (< 2^15): one IMAD.WIDE each
     auto above_seg = [](int ka, int Ha, int kb, int Hb, int kc, int Hc) {
         return (long long)(Hb - Ha) * (kc - kb) > (long long)(Hc - Hb) * (kb - ka);
     };
-    // 32 carries of columns [c0, c0 + 32) (kNoRow past the row end)
-    auto load32 = [&](int c0, uint32_t (&w)[16]) {
-        if (c0 + 32 <= a.Wp) {
-            const uint4* q = reinterpret_cast<const uint4*>(car + c0);
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const uint4 x = __ldg(q + v);
-                w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
-            }
-        } else {
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const uint32_t lo = c0 + 2 * t < a.W ? (uint32_t)__ldg(car + c0 + 2 * t) : kNoRow;
-                const uint32_t hi = c0 + 2 * t + 1 < a.W ? (uint32_t)__ldg(car + c0 + 2 * t + 1) : kNoRow;
-                w[t] = lo | (hi << 16);
-            }
-        }
-    };
 
-    // ---- monotone chain over the window ----
-    int n = 0;
-    bool overflow = false;
-    int tk = 0, tH = 0, sk = 0, sH = 0;  // top and second entries
-    for (int c0 = k0; c0 < k1; c0 += 32) {
-        uint32_t w[16];
-        load32(c0, w);
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const uint32_t r = (w[t >> 1] >> (16 * (t & 1))) & 0xffffu;
-            const int k = c0 + t;
-            if (r == kNoRow || k >= k1 || overflow) continue;
-            const int d = side ? (int)r - line : line - (int)r;
-            const int H = d * d + k * k;
-            while (n >= 2 && above_seg(sk, sH, tk, tH, k, H)) {
-                --n;
-                tk = sk;
-                tH = sH;
-                if (n >= 2) {
-                    sk = k0 + sm.c[n - 2][lane];
-                    sH = sm.h[n - 2][lane];
-                }
-            }
-            if (n == kHullCap) {
-                overflow = true;
-                continue;
-            }
-            sm.h[n][lane] = H;
-            sm.c[n][lane] = (uint16_t)(k - k0);
-            ++n;
-            sk = tk;
-            sH = tH;
-            tk = k;
-            tH = H;
+    // ---- thread-local lower hull of 32 columns (monotone chain, stack = mask) ----
+    const int c0 = 32 * tid;
+    uint32_t st = 0;
+    int tc = -1, tH = 0;
+    for (int c = 0; c < 32; ++c) {
+        const int k = c0 + c;
+        if (D[k] == kNone) continue;
+        const int Hk = Hof(k);
+        while (st & (st - 1)) {  // at least two entries
+            const int sc = 31 - __clz(st & ((1u << tc) - 1u));
+            const int sH = Hof(c0 + sc);
+            if (!above_seg(c0 + sc, sH, c0 + tc, tH, k, Hk)) break;
+            st ^= 1u << tc;
+            tc = sc;
+            tH = sH;
         }
+        st |= 1u << c;
+        tc = c;
+        tH = Hk;
     }
-    sm.lo[lane] = 0;
-    sm.hi[lane] = overflow ? 0 : n;
-    __syncwarp();
+    M[tid] = st;
+    __syncthreads();
 
-    // ---- bridge merges: groups of g windows, leaders at multiples of 2g ----
-    for (int g = 1; g < 32; g <<= 1) {
-        if ((lane & (2 * g - 1)) == 0) {
-            const int lead = lane, mid = lane + g, end = lane + 2 * g;
-            int wa = -1, ia = 0, wb = -1, ib = 0;
+    // ---- bridge merges: groups of g threads, leaders at multiples of 2g ----
+    for (int g = 1; g < T; g <<= 1) {
+        if ((tid & (2 * g - 1)) == 0 && tid + g < T) {
+            const int lead = tid, mid = tid + g, end = min(T, tid + 2 * g);
+            int xa = -1, xb = -1;
             for (int l = mid - 1; l >= lead; --l)
-                if (sm.hi[l] > sm.lo[l]) { wa = l; ia = sm.hi[l] - 1; break; }
+                if (M[l]) { xa = 32 * l + 31 - __clz(M[l]); break; }
             for (int l = mid; l < end; ++l)
-                if (sm.hi[l] > sm.lo[l]) { wb = l; ib = sm.lo[l]; break; }
-            if (wa >= 0 && wb >= 0) {
-                int ka = wa * WIN + sm.c[ia][wa], Ha = sm.h[ia][wa];
-                int kb = wb * WIN + sm.c[ib][wb], Hb = sm.h[ib][wb];
+                if (M[l]) { xb = 32 * l + __ffs(M[l]) - 1; break; }
+            if (xa >= 0 && xb >= 0) {
+                int Ha = Hof(xa), Hb = Hof(xb);
                 for (;;) {
                     bool moved = false;
-                    for (;;) {  // the predecessor of a in the left group
-                        int wp = wa, ip = ia - 1;
-                        if (ip < sm.lo[wp]) {
-                            for (wp = wa - 1; wp >= lead && sm.hi[wp] <= sm.lo[wp]; --wp) {}
-                            if (wp < lead) break;
-                            ip = sm.hi[wp] - 1;
-                        }
-                        const int kp = wp * WIN + sm.c[ip][wp], Hp = sm.h[ip][wp];
-                        if (!above_seg(kp, Hp, ka, Ha, kb, Hb)) break;
-                        sm.hi[wa] = ia;  // a is the left group's last vertex
-                        wa = wp; ia = ip; ka = kp; Ha = Hp;
+                    for (;;) {  // the predecessor of xa in the left group
+                        int l = xa >> 5;
+                        uint32_t m = M[l] & ((1u << (xa & 31)) - 1u);
+                        while (!m && l > lead) m = M[--l];
+                        if (!m) break;
+                        const int xp = 32 * l + 31 - __clz(m);
+                        const int Hp = Hof(xp);
+                        if (!above_seg(xp, Hp, xa, Ha, xb, Hb)) break;
+                        M[xa >> 5] &= ~(1u << (xa & 31));
+                        xa = xp;
+                        Ha = Hp;
                         moved = true;
                     }
-                    for (;;) {  // the successor of b in the right group
-                        int ws = wb, is = ib + 1;
-                        if (is >= sm.hi[ws]) {
-                            for (ws = wb + 1; ws < end && sm.hi[ws] <= sm.lo[ws]; ++ws) {}
-                            if (ws >= end) break;
-                            is = sm.lo[ws];
-                        }
-                        const int ks = ws * WIN + sm.c[is][ws], Hs = sm.h[is][ws];
-                        if (!above_seg(ka, Ha, kb, Hb, ks, Hs)) break;
-                        sm.lo[wb] = ib + 1;  // b is the right group's first vertex
-                        wb = ws; ib = is; kb = ks; Hb = Hs;
+                    for (;;) {  // the successor of xb in the right group
+                        int l = xb >> 5;
+                        uint32_t m = (xb & 31) == 31 ? 0u : M[l] & ~((2u << (xb & 31)) - 1u);
+                        while (!m && l < end - 1) m = M[++l];
+                        if (!m) break;
+                        const int xs = 32 * l + __ffs(m) - 1;
+                        const int Hs = Hof(xs);
+                        if (!above_seg(xa, Ha, xb, Hb, xs, Hs)) break;
+                        M[xb >> 5] &= ~(1u << (xb & 31));
+                        xb = xs;
+                        Hb = Hs;
                         moved = true;
                     }
                     if (!moved) break;
                 }
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
+    uint32_t word = M[tid];
 
-    // ---- the window's candidate words (side 0 adds the band's object columns) ----
-    const int s = p / a.n_img, im = p - s * a.n_img;
-    const int pol = a.pol0 + s;
-    const int nrows = min(32, a.Hg - 32 * gb);
-    const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
-    const uint32_t* mrow = a.bmask + ((int64_t)im * a.nb + b) * a.Wp;
-    uint32_t* out = a.cand + (((int64_t)p * a.nb + b) * 2 + side) * a.Ww;
-    int idx = sm.lo[lane];
-    const int ihi = sm.hi[lane];
-    for (int c0 = k0; c0 < k1; c0 += 32) {
-        uint32_t z = 0;
-        while (idx < ihi && k0 + sm.c[idx][lane] < c0 + 32) {
-            z |= 1u << ((k0 + sm.c[idx][lane]) & 31);
-            ++idx;
-        }
-        if (overflow) {  // every valid column of the window
-            uint32_t w[16];
-            load32(c0, w);
-#pragma unroll
-            for (int t = 0; t < 32; ++t)
-                z |= (uint32_t)(((w[t >> 1] >> (16 * (t & 1))) & 0xffffu) != kNoRow) << t;
-        }
-        if (side == 0) {
+    // ---- side 0 adds every column with an object in the group's bands ----
+    if (side == 0 && c0 < a.W) {
+        const int s = p / a.n_img, im = p - s * a.n_img;
+        const int pol = a.pol0 + s;
+        for (int b = bfirst; b <= blast; ++b) {
+            const int gbb = a.band0 + b;
+            const int nrows = min(32, a.Hg - 32 * gbb);
+            const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
+            const uint32_t* mrow = a.bmask + ((int64_t)im * nb + b) * a.Wp;
             if (c0 + 32 <= a.Wp) {
                 const uint4* q = reinterpret_cast<const uint4*>(mrow + c0);
 #pragma unroll
                 for (int v = 0; v < 8; ++v) {
                     const uint4 x = __ldg(q + v);
-                    z |= (uint32_t)(pol_mask(x.x, pol, valid) != 0u) << (4 * v);
-                    z |= (uint32_t)(pol_mask(x.y, pol, valid) != 0u) << (4 * v + 1);
-                    z |= (uint32_t)(pol_mask(x.z, pol, valid) != 0u) << (4 * v + 2);
-                    z |= (uint32_t)(pol_mask(x.w, pol, valid) != 0u) << (4 * v + 3);
+                    word |= (uint32_t)(pol_mask(x.x, pol, valid) != 0u) << (4 * v);
+                    word |= (uint32_t)(pol_mask(x.y, pol, valid) != 0u) << (4 * v + 1);
+                    word |= (uint32_t)(pol_mask(x.z, pol, valid) != 0u) << (4 * v + 2);
+                    word |= (uint32_t)(pol_mask(x.w, pol, valid) != 0u) << (4 * v + 3);
                 }
             } else {
                 for (int c = 0; c < 32 && c0 + c < a.Wp; ++c)
-                    z |= (uint32_t)(pol_mask(__ldg(mrow + c0 + c), pol, valid) != 0u) << c;
+                    word |= (uint32_t)(pol_mask(__ldg(mrow + c0 + c), pol, valid) != 0u) << c;
             }
         }
-        if (k1 - c0 < 32) z &= (1u << (k1 - c0)) - 1u;  // columns past the row end
-        out[c0 >> 5] = z;
+        if (a.W - c0 < 32) word &= (1u << (a.W - c0)) - 1u;  // columns past the row end
     }
+    if (tid < a.Ww) a.cand[(((int64_t)p * a.ngroups + grp) * 2 + side) * a.Ww + tid] = word;
 }
 
+inline int hull_threads(int W) { return std::max(32, (int)(((W + 31) / 32 + 31) / 32 * 32)); }
+inline int hull_smem_bytes(int W) { const int T = hull_threads(W); return T * 4 + T * 32 * 2; }
+
 // ------------------------------------------------------------ per-row stacks
+// CTA = (plane, band), kBandWarps warps.  The band's candidates (the group's
+// words) are listed in shared memory with their band mask and carries, then
+// cut into kBandWarps chunks of equal candidate counts; chunk w covers the
+// columns [c0, c1) from its first candidate to the next chunk's.  Lane = row:
+// the owners of c0 - 1 and c1 - 1 (exact, by an outward search over the
+// candidate list that stops once the nearest unexamined column d has d^2 >
+// best) bound the candidates any column of the chunk can take (owners are
+// monotone in j under either tie rule, as in k_rows_lr.cu), and the
+// reference's stack algorithm runs over that range with the domain restricted
+// to [c0, c1): an empty stack pushes with start c0, a parabola starting past
+// c1 - 1 is not pushed (:218).  The top kBandCap entries of each stack live
+// in a shared-memory ring that spills its bottom to the row's list for the
+// chunk (global, at row * Ws + c0: a chunk's stack holds distinct starts in
+// [c0, c1), so the lists of a row never overlap) and reloads from it.  Bands
+// with more than kCandCap candidates run the whole row in one chunk, with the
+// candidates streamed 1024 at a time.
 struct BandSmem {
-    uint32_t ks[kBandCap][32];   // ring: column | start << 16
-    uint16_t rr[kBandCap][32];   // ring: the column's nearest object row
-    uint16_t cols[1024];         // candidate columns of one 32-word group
+    uint16_t col[kCandCap];      // the band's candidate columns, ascending
+    uint32_t msk[kCandCap];      // their band masks (raw: nonzero rows)
+    uint32_t car[kCandCap];      // their carries: above | below << 16
+    uint32_t ks[kBandWarps][kBandCap][32];  // rings: column | start << 16
+    uint16_t rr[kBandWarps][kBandCap][32];  // rings: the column's nearest object row
+    int warp_n[kBandWarps + 1];
+    int n;
 };
 
 template <bool TAKE_NEW>
 __global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
-    __shared__ BandSmem smem[kBandWarps];
-    BandSmem& sm = smem[threadIdx.x >> 5];
+    extern __shared__ uint4 band_raw[];
+    BandSmem& sm = *reinterpret_cast<BandSmem*>(band_raw);
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int MASK = kBandCap - 1;
-    const int lane = threadIdx.x & 31;
-    const int64_t task = (int64_t)blockIdx.x * kBandWarps + (threadIdx.x >> 5);
-    if (task >= (int64_t)a.nplanes * a.nb) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t task = blockIdx.x;
     const int p = (int)(task / a.nb), b = (int)(task - (int64_t)p * a.nb);
-    if (!band_plane(a, p)) return;  // warp-uniform
+    if (!band_plane(a, p)) return;  // CTA-uniform
     const int s = p / a.n_img, im = p - s * a.n_img;
     const int pol = a.pol0 + s;
     const int gb = a.band0 + b;  // global band; rows of the image [32 gb, 32 gb + nrows)
@@ -288,131 +279,245 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
     const uint32_t i = (uint32_t)(32 * gb + lane);  // global row
     const uint32_t upmask = 0xffffffffu >> (31 - lane);
     const int64_t row = (int64_t)p * a.H + 32 * b + lane;  // local row
-    uint32_t* gE = a.ent + (active ? row * a.Ws : 0);
-    uint16_t* gR = a.entr + (active ? row * a.Ws : 0);
-    const uint32_t* cA = a.cand + ((int64_t)p * a.nb + b) * 2 * a.Ww;
+    const uint32_t* cA = a.cand + ((int64_t)p * a.ngroups + b / a.group) * 2 * a.Ww;
     const uint32_t* cB = cA + a.Ww;
     const uint32_t* mrow = a.bmask + ((int64_t)im * a.nb + b) * a.Wp;
     const uint16_t* arow = a.above + ((int64_t)p * a.nb + b) * a.Wp;
     const uint16_t* brow = a.below + ((int64_t)p * a.nb + b) * a.Wp;
     const int W = a.W;
+    int* bounds = a.cbound + task * (kBandWarps + 1);
 
-    int n = 0, head = 0, ng = 0;  // ring entries head .. head+n-1; ng entries in the global list
-    int tk = 0, ts = 0;           // top entry
+    // ---- 1. the candidate list: a CTA prefix over the words ----
+    const int per = (a.Ww + blockDim.x - 1) / blockDim.x;  // words per thread, consecutive
+    const int w0 = tid * per, w1 = min(a.Ww, w0 + per);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(__ldg(cA + w) | __ldg(cB + w));
+    int pre = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, pre, o);
+        if (lane >= o) pre += v;
+    }
+    if (lane == 31) sm.warp_n[warp + 1] = pre;
+    __syncthreads();
+    if (tid == 0) {
+        sm.warp_n[0] = 0;
+        for (int w = 1; w <= kBandWarps; ++w) sm.warp_n[w] += sm.warp_n[w - 1];
+        sm.n = sm.warp_n[kBandWarps];
+    }
+    __syncthreads();
+    const int n = sm.n;
+    const bool streamed = n > kCandCap;
+    if (!streamed) {
+        int pos = sm.warp_n[warp] + pre - cnt;
+        for (int w = w0; w < w1; ++w)
+            for (uint32_t x = __ldg(cA + w) | __ldg(cB + w); x; x &= x - 1) {
+                const int k = 32 * w + __ffs(x) - 1;
+                sm.col[pos] = (uint16_t)k;
+                sm.msk[pos] = __ldg(mrow + k);
+                sm.car[pos] = (uint32_t)__ldg(arow + k) | ((uint32_t)__ldg(brow + k) << 16);
+                ++pos;
+            }
+    }
+    __syncthreads();
+    // chunk w: from the 32-column block of candidate w n / N to the next
+    // chunk's (aligned, so the fill's 16-byte stores stay aligned)
+    const int NC = streamed ? 1 : kBandWarps;
+    if (warp >= NC) return;
+    const int ilo = (int)((int64_t)warp * n / NC), ihi = (int)((int64_t)(warp + 1) * n / NC);
+    const int c0 = (warp == 0 || streamed || ilo >= n) ? (warp == 0 || streamed ? 0 : W) : (sm.col[ilo] & ~31);
+    const int c1 = (warp == NC - 1 || ihi >= n) ? W : (sm.col[ihi] & ~31);
+    if (lane == 0) {
+        bounds[warp] = c0;
+        if (warp == NC - 1)
+            for (int w = NC; w <= kBandWarps; ++w) bounds[w] = W;
+    }
+    if (c0 >= c1) {  // an empty chunk (fewer candidates than chunks)
+        if (active) a.nent[row * kBandWarps + warp] = 0;
+        return;
+    }
+
+    // nearest object row of a candidate column for this lane's row (upper on ties)
+    auto nearest = [&](uint32_t m, uint32_t c2) -> uint32_t {
+        const uint32_t mk = pol_mask(m, pol, valid);
+        const uint32_t up = mk & upmask, dn = mk >> lane;
+        const uint32_t ra = up ? (uint32_t)(32 * gb + 31 - __clz(up)) : (c2 & 0xffffu);
+        const uint32_t rb = dn ? (uint32_t)(i + __ffs(dn) - 1) : (c2 >> 16);
+        return pick_nearest(i, ra, rb);
+    };
+
+    uint32_t* gE = a.ent + (active ? row * a.Ws + c0 : 0);
+    uint16_t* gR = a.entr + (active ? row * a.Ws + c0 : 0);
+    uint32_t (*ks)[32] = sm.ks[warp];
+    uint16_t (*rr)[32] = sm.rr[warp];
+    int nst = 0, head = 0, ng = 0;  // ring entries head .. head+nst-1; ng entries in the list
+    int tk = 0, ts = 0;             // top entry
     uint32_t tg = 0;
+    const int cmax = c1 - 1;
 
+    // one candidate column m with nearest row r: pops, then a push (exact_edt.cpp:208-223)
     auto cand = [&](int m, uint32_t r) {
         const uint32_t av = i > r ? i - r : r - i;
         const uint32_t gm = av * av;
-        int start = 0;
+        int start = c0;
         for (;;) {
-            if (n == 0) {
-                if (ng == 0) break;  // empty stack: push with start 0
+            if (nst == 0) {
+                if (ng == 0) break;  // empty stack: push with start c0
                 --ng;                // reload the list's last entry as the ring's only one
                 const uint32_t e = gE[ng];
                 const uint16_t rk = gR[ng];
                 head = 0;
-                sm.ks[0][lane] = e;
-                sm.rr[0][lane] = rk;
-                n = 1;
+                ks[0][lane] = e;
+                rr[0][lane] = rk;
+                nst = 1;
                 tk = (int)(e & 0xffffu);
                 ts = (int)(e >> 16);
                 const uint32_t ak = i > rk ? i - rk : rk - i;
                 tg = ak * ak;
             }
-            // num = g_m - g_k + m^2 - k^2, |num| < 2^31; ts*den, (W-1)*den < 2^31
+            // num = g_m - g_k + m^2 - k^2, |num| < 2^31; ts*den, cmax*den < 2^31
             const int dm = m - tk;
             const int num = (int)gm - (int)tg + dm * (m + tk);
             const int den = 2 * dm;
             const int lim = ts * den;  // start <= js[idx]: pop (:214)
             if (TAKE_NEW ? num <= lim : num < lim) {
-                if (--n > 0) {
-                    const int idx = (head + n - 1) & MASK;
-                    const uint32_t e = sm.ks[idx][lane];
+                if (--nst > 0) {
+                    const int idx = (head + nst - 1) & MASK;
+                    const uint32_t e = ks[idx][lane];
                     tk = (int)(e & 0xffffu);
                     ts = (int)(e >> 16);
-                    const uint32_t rk = sm.rr[idx][lane];
+                    const uint32_t rk = rr[idx][lane];
                     const uint32_t ak = i > rk ? i - rk : rk - i;
                     tg = ak * ak;
                 }
                 continue;
             }
-            // push iff start <= W-1 (:218); 0 <= num, quotient < W <= 2^15
-            if (TAKE_NEW ? num > (W - 1) * den : num >= (W - 1) * den) return;
+            // push iff start <= c1-1 (:218 with cols -> c1); 0 <= num, quotient < W <= 2^15
+            if (TAKE_NEW ? num > cmax * den : num >= cmax * den) return;
             const uint32_t q = small_udiv((uint32_t)num, (uint32_t)den);
             // keep_old: floor(x)+1 ; take_new: ceil(x)   (:205)
             start = TAKE_NEW ? (int)(q + ((uint32_t)num != q * (uint32_t)den)) : (int)q + 1;
             break;
         }
-        if (n == kBandCap) {  // full ring: its bottom entry moves to the list
-            gE[ng] = sm.ks[head][lane];
-            gR[ng] = sm.rr[head][lane];
+        if (nst == kBandCap) {  // full ring: its bottom entry moves to the list
+            gE[ng] = ks[head][lane];
+            gR[ng] = rr[head][lane];
             ++ng;
             head = (head + 1) & MASK;
-            --n;
+            --nst;
         }
-        const int idx = (head + n) & MASK;
-        sm.ks[idx][lane] = (uint32_t)m | ((uint32_t)start << 16);
-        sm.rr[idx][lane] = (uint16_t)r;
-        ++n;
+        const int idx = (head + nst) & MASK;
+        ks[idx][lane] = (uint32_t)m | ((uint32_t)start << 16);
+        rr[idx][lane] = (uint16_t)r;
+        ++nst;
         tk = m;
         ts = start;
         tg = gm;
     };
 
-    // ---- the band's candidates, 32 mask words (<= 1024 columns) at a time ----
-    for (int w0 = 0; w0 < a.Ww; w0 += 32) {
-        const int w = w0 + lane;
-        const uint32_t cw = w < a.Ww ? (__ldg(cA + w) | __ldg(cB + w)) : 0u;
-        const int c = __popc(cw);
-        int pre = c;  // inclusive prefix
+    if (!streamed) {
+        // ---- 2. exact scan bounds: the owners of c0 - 1 and c1 - 1 ----
+        // index of the owner of column x among all candidates (outward search)
+        auto owner_idx = [&](int x) -> int {
+            int lo = 0, hi = n;  // first candidate >= x (warp-uniform binary search)
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((int)sm.col[mid] < x) lo = mid + 1; else hi = mid;
+            }
+            uint32_t best = kInfU;
+            int bi = -1, bk = 0;
+            int l = lo - 1, r = lo;
+            bool go = active;
+            for (;;) {
+                const int dl = l >= 0 ? x - (int)sm.col[l] : INT32_MAX;
+                const int dr = r < n ? (int)sm.col[r] - x : INT32_MAX;
+                const int d = min(dl, dr);
+                go = go && d != INT32_MAX && (uint32_t)d * (uint32_t)d <= best;
+                if (!__any_sync(FULL, go)) break;
+                const bool left = dl <= dr;  // warp-uniform: same x, same list
+                const int t = left ? l : r;
+                if (go) {
+                    const uint32_t rw = nearest(sm.msk[t], sm.car[t]);
+                    if (rw != kNoRow) {
+                        const uint32_t av = i > rw ? i - rw : rw - i;
+                        const uint32_t v = av * av + (uint32_t)d * (uint32_t)d;
+                        const int k = sm.col[t];
+                        if (v < best || (v == best && (TAKE_NEW ? k > bk : k < bk))) {
+                            best = v;
+                            bi = t;
+                            bk = k;
+                        }
+                    }
+                }
+                if (left) --l; else ++r;
+            }
+            return bi;
+        };
+        int iS = 0, iE = n - 1;
+        if (c0 > 0) iS = owner_idx(c0 - 1);
+        if (c1 < W) iE = owner_idx(c1 - 1);
+        // ---- 3. the stack over candidates [iS, iE] (a featureless row: no owner) ----
+        const int jS = __reduce_min_sync(FULL, (unsigned)(active && iS >= 0 ? iS : n));
+        const int jE = (int)__reduce_max_sync(FULL, (unsigned)(active && iE >= 0 ? iE + 1 : 0)) - 1;
+        for (int t = jS; t <= jE; ++t) {
+            if (!active || iS < 0 || t < iS || t > iE) continue;
+            const uint32_t r = nearest(sm.msk[t], sm.car[t]);
+            if (r != kNoRow) cand((int)sm.col[t], r);
+        }
+    } else {
+        // ---- dense band: the whole row, candidates streamed 1024 at a time ----
+        uint16_t* cols = sm.col;  // reused as the group's column list
+        for (int wg = 0; wg < a.Ww; wg += 32) {
+            const int w = wg + lane;
+            const uint32_t cw = w < a.Ww ? (__ldg(cA + w) | __ldg(cB + w)) : 0u;
+            const int c = __popc(cw);
+            int pre2 = c;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL, pre, o);
-            if (lane >= o) pre += v;
-        }
-        const int T = __shfl_sync(FULL, pre, 31);
-        int pos = pre - c;
-        for (uint32_t x = cw; x; x &= x - 1) sm.cols[pos++] = (uint16_t)(32 * w + __ffs(x) - 1);
-        __syncwarp();
-        for (int t0 = 0; t0 < T; t0 += 32) {
-            // lane loads candidate t0 + lane: column, band mask, both carries
-            uint32_t kk = 0, mm = 0, cc = 0;
-            if (t0 + lane < T) {
-                kk = sm.cols[t0 + lane];
-                mm = __ldg(mrow + kk);
-                cc = (uint32_t)__ldg(arow + kk) | ((uint32_t)__ldg(brow + kk) << 16);
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, pre2, o);
+                if (lane >= o) pre2 += v;
             }
-            const int nu = min(32, T - t0);
-            for (int u = 0; u < nu; ++u) {
-                const int m = (int)__shfl_sync(FULL, kk, u);
-                const uint32_t mk = pol_mask(__shfl_sync(FULL, mm, u), pol, valid);
-                const uint32_t c2 = __shfl_sync(FULL, cc, u);
-                if (!active) continue;
-                const uint32_t up = mk & upmask, dn = mk >> lane;
-                const uint32_t ra = up ? (uint32_t)(32 * gb + 31 - __clz(up)) : (c2 & 0xffffu);
-                const uint32_t rb = dn ? (uint32_t)(i + __ffs(dn) - 1) : (c2 >> 16);
-                const uint32_t r = pick_nearest(i, ra, rb);
-                if (r != kNoRow) cand(m, r);
+            const int T = __shfl_sync(FULL, pre2, 31);
+            int pos = pre2 - c;
+            for (uint32_t x = cw; x; x &= x - 1) cols[pos++] = (uint16_t)(32 * w + __ffs(x) - 1);
+            __syncwarp();
+            for (int t0 = 0; t0 < T; t0 += 32) {
+                uint32_t kk = 0, mm = 0, cc = 0;
+                if (t0 + lane < T) {
+                    kk = cols[t0 + lane];
+                    mm = __ldg(mrow + kk);
+                    cc = (uint32_t)__ldg(arow + kk) | ((uint32_t)__ldg(brow + kk) << 16);
+                }
+                const int nu = min(32, T - t0);
+                for (int u = 0; u < nu; ++u) {
+                    const int m = (int)__shfl_sync(FULL, kk, u);
+                    const uint32_t m2 = __shfl_sync(FULL, mm, u);
+                    const uint32_t c2 = __shfl_sync(FULL, cc, u);
+                    if (!active) continue;
+                    const uint32_t r = nearest(m2, c2);
+                    if (r != kNoRow) cand(m, r);
+                }
             }
+            __syncwarp();
         }
-        __syncwarp();
     }
     if (!active) return;
-    // ---- the final stack is the row's owner list ----
-    for (int e = 0; e < n; ++e) {
+    // ---- the final stack is the chunk's owner list ----
+    for (int e = 0; e < nst; ++e) {
         const int idx = (head + e) & MASK;
-        gE[ng] = sm.ks[idx][lane];
-        gR[ng] = sm.rr[idx][lane];
+        gE[ng] = ks[idx][lane];
+        gR[ng] = rr[idx][lane];
         ++ng;
     }
-    if (ng == 0) {  // featureless plane: one "no owner" entry
-        gE[0] = kLrInfK;
+    if (ng == 0) {  // a featureless row: one "no owner" entry
+        gE[0] = kLrInfK | ((uint32_t)c0 << 16);
         gR[0] = kNoRow;
         ng = 1;
     }
-    a.nent[row] = ng;
+    a.nent[row * kBandWarps + warp] = ng;
 }
+
+inline int band_rows_smem_bytes() { return (int)sizeof(BandSmem); }
 
 // ------------------------------------------------------------------- fill
 struct FillSmem {
@@ -428,62 +533,64 @@ __global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandA
     const int W = a.W;
     const int64_t total = (int64_t)a.nplanes * a.H;
     const int64_t nw = (int64_t)gridDim.x * kFillWarps;
-    const uint32_t sE_addr = (uint32_t)__cvta_generic_to_shared(sm.e);
-    const uint32_t sR_addr = (uint32_t)__cvta_generic_to_shared(sm.r);
     const bool donly = ra.D && !ra.S && !ra.LB && !ra.NC;
     for (int64_t row = (int64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5); row < total; row += nw) {
         const int p = (int)(row / a.H);
         if (!band_plane(a, p)) continue;  // warp-uniform
         const int64_t iR = row - (int64_t)p * a.H;
         const uint32_t gi = (uint32_t)(iR + 32 * a.band0);  // global row
-        const int nE = __ldcg(a.nent + row);
-        const uint32_t* gE = a.ent + row * a.Ws;
-        const uint16_t* gR = a.entr + row * a.Ws;
+        const int* bounds = a.cbound + ((int64_t)p * a.nb + iR / 32) * (kBandWarps + 1);
         int32_t* Drow = ra.D ? reinterpret_cast<int32_t*>(ra.D + p * ra.sD) + iR * W : nullptr;
         float* Srow = ra.S ? reinterpret_cast<float*>(ra.S + p * ra.sS) + iR * W : nullptr;
         int32_t* Lrow = ra.LB ? reinterpret_cast<int32_t*>(ra.LB + p * ra.sL) + iR * W : nullptr;
         int32_t* Nrow = ra.NC ? reinterpret_cast<int32_t*>(ra.NC + p * ra.sN) + iR * W : nullptr;
-        if (nE <= kFillCap) {
-            __syncwarp();
-            for (int q = lane; 4 * q < nE; q += 32)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sE_addr + 16u * q), "l"(gE + 4 * q));
-            for (int q = lane; 8 * q < nE; q += 32)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sR_addr + 16u * q), "l"(gR + 8 * q));
-            asm volatile("cp.async.wait_all;\n" ::: "memory");
-            __syncwarp();
-            if (donly)
-                lr_fill_row<true>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, 0, W, lane);
-            else
-                lr_fill_row<false>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, 0, W, lane);
-            continue;
-        }
-        // a long list (dense stretches): 32-column blocks straight from L2
-        int base = 0;
-        for (int b = 0; b < W; b += 32) {
-            const int idx = base + lane;
-            const uint32_t we = idx < nE ? __ldcg(gE + idx) : FULL;
-            const uint32_t wr = idx < nE ? (uint32_t)__ldcg(gR + idx) : kNoRow;
-            const int s = (int)(we >> 16);
-            const bool in = lane >= 1 && s <= b + 31;
-            const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
-            const int ow = __popc(Z & ((2u << lane) - 1u));
-            const uint32_t ke = __shfl_sync(FULL, we, ow);
-            const uint32_t kr = __shfl_sync(FULL, wr, ow);
-            const int j = b + lane;
-            if (j < W) {
-                const uint32_t k = ke & 0xffffu;
-                const bool inf = k == kLrInfK;
-                const uint32_t av = gi > kr ? gi - kr : kr - gi;
-                const int dj = j - (int)k;
-                const uint32_t d = inf ? (uint32_t)DFC_INF_I32 : av * av + (uint32_t)(dj * dj);
-                if (Drow) __stcs(Drow + j, (int32_t)d);
-                if (Srow) __stcs(Srow + j, dist_f32(d));
-                if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(kr * (uint32_t)W + k));
-                if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+        for (int w = 0; w < kBandWarps; ++w) {
+            const int c0 = __ldcg(bounds + w), c1 = __ldcg(bounds + w + 1);
+            if (c0 >= c1) continue;
+            const int nE = __ldcg(a.nent + row * kBandWarps + w);
+            const uint32_t* gE = a.ent + row * a.Ws + c0;
+            const uint16_t* gR = a.entr + row * a.Ws + c0;
+            if (nE <= kFillCap) {
+                __syncwarp();
+                for (int q = lane; q < nE; q += 32) {
+                    sm.e[q] = __ldcg(gE + q);
+                    sm.r[q] = __ldcg(gR + q);
+                }
+                __syncwarp();
+                if (donly)
+                    lr_fill_row<true>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+                else
+                    lr_fill_row<false>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+                continue;
             }
-            const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (__ldcg(gE + base + 32) >> 16) : 0xffffu;
-            base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
-                    ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
+            // a long list (dense stretches): 32-column blocks straight from L2
+            int base = 0;
+            for (int b = c0; b < c1; b += 32) {
+                const int idx = base + lane;
+                const uint32_t we = idx < nE ? __ldcg(gE + idx) : FULL;
+                const uint32_t wr = idx < nE ? (uint32_t)__ldcg(gR + idx) : kNoRow;
+                const int s = (int)(we >> 16);
+                const bool in = lane >= 1 && s <= b + 31;
+                const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
+                const int ow = __popc(Z & ((2u << lane) - 1u));
+                const uint32_t ke = __shfl_sync(FULL, we, ow);
+                const uint32_t kr = __shfl_sync(FULL, wr, ow);
+                const int j = b + lane;
+                if (j < c1) {
+                    const uint32_t k = ke & 0xffffu;
+                    const bool inf = k == kLrInfK;
+                    const uint32_t av = gi > kr ? gi - kr : kr - gi;
+                    const int dj = j - (int)k;
+                    const uint32_t d = inf ? (uint32_t)DFC_INF_I32 : av * av + (uint32_t)(dj * dj);
+                    if (Drow) __stcs(Drow + j, (int32_t)d);
+                    if (Srow) __stcs(Srow + j, dist_f32(d));
+                    if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(kr * (uint32_t)W + k));
+                    if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+                }
+                const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (__ldcg(gE + base + 32) >> 16) : 0xffffu;
+                base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
+                        ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
+            }
         }
     }
 }

@@ -258,6 +258,74 @@ def row_stack(i, b, cand, above, below, masks, W, take_new, cap=32):
     return gl, stats
 
 
+def owner_of(i, b, cand, above, below, masks, x, take_new):
+    """Exact owner (column) of column x of row i among the candidates (None: no
+    finite candidate) -- k_band_rows' outward search."""
+    best, bk = None, None
+    for m in cand:
+        r = nearest_row(i, b, masks[b][m], above[b][m], below[b][m])
+        if r is None:
+            continue
+        v = (i - r) ** 2 + (x - m) ** 2
+        if best is None or v < best or (v == best and (m > bk if take_new else m < bk)):
+            best, bk = v, m
+    return bk
+
+
+def row_stack_chunked(i, b, cand, above, below, masks, W, take_new, nch=8, cap=16):
+    """k_band_rows: the candidates cut into nch chunks of equal counts, chunk w
+    = columns [c0, c1) from the 32-column block of its first candidate; each
+    chunk runs the stack over [owner(c0-1), owner(c1-1)] with the domain
+    restricted to [c0, c1).  Returns [(c0, c1, list)]."""
+    n = len(cand)
+    out = []
+    bounds = []
+    for w in range(nch):
+        ilo, ihi = w * n // nch, (w + 1) * n // nch
+        c0 = 0 if w == 0 else (W if ilo >= n else cand[ilo] & ~31)
+        c1 = W if (w == nch - 1 or ihi >= n) else cand[ihi] & ~31
+        bounds.append((c0, c1))
+    for (c0, c1) in bounds:
+        if c0 >= c1:
+            continue
+        kS = owner_of(i, b, cand, above, below, masks, c0 - 1, take_new) if c0 > 0 else (cand[0] if cand else None)
+        kE = owner_of(i, b, cand, above, below, masks, c1 - 1, take_new) if c1 < W else (cand[-1] if cand else None)
+        sub = [] if kS is None else [m for m in cand if kS <= m <= kE]
+        gl, ring = [], []
+        for m in sub:
+            r = nearest_row(i, b, masks[b][m], above[b][m], below[b][m])
+            if r is None:
+                continue
+            gm = (i - r) ** 2
+            start, push = c0, True
+            while True:
+                if not ring:
+                    if not gl:
+                        break
+                    ring.append(gl.pop())
+                tk, ts, tr = ring[-1]
+                dm = m - tk
+                num = gm - (i - tr) ** 2 + dm * (m + tk)
+                den = 2 * dm
+                if (num <= ts * den) if take_new else (num < ts * den):
+                    ring.pop()
+                    continue
+                if (num > (c1 - 1) * den) if take_new else (num >= (c1 - 1) * den):
+                    push = False
+                    break
+                q = num // den
+                start = (q + (1 if num != q * den else 0)) if take_new else q + 1
+                break
+            if not push:
+                continue
+            if len(ring) == cap:
+                gl.append(ring.pop(0))
+            ring.append((m, start, r))
+        gl.extend(ring)
+        out.append((c0, c1, gl))
+    return out
+
+
 def fill(lst, i, W):
     """D and owner per column from a row list (None for a featureless row)."""
     if not lst:
@@ -272,6 +340,39 @@ def fill(lst, i, W):
         K.append(k)
         R.append(r)
     return D, K, R
+
+
+def band_transform_chunked(img, take_new=False, nch=8, cap=16, group=1):
+    """(D, K, R) via grouped candidates (k_band_hull: hullA of the group's first
+    band + hullB of its last + the group's object columns) and chunked stacks."""
+    H, W = len(img), len(img[0])
+    above, below, masks = carries(img, H, W)
+    nb = (H + 31) // 32
+    Dm, Km, Rm = [], [], []
+    for b in range(nb):
+        g0 = b // group * group
+        g1 = min(nb - 1, g0 + group - 1)
+        cand = set()
+        for bb in range(g0, g1 + 1):
+            cand |= set(k for k in range(W) if masks[bb][k])
+        cand |= window_hull(above[g0], 32 * g0, 0, W, 1, W)
+        cand |= window_hull(below[g1], min(32 * g1 + 31, H - 1), 0, W, 1, W)
+        cand = sorted(cand)
+        for i in range(32 * b, min(32 * b + 32, H)):
+            D, K, R = [None] * W, [None] * W, [None] * W
+            for (c0, c1, lst) in row_stack_chunked(i, b, cand, above, below, masks, W, take_new, nch, cap):
+                if not lst:
+                    continue
+                e = 0
+                for j in range(c0, c1):
+                    while e + 1 < len(lst) and lst[e + 1][1] <= j:
+                        e += 1
+                    k, _, r = lst[e]
+                    D[j], K[j], R[j] = (i - r) ** 2 + (j - k) ** 2, k, r
+            Dm.append(D)
+            Km.append(K)
+            Rm.append(R)
+    return Dm, Km, Rm
 
 
 def band_transform(img, take_new=False, cap=32, lane_cols=32, lanes=32, hcap=None):

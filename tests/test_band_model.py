@@ -33,7 +33,7 @@ def _img(rnd, H, W, dens, mode):
 @pytest.mark.parametrize("take_new", [False, True])
 def test_band_model_matches_brute_force(take_new):
     rnd = random.Random(11 + take_new)
-    for it in range(260):
+    for it in range(140):
         H = rnd.randint(1, 100)
         W = rnd.randint(1, 48)
         mode = rnd.choice(["bern", "bern", "rowline", "few", "lattice"])
@@ -78,3 +78,22 @@ def test_candidate_counts_are_small_on_sparse_tiles():
     _, _, _, ncand, st = bm.band_transform(img, False, 32, 32, 32)
     assert max(ncand) < W // 3
     assert st["spills"] == 0
+
+
+@pytest.mark.parametrize("take_new", [False, True])
+def test_band_model_grouped_chunked(take_new):
+    """Grouped candidates (hulls at the group's first / last band + the
+    group's object columns) and chunked stacks with exact scan bounds."""
+    rnd = random.Random(23 + take_new)
+    for it in range(60):
+        H = rnd.randint(1, 140)
+        W = rnd.randint(1, 100)
+        mode = rnd.choice(["bern", "bern", "rowline", "few", "lattice"])
+        img = _img(rnd, H, W, rnd.choice([0.0, 0.003, 0.02, 0.1, 0.4]), mode)
+        D, K, R = bm.band_transform_chunked(img, take_new, nch=rnd.choice([1, 2, 3, 8]),
+                                            cap=rnd.choice([1, 2, 16]), group=rnd.choice([1, 2, 4]))
+        bD, bK, bR = bm.brute(img, take_new)
+        assert D == bD, (it, mode, H, W)
+        assert K == bK, (it, mode, H, W)
+        if not take_new:
+            assert R == bR, (it, mode, H, W)
