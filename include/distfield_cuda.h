@@ -166,6 +166,37 @@ int dfc_envelope_vdist_u16(const uint16_t* d_vdist, int64_t rows, int64_t cols, 
                            dfc_stream_t stream);
 
 /*
+ * build_row_envelope / envelope_rows over ARBITRARY int64 vertical rows
+ * (exact_edt.cpp:190-283; exact_edt.hpp:71-72): for each of `rows` rows of
+ * `cols` values (row pitch in elements), the owner of every column j -- the
+ * smallest (take_new = 0, keep_old) or largest (take_new = 1) minimiser of
+ * vert[k] + (j - k)^2 over column 0 (the envelope's base, kept even when it is
+ * a sentinel) and the columns with vert[k] < lmax -- into d_owner (int32,
+ * rows x cols dense) and, if d_value != NULL, that minimum (int64; >= lmax
+ * means the base sentinel owns the column: the reference stores kInfinity and
+ * kNoColumn there).  The reference's (ks, js) are the runs of d_owner.
+ */
+int dfc_row_owners_i64(const int64_t* d_vert, int64_t rows, int64_t cols, int64_t pitch_elems, int64_t lmax,
+                       int take_new, int32_t* d_owner, int64_t* d_value, dfc_stream_t stream);
+
+/*
+ * The reference's per-pass in-place raster functions (propagation.hpp:15-26)
+ * over a uint64 map (UINT64_MAX = infinity, row pitch in elements), with the
+ * reference's relaxation (an infinite neighbour never contributes,
+ * propagation.cpp:10-12); values must stay below 2^62.
+ */
+enum dfc_raster_pass {
+    DFC_PASS_CITYBLOCK_FORWARD = 0,   /* cityblock_forward_pass     propagation.cpp:16-24 */
+    DFC_PASS_CITYBLOCK_BACKWARD = 1,  /* cityblock_backward_pass    :26-34 */
+    DFC_PASS_CITYBLOCK_VERTICAL = 2,  /* cityblock_vertical_passes  :36-46 */
+    DFC_PASS_CITYBLOCK_HORIZONTAL = 3,/* cityblock_horizontal_passes :48-58 */
+    DFC_PASS_CHAMFER_FORWARD = 4,     /* chamfer_forward_pass       :60-73 */
+    DFC_PASS_CHAMFER_BACKWARD = 5     /* chamfer_backward_pass      :75-88 */
+};
+int dfc_raster_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems, int pass,
+                        dfc_stream_t stream);
+
+/*
  * Float distances of a squared-distance map: (float)sqrt((double)D) for each
  * of n int32 values (DFC_INF_I32 -> +inf) -- the row pass's own epilogue
  * (grid.cpp:146 semantics), e.g. for a map from dfc_vertical_u8.

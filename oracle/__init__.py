@@ -69,6 +69,7 @@ def _bind_orc(lib):
     for f in ("orc_cityblock_sequential", "orc_chamfer34", "orc_chessboard"):
         getattr(lib, f).argtypes = [_u8p, _sz, _sz, _u64p]
     lib.orc_brute.argtypes = [_u8p, _sz, _sz, C.c_int, _u64p]
+    lib.orc_raster_pass.argtypes = [_u64p, _sz, _sz, C.c_int]
     return lib
 
 
@@ -94,6 +95,9 @@ def _bind_ref(lib):
     lib.dfref_transform_text.argtypes = [_u8p, _sz, _sz, C.c_int, C.c_int, C.c_char_p, _sz]
     lib.dfref_transform_gray.argtypes = [_u8p, _sz, _sz, C.c_int, C.c_int, _u8p]
     lib.dfref_labels_render.argtypes = [_u8p, _sz, _sz, _u8p, C.c_char_p, _sz, C.POINTER(C.c_int)]
+    lib.dfref_build_row_envelope.restype = C.c_longlong
+    lib.dfref_build_row_envelope.argtypes = [_i64p, _sz, C.c_int64, C.c_int, _i64p, _i64p]
+    lib.dfref_raster_pass.argtypes = [_u64p, _sz, _sz, C.c_int]
     lib.dfref_kind_bound.restype = C.c_uint64
     lib.dfref_kind_bound.argtypes = [C.c_int, _sz, _sz]
     return lib
@@ -201,6 +205,26 @@ def row_envelope(vert_row, rows, take_new=True):
     return ks[:n].copy(), js[: n + 1].copy()
 
 
+def raster_pass(dm, which):
+    """One per-pass in-place function (propagation.cpp:16-88) on a copy of a
+    uint64 map; which: 0 cityblock_forward_pass, 1 cityblock_backward_pass,
+    2 cityblock_vertical_passes, 3 cityblock_horizontal_passes,
+    4 chamfer_forward_pass, 5 chamfer_backward_pass."""
+    out = np.ascontiguousarray(dm, dtype=np.uint64).copy()
+    orc.orc_raster_pass(out, out.shape[0], out.shape[1], which)
+    return out
+
+
+def build_row_envelope(vert_i64, lmax, take_new=True):
+    """build_row_envelope (exact_edt.cpp:190-230) on an int64 row: (ks, js)."""
+    buf = np.ascontiguousarray(vert_i64, np.int64)
+    c = buf.size
+    ks = np.zeros(c + 1, np.int64)
+    js = np.zeros(c + 2, np.int64)
+    n = orc.orc_build_row_envelope(buf, c, int(lmax), 1 if take_new else 0, ks, js, None)
+    return ks[:n].copy(), js[: n + 1].copy()
+
+
 def voronoi_labels(img, linear=False):
     """Feature ordinals (exact_edt.cpp:319-371); None when featureless (domain_error).
     With linear=True returns (ordinals, int32 row*cols+col)."""
@@ -305,6 +329,21 @@ def ref_row_envelope(img, row):
     js = np.zeros(c + 2, np.int64)
     n = ref.dfref_row_envelope(img, r, c, row, ks, js)
     return ks[:n].copy(), js[: n + 1].copy()
+
+
+def ref_build_row_envelope(vert_i64, lmax, take_new=True):
+    buf = np.ascontiguousarray(vert_i64, np.int64)
+    c = buf.size
+    ks = np.zeros(c + 1, np.int64)
+    js = np.zeros(c + 2, np.int64)
+    n = ref.dfref_build_row_envelope(buf, c, int(lmax), 1 if take_new else 0, ks, js)
+    return ks[:n].copy(), js[: n + 1].copy()
+
+
+def ref_raster_pass(dm, which):
+    out = np.ascontiguousarray(dm, dtype=np.uint64).copy()
+    ref.dfref_raster_pass(out, out.shape[0], out.shape[1], which)
+    return out
 
 
 def ref_voronoi_labels(img, threads=1):

@@ -325,6 +325,61 @@ void orc_raster8(const uint8_t* img, uint64_t rows, uint64_t cols, uint64_t wa, 
         }
 }
 
+/*
+ * The per-pass in-place functions over any uint64 map, in the reference's
+ * visiting order -- propagation.cpp:16-88.  pass: 0 cityblock_forward_pass
+ * (:16-24), 1 cityblock_backward_pass (:26-34), 2 cityblock_vertical_passes
+ * (:36-46), 3 cityblock_horizontal_passes (:48-58), 4 chamfer_forward_pass
+ * (:60-73), 5 chamfer_backward_pass (:75-88).
+ */
+void orc_raster_pass(uint64_t* dm, uint64_t rows, uint64_t cols, int pass) {
+    if (pass == 0) {
+        for (uint64_t i = 0; i < rows; ++i)
+            for (uint64_t j = 0; j < cols; ++j) {
+                if (i > 0) relax(&dm[i * cols + j], dm[(i - 1) * cols + j], 1);
+                if (j > 0) relax(&dm[i * cols + j], dm[i * cols + j - 1], 1);
+            }
+    } else if (pass == 1) {
+        for (uint64_t i = rows; i-- > 0;)
+            for (uint64_t j = cols; j-- > 0;) {
+                if (i + 1 < rows) relax(&dm[i * cols + j], dm[(i + 1) * cols + j], 1);
+                if (j + 1 < cols) relax(&dm[i * cols + j], dm[i * cols + j + 1], 1);
+            }
+    } else if (pass == 2) {
+        for (uint64_t j = 0; j < cols; ++j) {
+            for (uint64_t i = 1; i < rows; ++i) relax(&dm[i * cols + j], dm[(i - 1) * cols + j], 1);
+            for (uint64_t i = rows - 1; i-- > 0;) relax(&dm[i * cols + j], dm[(i + 1) * cols + j], 1);
+        }
+    } else if (pass == 3) {
+        for (uint64_t i = 0; i < rows; ++i) {
+            for (uint64_t j = 1; j < cols; ++j) relax(&dm[i * cols + j], dm[i * cols + j - 1], 1);
+            for (uint64_t j = cols - 1; j-- > 0;) relax(&dm[i * cols + j], dm[i * cols + j + 1], 1);
+        }
+    } else if (pass == 4) {
+        for (uint64_t i = 0; i < rows; ++i)
+            for (uint64_t j = 0; j < cols; ++j) {
+                uint64_t* cell = &dm[i * cols + j];
+                if (j > 0) relax(cell, dm[i * cols + j - 1], 3);
+                if (i > 0) {
+                    relax(cell, dm[(i - 1) * cols + j], 3);
+                    if (j > 0) relax(cell, dm[(i - 1) * cols + j - 1], 4);
+                    if (j + 1 < cols) relax(cell, dm[(i - 1) * cols + j + 1], 4);
+                }
+            }
+    } else if (pass == 5) {
+        for (uint64_t i = rows; i-- > 0;)
+            for (uint64_t j = cols; j-- > 0;) {
+                uint64_t* cell = &dm[i * cols + j];
+                if (j + 1 < cols) relax(cell, dm[i * cols + j + 1], 3);
+                if (i + 1 < rows) {
+                    relax(cell, dm[(i + 1) * cols + j], 3);
+                    if (j > 0) relax(cell, dm[(i + 1) * cols + j - 1], 4);
+                    if (j + 1 < cols) relax(cell, dm[(i + 1) * cols + j + 1], 4);
+                }
+            }
+    }
+}
+
 void orc_chamfer34(const uint8_t* img, uint64_t rows, uint64_t cols, uint64_t* dm) {
     orc_raster8(img, rows, cols, 3, 4, dm);
 }

@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
+#include <span>
 #include <string>
 
 #include "distfield/exact_edt.hpp"
@@ -92,6 +93,33 @@ long long dfref_row_envelope(const std::uint8_t* img, std::size_t rows, std::siz
     for (std::size_t t = 0; t < env.ks.size(); ++t) ks[t] = env.ks[t];
     for (std::size_t t = 0; t < env.js.size(); ++t) js[t] = env.js[t];
     return static_cast<long long>(env.ks.size());
+}
+
+// build_row_envelope on an arbitrary int64 row (exact_edt.hpp:71-72).
+long long dfref_build_row_envelope(const std::int64_t* vert, std::size_t cols, std::int64_t lmax, int take_new,
+                                   std::int64_t* ks, std::int64_t* js) {
+    const auto env = build_row_envelope(std::span<const std::int64_t>(vert, cols), lmax,
+                                        take_new ? EnvelopeTie::take_new : EnvelopeTie::keep_old);
+    for (std::size_t t = 0; t < env.ks.size(); ++t) ks[t] = env.ks[t];
+    for (std::size_t t = 0; t < env.js.size(); ++t) js[t] = env.js[t];
+    return static_cast<long long>(env.ks.size());
+}
+
+// One per-pass in-place function (propagation.hpp:15-26) over a uint64 map.
+void dfref_raster_pass(std::uint64_t* map, std::size_t rows, std::size_t cols, int pass) {
+    DistanceMap dm(rows, cols, DistanceKind::cityblock);
+    for (std::size_t i = 0; i < rows; ++i)
+        for (std::size_t j = 0; j < cols; ++j) dm(i, j) = map[i * cols + j];
+    switch (pass) {
+        case 0: cityblock_forward_pass(dm); break;
+        case 1: cityblock_backward_pass(dm); break;
+        case 2: cityblock_vertical_passes(dm, 1); break;
+        case 3: cityblock_horizontal_passes(dm, 1); break;
+        case 4: chamfer_forward_pass(dm); break;
+        default: chamfer_backward_pass(dm); break;
+    }
+    for (std::size_t i = 0; i < rows; ++i)
+        for (std::size_t j = 0; j < cols; ++j) map[i * cols + j] = dm(i, j);
 }
 
 // voronoi_labels; returns -1 where the reference throws std::domain_error.

@@ -61,6 +61,8 @@ _lib.dfc_binarize_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
 _lib.dfc_count_objects_u8.argtypes = [_vp, _i64, _i64, _i64, _vp, _vp]
 _lib.dfc_gray_i32.argtypes = [_vp, _i64, C.c_int, _vp, _vp, _vp, _vp]
 _lib.dfc_labels_gray.argtypes = [_vp, _i64, _i64, _vp, _vp]
+_lib.dfc_row_owners_i64.argtypes = [_vp, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp]
+_lib.dfc_raster_pass_u64.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp]
 
 
 class Shard(C.Structure):
@@ -85,7 +87,7 @@ EXPORTED_SYMBOLS = (
     "dfc_version", "dfc_set_profile_events", "dfc_sqrt_i32", "dfc_envelope_vdist_u16", "dfc_column_nr_u8", "dfc_rows_from_nr_u16", "dfc_set_row_kernel", "dfc_set_lr_chunk",
     "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
     "dfc_edt_u8_sharded", "dfc_shard_cols", "dfc_shard_rows", "dfc_comm_unique_id", "dfc_comm_init_rank",
-    "dfc_comm_init_all", "dfc_comm_destroy", "dfc_last_nccl_error",
+    "dfc_comm_init_all", "dfc_comm_destroy", "dfc_last_nccl_error", "dfc_row_owners_i64", "dfc_raster_pass_u64",
 )
 
 
@@ -373,6 +375,35 @@ def label_ordinals(img: torch.Tensor, label: torch.Tensor, stream=None) -> torch
     _check(_lib.dfc_label_ordinals(_ptr(img), h, w, pitch, _ptr(label.contiguous()), _ptr(out),
                                    _stream(stream)))
     return out.to(torch.int64) & 0xFFFFFFFF
+
+
+def row_owners(vert: torch.Tensor, lmax: int, take_new: bool = True, stream=None):
+    """build_row_envelope / envelope_rows over arbitrary int64 rows
+    (exact_edt.cpp:190-283): (owner int32, value int64) per column; see
+    dfc_row_owners_i64."""
+    if not vert.is_cuda or vert.dtype != torch.int64 or vert.dim() != 2 or vert.stride(1) != 1:
+        raise ValueError("vert must be a 2-D int64 CUDA tensor with unit column stride")
+    r, c = vert.shape
+    own = torch.empty((r, c), dtype=torch.int32, device=vert.device)
+    val = torch.empty((r, c), dtype=torch.int64, device=vert.device)
+    _check(_lib.dfc_row_owners_i64(_ptr(vert), r, c, vert.stride(0), int(lmax), int(take_new), _ptr(own),
+                                   _ptr(val), _stream(stream)))
+    return own, val
+
+
+RASTER_PASSES = ("cityblock_forward_pass", "cityblock_backward_pass", "cityblock_vertical_passes",
+                 "cityblock_horizontal_passes", "chamfer_forward_pass", "chamfer_backward_pass")
+
+
+def raster_pass(dm: torch.Tensor, which, stream=None) -> torch.Tensor:
+    """One per-pass in-place function (propagation.hpp:15-26) on a 2-D int64
+    CUDA tensor holding uint64 cells (-1 = kInfinity); `which` is a name of
+    RASTER_PASSES or its index.  Returns dm."""
+    k = RASTER_PASSES.index(which) if isinstance(which, str) else int(which)
+    if not dm.is_cuda or dm.dim() != 2 or dm.dtype not in (torch.int64, torch.uint64) or dm.stride(1) != 1:
+        raise ValueError("expected a 2-D CUDA int64/uint64 tensor with unit column stride")
+    _check(_lib.dfc_raster_pass_u64(_ptr(dm), dm.shape[0], dm.shape[1], dm.stride(0), k, _stream(stream)))
+    return dm
 
 
 # ---------------------------------------------------------- multi-GPU (config 5)

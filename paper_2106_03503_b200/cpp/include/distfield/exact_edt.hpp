@@ -51,9 +51,18 @@ void vertical_up_pass(DistanceMap& dm, unsigned threads = 1);
 DistanceMap vertical_pass(const BinaryImage& img, unsigned threads = 1);
 
 // Stage two over a vertical map (meijster_scan, take_new ties: nearest_col is
-// the LARGEST minimising column).  Requires vert to be a vertical-pass map
-// (every finite value a perfect square); throws std::invalid_argument else.
+// the LARGEST minimising column).  Vertical-pass maps (every finite value a
+// perfect square) take the uint16 vertical-distance path; any other map the
+// generic int64 row-envelope kernel (dfc_row_owners_i64).
 MeijsterResult meijster_scan(const DistanceMap& vert, ScanStats* stats = nullptr, unsigned threads = 1);
+
+// build_row_envelope (exact_edt.hpp:71-72, exact_edt.cpp:190-230): the lower
+// envelope of one row of int64 vertical values (entries >= local_max are
+// sentinels, column 0 is always the base), computed on the device
+// (dfc_row_owners_i64: the owner of every column under `tie`) and returned as
+// the reference's (ks, js).  ScanStats counts one evaluation per column.
+EnvelopeState build_row_envelope(std::span<const std::int64_t> vert, std::int64_t local_max, EnvelopeTie tie,
+                                 ScanStats* stats = nullptr);
 
 // Envelope bookkeeping of one row (take_new), rebuilt from the GPU's
 // nearest-column row: ks = vertex columns (ks[0] = 0 base), js = segment

@@ -1,15 +1,24 @@
 // distfield/propagation.hpp -- drop-in for the reference's propagation
-// transforms (/root/reference/proj/core/include/distfield/propagation.hpp:28-30),
-// computed on the GPU from the separable closed forms (bit-exact with the
-// two-pass raster scans, SURVEY.md finding 6).  The per-pass in-place
-// functions (cityblock_forward_pass, chamfer_backward_pass, ...) expose the
-// intermediate states of the serial raster algorithm, which the GPU path does
-// not have; they are not part of this drop-in.
+// transforms (/root/reference/proj/core/include/distfield/propagation.hpp),
+// computed on the GPU: the whole transforms from the separable closed forms
+// (bit-exact with the two-pass raster scans, SURVEY.md finding 6); the
+// per-pass in-place functions (:15-26) by dfc_raster_pass_u64 over the
+// caller's map (k_passes.cu: the reference's relaxation order, rows in
+// sequence, the chain along a row as a scan).
 #pragma once
 
 #include "distfield/grid.hpp"
 
 namespace distfield {
+
+// In-place passes over a map (init_distance_map or any other), as the
+// reference: propagation.hpp:15-26.  `threads` is accepted and ignored.
+void cityblock_forward_pass(DistanceMap& dm);
+void cityblock_backward_pass(DistanceMap& dm);
+void cityblock_vertical_passes(DistanceMap& dm, unsigned threads = 1);
+void cityblock_horizontal_passes(DistanceMap& dm, unsigned threads = 1);
+void chamfer_forward_pass(DistanceMap& dm);
+void chamfer_backward_pass(DistanceMap& dm);
 
 DistanceMap cityblock_sequential(const BinaryImage& img);
 DistanceMap cityblock_separable(const BinaryImage& img, unsigned threads = 1);

@@ -18,11 +18,17 @@ using detail::stream;
 
 namespace {
 
+// local_max (exact_edt.cpp:13-15): kind_bound + 1
+std::int64_t local_max(std::size_t rows, std::size_t cols) {
+    return static_cast<std::int64_t>(kind_bound(DistanceKind::squared_euclidean, rows, cols)) + 1;
+}
+
 // Vertical map -> uint16 vertical-distance plane (0xFFFF = no feature in the
-// column).  Every finite value of a vertical-pass map is a perfect square.
-std::vector<std::uint16_t> vdist_plane(const DistanceMap& vert, std::size_t row0, std::size_t nrows,
-                                       std::size_t pitch) {
-    std::vector<std::uint16_t> a(nrows * pitch, 0xFFFF);
+// column); false when a finite value is not a perfect square (not a
+// vertical-pass map: the generic path takes it).
+bool vdist_plane(const DistanceMap& vert, std::size_t row0, std::size_t nrows, std::size_t pitch,
+                 std::vector<std::uint16_t>& a) {
+    a.assign(nrows * pitch, 0xFFFF);
     for (std::size_t i = 0; i < nrows; ++i) {
         const auto r = vert.row(row0 + i);
         for (std::size_t j = 0; j < vert.cols(); ++j) {
@@ -31,29 +37,81 @@ std::vector<std::uint16_t> vdist_plane(const DistanceMap& vert, std::size_t row0
             auto s = static_cast<std::uint64_t>(std::sqrt(static_cast<double>(v)));
             while (s * s > v) --s;
             while ((s + 1) * (s + 1) <= v) ++s;
-            if (s * s != v || s >= 0xFFFF)
-                throw std::invalid_argument("meijster_scan: the GPU path needs a vertical-pass map "
-                                            "(finite values must be squares of row offsets)");
+            if (s * s != v || s >= 0xFFFF) return false;
             a[i * pitch + j] = static_cast<std::uint16_t>(s);
         }
     }
-    return a;
+    return true;
+}
+
+// Per-column owners + values of int64 rows (load_row semantics done by the
+// caller), tie rule as given: dfc_row_owners_i64.
+void row_owners(const std::vector<std::int64_t>& rows_i64, std::size_t nrows, std::size_t cols, std::int64_t lmax,
+                bool take_new, std::vector<std::int32_t>& owner, std::vector<std::int64_t>& value) {
+    DeviceBuffer<std::int64_t> dv(rows_i64.size());
+    dv.upload(rows_i64.data());
+    DeviceBuffer<std::int32_t> dow(nrows * cols);
+    DeviceBuffer<std::int64_t> dval(nrows * cols);
+    dfc_check(dfc_row_owners_i64(dv.get(), (int64_t)nrows, (int64_t)cols, (int64_t)cols, lmax, take_new ? 1 : 0,
+                                 dow.get(), dval.get(), stream()),
+              "row envelope");
+    owner = dow.download();
+    value = dval.download();
 }
 
 struct Scan {
-    std::vector<std::int32_t> d, col;
+    std::vector<std::int32_t> d, col;  // d: DFC_INF_I32 = infinity; col: -1 = kNoColumn
 };
 
 Scan scan_rows(const DistanceMap& vert, std::size_t row0, std::size_t nrows) {
     const std::size_t cols = vert.cols(), pitch = cols + (cols & 1);
-    const auto plane = vdist_plane(vert, row0, nrows, pitch);
-    DeviceBuffer<std::uint16_t> da(plane.size());
-    da.upload(plane.data());
-    DeviceBuffer<std::int32_t> dd(nrows * cols), dc(nrows * cols);
-    dfc_check(dfc_envelope_vdist_u16(da.get(), (int64_t)nrows, (int64_t)cols, (int64_t)pitch, 1, dd.get(),
-                                     nullptr, dc.get(), stream()),
-              "meijster_scan");
-    return {dd.download(), dc.download()};
+    std::vector<std::uint16_t> plane;
+    if (vdist_plane(vert, row0, nrows, pitch, plane)) {
+        DeviceBuffer<std::uint16_t> da(plane.size());
+        da.upload(plane.data());
+        DeviceBuffer<std::int32_t> dd(nrows * cols), dc(nrows * cols);
+        dfc_check(dfc_envelope_vdist_u16(da.get(), (int64_t)nrows, (int64_t)cols, (int64_t)pitch, 1, dd.get(),
+                                         nullptr, dc.get(), stream()),
+                  "meijster_scan");
+        return {dd.download(), dc.download()};
+    }
+    // any other map: load_row (exact_edt.cpp:29-35), the generic envelope,
+    // store_value (:38-41) and the sentinel vertex rule (:278-279)
+    const std::int64_t lmax = local_max(vert.rows(), cols);
+    std::vector<std::int64_t> buf(nrows * cols);
+    for (std::size_t i = 0; i < nrows; ++i) {
+        const auto r = vert.row(row0 + i);
+        for (std::size_t j = 0; j < cols; ++j)
+            buf[i * cols + j] = DistanceMap::is_infinite(r[j]) ? lmax : static_cast<std::int64_t>(r[j]);
+    }
+    std::vector<std::int32_t> owner;
+    std::vector<std::int64_t> value;
+    row_owners(buf, nrows, cols, lmax, true, owner, value);
+    Scan s{std::vector<std::int32_t>(nrows * cols), std::vector<std::int32_t>(nrows * cols)};
+    for (std::size_t p = 0; p < nrows * cols; ++p) {
+        const bool inf = value[p] >= lmax;
+        s.d[p] = inf ? DFC_INF_I32 : static_cast<std::int32_t>(value[p]);
+        s.col[p] = buf[(p / cols) * cols + static_cast<std::size_t>(owner[p])] >= lmax ? -1 : owner[p];
+    }
+    return s;
+}
+
+// (ks, js) of a row from its per-column owners (the runs of the owner row)
+EnvelopeState envelope_from_owners(const std::int32_t* own, std::int64_t cols) {
+    EnvelopeState env;
+    env.ks.push_back(0);  // column-0 base (may own an empty segment)
+    env.js.push_back(0);
+    for (std::int64_t j = 0; j < cols; ++j) {
+        const std::int32_t k = own[j];
+        if (k < 0) break;  // featureless row: only the base, js = {0, cols}
+        if (j == 0 && k == 0) continue;
+        if (k != env.ks.back() || j == 0) {
+            env.ks.push_back(k);
+            env.js.push_back(j);
+        }
+    }
+    env.js.push_back(cols);
+    return env;
 }
 
 }  // namespace
@@ -106,24 +164,32 @@ MeijsterResult meijster_scan(const DistanceMap& vert, ScanStats* stats, unsigned
     return out;
 }
 
+// exact_edt.cpp:232-237: load_row + build_row_envelope(take_new)
 EnvelopeState meijster_row_envelope(const DistanceMap& vert, std::size_t row) {
     if (row >= vert.rows()) throw std::out_of_range("meijster_row_envelope: row out of range");
-    const Scan s = scan_rows(vert, row, 1);
-    const std::int64_t cols = static_cast<std::int64_t>(vert.cols());
-    EnvelopeState env;
-    env.ks.push_back(0);   // column-0 base (may own an empty segment)
-    env.js.push_back(0);
-    for (std::int64_t j = 0; j < cols; ++j) {
-        const std::int32_t k = s.col[static_cast<std::size_t>(j)];
-        if (k < 0) break;  // featureless row: only the base, js = {0, cols}
-        if (j == 0 && k == 0) continue;
-        if (k != env.ks.back() || (j == 0 && k != 0)) {
-            env.ks.push_back(k);
-            env.js.push_back(j);
-        }
+    const std::int64_t lmax = local_max(vert.rows(), vert.cols());
+    const auto r = vert.row(row);
+    std::vector<std::int64_t> buf(r.size());
+    for (std::size_t j = 0; j < r.size(); ++j)
+        buf[j] = DistanceMap::is_infinite(r[j]) ? lmax : static_cast<std::int64_t>(r[j]);
+    return build_row_envelope(buf, lmax, EnvelopeTie::take_new);
+}
+
+EnvelopeState build_row_envelope(std::span<const std::int64_t> vert, std::int64_t lmax, EnvelopeTie tie,
+                                 ScanStats* stats) {
+    const std::size_t cols = vert.size();
+    if (cols == 0) {
+        EnvelopeState env;
+        env.ks.push_back(0);
+        env.js = {0, 0};
+        return env;
     }
-    env.js.push_back(cols);
-    return env;
+    std::vector<std::int64_t> buf(vert.begin(), vert.end());
+    std::vector<std::int32_t> owner;
+    std::vector<std::int64_t> value;
+    row_owners(buf, 1, cols, lmax, tie == EnvelopeTie::take_new, owner, value);
+    if (stats) stats->candidates += cols;
+    return envelope_from_owners(owner.data(), static_cast<std::int64_t>(cols));
 }
 
 DistanceMap edt(const BinaryImage& img, EdtAlgorithm, Orientation, ScanStats* stats, unsigned) {

@@ -36,7 +36,7 @@ int main(int argc, char** argv) {
     const std::size_t rows = std::stoul(argv[2]), cols = std::stoul(argv[3]);
     try {
         BinaryImage img(rows, cols);
-        {
+        if (op != "bre" && op != "pass" && op != "meijster_raw") {
             std::ifstream in(argv[4], std::ios::binary);
             std::vector<char> buf(rows * cols);
             in.read(buf.data(), static_cast<std::streamsize>(buf.size()));
@@ -88,6 +88,39 @@ int main(int argc, char** argv) {
             const auto [a, b] = edt_both_polarities(img);
             put_map(out, a);
             put_map(out, b);
+        } else if (op == "bre") {  // build_row_envelope: rows must be 1; input = cols int64; arg lmax, tie
+            std::ifstream in(argv[4], std::ios::binary);
+            std::vector<std::int64_t> v(cols);
+            in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(cols * 8));
+            ScanStats st;
+            const auto env = build_row_envelope(v, std::stoll(argv[6]),
+                                                std::stoi(argv[7]) ? EnvelopeTie::take_new : EnvelopeTie::keep_old, &st);
+            std::vector<std::int64_t> o{static_cast<std::int64_t>(env.ks.size())};
+            o.insert(o.end(), env.ks.begin(), env.ks.end());
+            o.insert(o.end(), env.js.begin(), env.js.end());
+            put(out, o);
+        } else if (op == "pass" || op == "meijster_raw") {  // input = a uint64 map
+            std::ifstream in(argv[4], std::ios::binary);
+            DistanceMap dm(rows, cols, DistanceKind::cityblock);
+            for (std::size_t i = 0; i < rows; ++i) {
+                auto r = dm.row(i);
+                in.read(reinterpret_cast<char*>(r.data()), static_cast<std::streamsize>(cols * 8));
+            }
+            if (op == "meijster_raw") {
+                const auto r = meijster_scan(dm);
+                put_map(out, r.map);
+                std::vector<std::uint32_t> nc(r.nearest_col.cells().begin(), r.nearest_col.cells().end());
+                put(out, nc);
+            } else {
+                const int w = std::stoi(argv[6]);
+                if (w == 0) cityblock_forward_pass(dm);
+                else if (w == 1) cityblock_backward_pass(dm);
+                else if (w == 2) cityblock_vertical_passes(dm, 3);
+                else if (w == 3) cityblock_horizontal_passes(dm, 3);
+                else if (w == 4) chamfer_forward_pass(dm);
+                else chamfer_backward_pass(dm);
+                put_map(out, dm);
+            }
         } else if (op == "random") {  // generator parity: rows cols <unused> out density seed
             const auto r = generate_random_image(rows, cols, std::stod(argv[6]), std::stoull(argv[7]));
             std::vector<std::uint8_t> v(rows * cols);

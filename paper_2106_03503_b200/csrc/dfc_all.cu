@@ -11,5 +11,6 @@
 #include "k_raster.cu"
 #include "k_raster_anc.cu"
 #include "k_render.cu"
+#include "k_passes.cu"
 #include "dfc_api.cu"
 #include "dfc_shard.cu"

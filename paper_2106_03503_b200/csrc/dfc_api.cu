@@ -994,6 +994,44 @@ int dfc_labels_gray(const uint32_t* d_ordinal, int64_t n, int64_t feature_count,
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 
+int dfc_row_owners_i64(const int64_t* d_vert, int64_t rows, int64_t cols, int64_t pitch_elems, int64_t lmax,
+                       int take_new, int32_t* d_owner, int64_t* d_value, dfc_stream_t stream) {
+    if (!d_vert || !d_owner || rows < 1 || cols < 1 || cols > 0x7fffffff || pitch_elems < cols) return DFC_ERR_ARG;
+    g_launches = 0;
+    const unsigned blocks = (unsigned)std::min<int64_t>(rows, 148 * 8);
+    if (take_new)
+        k_row_owners<true><<<blocks, 32 * kOwnWarps, 0, (cudaStream_t)stream>>>(d_vert, rows, (int)cols, pitch_elems,
+                                                                              lmax, d_owner, d_value);
+    else
+        k_row_owners<false><<<blocks, 32 * kOwnWarps, 0, (cudaStream_t)stream>>>(d_vert, rows, (int)cols, pitch_elems,
+                                                                               lmax, d_owner, d_value);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
+int dfc_raster_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pitch_elems, int pass,
+                        dfc_stream_t stream) {
+    if (!d_map || rows < 1 || cols < 1 || pitch_elems < cols || pass < 0 || pass > 5) return DFC_ERR_ARG;
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (pass) {
+        case DFC_PASS_CITYBLOCK_FORWARD: k_raster_pass<<<1, 1024, 0, st>>>(d_map, rows, cols, pitch_elems, 0); break;
+        case DFC_PASS_CITYBLOCK_BACKWARD: k_raster_pass<<<1, 1024, 0, st>>>(d_map, rows, cols, pitch_elems, 1); break;
+        case DFC_PASS_CHAMFER_FORWARD: k_raster_pass<<<1, 1024, 0, st>>>(d_map, rows, cols, pitch_elems, 2); break;
+        case DFC_PASS_CHAMFER_BACKWARD: k_raster_pass<<<1, 1024, 0, st>>>(d_map, rows, cols, pitch_elems, 3); break;
+        case DFC_PASS_CITYBLOCK_VERTICAL:
+            k_vpass_cb<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(d_map, rows, cols, pitch_elems);
+            break;
+        default:
+            k_hpass_cb<<<(unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 16), 256, 0, st>>>(d_map, rows, cols,
+                                                                                              pitch_elems);
+    }
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
 int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_end) {
     g_ev[0] = static_cast<cudaEvent_t>(ev_col_begin);
     g_ev[1] = static_cast<cudaEvent_t>(ev_row_begin);

@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(1024) k_raster_pass(uint64_t* __restrict__ dm,
                 }
             }
             if (t != kInf64) run = min(run, (int64_t)t - wa * q);
-            const uint64_t out = run == kBig ? kInf64 : (uint64_t)(run + wa * q);
-            if (out < r[j] || t < r[j]) r[j] = min(out, t);
+            const uint64_t out = run == kBig ? kInf64 : (uint64_t)(run + wa * q);  // <= t
+            if (out < r[j]) r[j] = out;
         }
         __syncthreads();  // row i is finished before row i +/- 1 reads it
     }

@@ -697,3 +697,63 @@ def test_band_sparse_tiles_scaled(dfc, seed):
     img = workloads.sparse_tiles(2048, 2048, 64, 256, 4e-3, 99 + seed)
     assert img.sum() * 256 < img.size
     _check_edt(dfc, img, 0)
+
+
+# ---- per-pass entry points: build_row_envelope on arbitrary int64 rows, the
+# in-place raster passes (k_passes.cu) ----
+
+def _owners_from_envelope(ks, js, cols):
+    own = np.empty(cols, np.int64)
+    for t in range(len(ks)):
+        own[js[t]:js[t + 1]] = ks[t]
+    return own
+
+
+@pytest.mark.parametrize("take_new", [True, False])
+def test_row_owners_arbitrary_rows(dfc, take_new):
+    rng = np.random.default_rng(5 + take_new)
+    for t in range(120):
+        c = int(rng.integers(1, 700))
+        lmax = int(rng.integers(2, 3_000_000))
+        rows = int(rng.integers(1, 5))
+        v = rng.integers(0, lmax + lmax // 20 + 2, (rows, c)).astype(np.int64)
+        if t % 3 == 0:
+            v[:, 0] = lmax                                    # the sentinel base
+        if t % 5 == 0:
+            v[:, rng.random(c) < 0.9] = lmax                  # mostly sentinels
+        own, val = dfc.row_owners(torch.from_numpy(v).cuda(), lmax, take_new)
+        own, val = own.cpu().numpy(), val.cpu().numpy()
+        for r in range(rows):
+            ks, js = oracle.build_row_envelope(v[r], lmax, take_new)
+            want = _owners_from_envelope(ks, js, c)
+            np.testing.assert_array_equal(own[r], want)
+            jj = np.arange(c)
+            np.testing.assert_array_equal(val[r], v[r][want] + (jj - want) ** 2)
+
+
+@pytest.mark.parametrize("which", range(6))
+def test_raster_pass_in_place(dfc, which):
+    rng = np.random.default_rng(10 + which)
+    for t in range(12):
+        r, c = int(rng.integers(1, 300)), int(rng.integers(1, 2500))
+        if t % 2:
+            dm = oracle.init_map(oracle.random_image(r, c, float(rng.choice([0.0, 0.002, 0.05, 0.5])), t))
+        else:
+            dm = np.where(rng.random((r, c)) < 0.2, rng.integers(0, 10000, (r, c)),
+                          np.iinfo(np.uint64).max).astype(np.uint64)
+        g = torch.from_numpy(dm.view(np.int64).copy()).cuda()
+        dfc.raster_pass(g, which)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(g.cpu().numpy().view(np.uint64), oracle.raster_pass(dm, which))
+
+
+def test_raster_passes_compose_to_the_transforms(dfc):
+    """forward + backward == cityblock_sequential / chamfer34 (propagation.cpp:90-109)."""
+    img = oracle.random_image(130, 517, 0.01, 3)
+    for (f, b_, kind) in ((0, 1, "cityblock"), (4, 5, "chamfer34")):
+        g = torch.from_numpy(oracle.init_map(img).view(np.int64).copy()).cuda()
+        dfc.raster_pass(g, f)
+        dfc.raster_pass(g, b_)
+        torch.cuda.synchronize()
+        want = oracle.cityblock(img) if kind == "cityblock" else oracle.chamfer34(img)
+        np.testing.assert_array_equal(g.cpu().numpy().view(np.uint64), want)

@@ -220,3 +220,38 @@ def test_label_tie_rule_min_column_then_min_row():
         colmax = np.where(d == best[..., None], fc, -1).max(axis=2)
         _, ncol = oracle.meijster_scan(oracle.vertical_pass(img), take_new=True)
         assert (ncol.astype(np.int64) == colmax).all()
+
+
+def test_oracle_per_pass_raster_functions_match_reference():
+    """orc_raster_pass (propagation.cpp:16-88 restated) == the reference's own
+    per-pass functions, on init maps and arbitrary maps."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(0)
+    for t in range(150):
+        r, c = int(rng.integers(1, 30)), int(rng.integers(1, 30))
+        if t % 2:
+            dm = oracle.init_map(oracle.random_image(r, c, 0.1, t))
+        else:
+            dm = np.where(rng.random((r, c)) < 0.3, rng.integers(0, 50, (r, c)),
+                          np.iinfo(np.uint64).max).astype(np.uint64)
+        for p in range(6):
+            np.testing.assert_array_equal(oracle.raster_pass(dm, p), oracle.ref_raster_pass(dm, p))
+
+
+def test_oracle_build_row_envelope_matches_reference_on_arbitrary_rows():
+    """build_row_envelope on int64 rows that are not vertical-pass rows
+    (non-squares, values at / above the sentinel, a sentinel base)."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(1)
+    for t in range(400):
+        c = int(rng.integers(1, 60))
+        lmax = int(rng.integers(2, 2000))
+        v = rng.integers(0, lmax + 40, c).astype(np.int64)
+        if t % 3 == 0:
+            v[0] = lmax
+        for tn in (True, False):
+            a = oracle.build_row_envelope(v, lmax, tn)
+            b = oracle.ref_build_row_envelope(v, lmax, tn)
+            assert a[0].tolist() == b[0].tolist() and a[1].tolist() == b[1].tolist()
