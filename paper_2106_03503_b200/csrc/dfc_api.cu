@@ -72,6 +72,10 @@ void init_pool_once() {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
+        if (const char* v = getenv("DFC_SPARSE_DIV")) {  // tuning: the sparse-plane gate
+            const unsigned long long d = strtoull(v, nullptr, 10);
+            if (d >= 1) cudaMemcpyToSymbol(dfc::c_sparse_div, &d, sizeof(d));
+        }
     });
 }
 

@@ -89,10 +89,13 @@ __host__ __device__ __forceinline__ bool pts_plane(const unsigned long long* cou
     return on && counts != nullptr && counts[img] <= (unsigned long long)kPtsCap;
 }
 
-// Sparse plane (object pixels < 1/256 of the plane): its rows go to the
-// lane-per-row kernel (k_rows_lr.cu) in the default mode.
-__host__ __device__ __forceinline__ bool lr_plane(const unsigned long long* counts, int img, int H, int W) {
-    return counts != nullptr && counts[img] * 256ull < (unsigned long long)H * (unsigned long long)W;
+// Sparse plane (object pixels < 1/c_sparse_div of the plane): its rows go to
+// the band path (k_rows_band.cu) or the lane-per-row kernel (k_rows_lr.cu) in
+// the default mode.  The divisor is a per-device constant (DFC_SPARSE_DIV,
+// tuning; set once in init_pool_once).
+__device__ __constant__ unsigned long long c_sparse_div = 256ull;
+__device__ __forceinline__ bool lr_plane(const unsigned long long* counts, int img, int H, int W) {
+    return counts != nullptr && counts[img] * c_sparse_div < (unsigned long long)H * (unsigned long long)W;
 }
 
 // Object mask of polarity `pol` (0: object = nonzero, 1: object = zero) from
