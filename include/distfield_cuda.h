@@ -315,6 +315,12 @@ int dfc_set_lr_chunk(int cols);
 
 /* Number of kernels the last successful call on this thread enqueued. */
 int dfc_last_launch_count(void);
+/* Debug: with DFC_DEBUG_GUARD=1 in the environment every scratch allocation
+ * of the library carries canary zones on both sides and a poisoned interior;
+ * this returns the number of canary bytes overwritten so far on the current
+ * device (synchronises), or -1 when the mode is off.  The stand-in for
+ * compute-sanitizer memcheck/initcheck where that tool cannot be run. */
+long long dfc_debug_guard_violations(void);
 /* Human-readable status; never NULL. */
 const char* dfc_status_string(int status);
 /* The cudaError_t behind the last DFC_ERR_CUDA on this thread (0 if none). */

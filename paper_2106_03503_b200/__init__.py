@@ -159,8 +159,45 @@ def _img2d(img: torch.Tensor):
     return img, img.shape[0], img.shape[1], img.stride(0)
 
 
+# DFC_DEBUG_GUARD=1 (debug, see include/distfield_cuda.h): outputs this layer
+# allocates sit between two 4 KiB canary zones (0x5A bytes, interior poisoned
+# alike); check_guards() verifies them together with the library's scratch
+# canaries.  The stand-in for compute-sanitizer where that tool cannot run.
+_GUARD = os.environ.get("DFC_DEBUG_GUARD") == "1"
+_GUARD_PAD = 4096
+_guarded = []
+_lib.dfc_debug_guard_violations.restype = C.c_longlong
+
+
 def _empty(shape, dtype, like):
-    return torch.empty(shape, dtype=dtype, device=like.device)
+    if not _GUARD:
+        return torch.empty(shape, dtype=dtype, device=like.device)
+    n = 1
+    for d in shape:
+        n *= int(d)
+    nbytes = n * torch.empty((), dtype=dtype).element_size()
+    buf = torch.full((nbytes + 2 * _GUARD_PAD,), 0x5A, dtype=torch.uint8, device=like.device)
+    _guarded.append((buf, nbytes))
+    return buf[_GUARD_PAD:_GUARD_PAD + nbytes].view(dtype).view(shape)
+
+
+def check_guards() -> int:
+    """Debug (DFC_DEBUG_GUARD=1): raise if any kernel wrote outside an output
+    this layer allocated or outside a scratch allocation of the library;
+    returns the number of output buffers checked."""
+    if not _GUARD:
+        raise RuntimeError("DFC_DEBUG_GUARD=1 is not set")
+    torch.cuda.synchronize()
+    for buf, nbytes in _guarded:
+        lo, hi = buf[:_GUARD_PAD], buf[_GUARD_PAD + nbytes:]
+        if not (bool((lo == 0x5A).all()) and bool((hi == 0x5A).all())):
+            raise AssertionError("a kernel wrote outside an output buffer (canary zone changed)")
+    n = len(_guarded)
+    _guarded.clear()
+    bad = _lib.dfc_debug_guard_violations()
+    if bad != 0:
+        raise AssertionError(f"scratch canary zones: {bad} bytes overwritten")
+    return n
 
 
 def edt(img: torch.Tensor, polarity: int = 0, dist: bool = True, label: bool = False,

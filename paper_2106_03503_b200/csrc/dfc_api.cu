@@ -79,13 +79,55 @@ void init_pool_once() {
     });
 }
 
+// DFC_DEBUG_GUARD=1 (debug; compute-sanitizer's stand-in where that tool is
+// unavailable): every scratch allocation gets a kGuard-byte canary zone on
+// both sides and a poisoned interior (0xCD: a kernel that reads scratch it
+// never wrote computes garbage and fails parity); when the allocation is
+// released a kernel counts the canary bytes that changed.  The count is read
+// with dfc_debug_guard_violations().
+constexpr size_t kGuard = 65536;
+__device__ unsigned long long g_guard_bad;
+
+bool guard_on() {
+    static const bool on = [] {
+        const char* v = getenv("DFC_DEBUG_GUARD");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
+__global__ void k_guard_check(const uint8_t* lo, const uint8_t* hi, size_t n) {
+    unsigned bad = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        bad += (lo[i] != 0xA5) + (hi[i] != 0xA5);
+    if (bad) atomicAdd(&g_guard_bad, (unsigned long long)bad);
+}
+
 struct Scratch {
     void* p = nullptr;
+    void* raw = nullptr;
+    size_t bytes = 0;
     cudaStream_t st;
     explicit Scratch(cudaStream_t s) : st(s) {}
-    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, st); }
+    cudaError_t alloc(size_t n) {
+        if (!guard_on()) return cudaMallocAsync(&p, n, st);
+        bytes = (n + 255) / 256 * 256;
+        cudaError_t e = cudaMallocAsync(&raw, bytes + 2 * kGuard, st);
+        if (e != cudaSuccess) return e;
+        char* c = static_cast<char*>(raw);
+        p = c + kGuard;
+        if ((e = cudaMemsetAsync(c, 0xA5, kGuard, st)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(c + kGuard, 0xCD, bytes, st)) != cudaSuccess) return e;
+        return cudaMemsetAsync(c + kGuard + bytes, 0xA5, kGuard, st);
+    }
     ~Scratch() {
-        if (p) cudaFreeAsync(p, st);
+        if (raw) {
+            const uint8_t* c = static_cast<const uint8_t*>(raw);
+            k_guard_check<<<64, 256, 0, st>>>(c, c + kGuard + bytes, kGuard);
+            cudaFreeAsync(raw, st);
+        } else if (p) {
+            cudaFreeAsync(p, st);
+        }
     }
 };
 
@@ -130,7 +172,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
                 int pol0, int npol, uint16_t* nr, uint16_t* first, uint16_t* last, int Wp,
                 cudaStream_t st, int32_t* vsq = nullptr, unsigned long long* counts = nullptr,
                 uint32_t* pts = nullptr, uint32_t* bmask = nullptr, bool skip_full = false,
-                bool no_fill = false, bool skip_sparse = false) {
+                bool no_fill = false, bool skip_sparse = false, uint32_t* objcol = nullptr) {
     ColArgs c;
     c.img = img;
     c.pitch = pitch;
@@ -148,6 +190,7 @@ int column_pass(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pit
     c.bmask = bmask;
     c.skip_full = skip_full && bmask != nullptr && counts != nullptr;
     c.skip_sparse = skip_sparse && bmask != nullptr && counts != nullptr;
+    c.objcol = objcol;
     const unsigned long long* skip = c.pts ? counts : nullptr;
     const int tpb = 128;
     dim3 grid((unsigned)(((W + 3) / 4 + tpb - 1) / tpb), (unsigned)c.nb, (unsigned)n);
@@ -210,12 +253,13 @@ struct BandSrc {
     const uint32_t* bmask = nullptr;   // K1a's masks (single images), else null
     const uint16_t* above = nullptr;
     const uint16_t* below = nullptr;
+    uint32_t* objcol = nullptr;        // K1a's object-column bits of these planes (band path), else null
     int nb = 0, n_img = 1, pol0 = 0;
     bool anc = false;     // k_rows_anc stages its rows from the bands
     bool sparse = false;  // the band path (k_rows_band.cu) takes the sparse planes
 };
 
-// Bands per candidate group of the band path (k_band_hull): DFC_BAND_GROUP
+// Bands per candidate group of the band path (k_hull<2>): DFC_BAND_GROUP
 // (tuning), default 4.
 int band_group() {
     static const int g = [] {
@@ -236,30 +280,149 @@ bool band_sparse_on() {
     return on;
 }
 
+// Slices of the band path (DFC_BAND_SLICES, tuning; 1 = no pipelining).
+int band_slices() {
+    static const int n = [] {
+        const char* v = getenv("DFC_BAND_SLICES");
+        const int x = v ? atoi(v) : 0;
+        return x >= 1 && x <= 16 ? x : 1;
+    }();
+    return n;
+}
+
+// k_rows_fill CTAs per SM (DFC_FILL_CTAS, tuning): few enough that the next
+// slice's k_hull / k_band_rows CTAs find registers and shared memory
+// beside the resident fill CTAs.
+int fill_ctas() {
+    static const int n = [] {
+        const char* v = getenv("DFC_FILL_CTAS");
+        const int x = v ? atoi(v) : 0;
+        return x >= 1 && x <= 16 ? x : 4;
+    }();
+    return n;
+}
+
+// Per-device helper stream and events of the pipelined band path: a
+// high-priority stream runs the hull filter and the per-row stacks of slice
+// s + 1 while the caller's stream fills slice s (the fill is HBM-bound, the
+// other two latency-bound).  Fork/join by events only -- no host
+// synchronisation, legal under stream capture.  The mutex serialises the
+// host-side enqueue per device (the events are shared).
+constexpr int kMaxSlices = 16;
+struct BandPipe {
+    std::mutex mu;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr;
+    cudaEvent_t done[kMaxSlices] = {};
+    bool ok = false;
+};
+BandPipe* band_pipe() {
+    constexpr int kMaxDev = 64;
+    static BandPipe pipes[kMaxDev];
+    static std::once_flag flags[kMaxDev];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    BandPipe* bp = &pipes[dev];
+    std::call_once(flags[dev], [bp] {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        bool ok = cudaStreamCreateWithPriority(&bp->aux, cudaStreamNonBlocking, greatest) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&bp->fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; i < kMaxSlices && ok; ++i)
+            ok = cudaEventCreateWithFlags(&bp->done[i], cudaEventDisableTiming) == cudaSuccess;
+        bp->ok = ok;
+        if (!ok) cudaGetLastError();
+    });
+    return bp->ok ? bp : nullptr;
+}
+
 // The band path (k_rows_band.cu) over the sparse planes of `ba`: hull filter,
-// per-row stacks, fill into a's outputs.
-int launch_band_path(const RowArgs& a, const BandArgs& ba, bool take_new, cudaStream_t st) {
-    BandArgs hb = ba;
-    const int hsm = hull_smem_bytes(ba.W);
-    cudaError_t e = cudaFuncSetAttribute(k_band_hull, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+// per-row stacks, fill into a's outputs.  A single plane with enough bands is
+// cut into slices of whole candidate groups, pipelined over two streams.
+int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cudaStream_t st) {
+    const int hsm0 = hull_smem_bytes(0), hsm = hull_smem_bytes(1);
+    cudaError_t e = cudaFuncSetAttribute(k_hull<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm0);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hull<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hull<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
     if (e != cudaSuccess) return cuda_fail(e);
-    k_band_hull<<<dim3((unsigned)ba.ngroups, (unsigned)(2 * ba.nplanes)), hull_threads(ba.W), hsm, st>>>(hb);
-    const int64_t tasks = (int64_t)ba.nplanes * ba.nb;
     const int rsm = band_rows_smem_bytes();
     const void* rfn = take_new ? (const void*)k_band_rows<true> : (const void*)k_band_rows<false>;
     e = cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
     if (e != cudaSuccess) return cuda_fail(e);
-    if (take_new)
-        k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(hb);
-    else
-        k_band_rows<false><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(hb);
+    const int donly = a.D && !a.LB && !a.NC ? (a.S ? 2 : 1) : 0;  // values only (D, optionally sqrt D)
+    const void* ffn = donly == 1 ? (const void*)k_rows_fill<1> : donly == 2 ? (const void*)k_rows_fill<2>
+                                                                            : (const void*)k_rows_fill<0>;
     const int fsm = fill_smem_bytes();
-    e = cudaFuncSetAttribute(k_rows_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+    e = cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
     if (e != cudaSuccess) return cuda_fail(e);
-    const int64_t rows = (int64_t)ba.nplanes * ba.H;
-    const int64_t fblocks = std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * 6);
-    k_rows_fill<<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
+
+    // object columns per band and the coarse lines' hulls (all columns) first
+    BandArgs ba = ba_in;
+    ba.cbands = ba.group >= kCoarseBands ? ba.group : kCoarseBands / ba.group * ba.group;
+    ba.ncoarse = (ba.nb + ba.cbands - 1) / ba.cbands;
+    ba.grp0 = 0;
+    ba.grp1 = ba.ngroups;
+    Scratch hs(st);
+    const size_t oc_bytes = (size_t)round_up((int64_t)ba.nplanes * ba.nb * ba.Ww * 4, 256);
+    const size_t co_bytes = (size_t)round_up((int64_t)ba.nplanes * ba.ncoarse * 2 * ba.Ww * 4, 256);
+    const bool have_oc = ba_in.objcol != nullptr;  // K1a wrote the object-column bits
+    e = hs.alloc((have_oc ? 2 : 3) * oc_bytes + co_bytes);
+    if (e != cudaSuccess) return cuda_fail(e);
+    ba.objpre = static_cast<uint32_t*>(hs.p);
+    ba.objsuf = reinterpret_cast<uint32_t*>(static_cast<char*>(hs.p) + oc_bytes);
+    ba.coarse = reinterpret_cast<uint32_t*>(static_cast<char*>(hs.p) + 2 * oc_bytes);
+    if (!have_oc) {
+        ba.objcol = reinterpret_cast<uint32_t*>(static_cast<char*>(hs.p) + 2 * oc_bytes + co_bytes);
+        k_band_objcols<<<dim3((unsigned)((ba.Ww * 32 + 255) / 256), (unsigned)std::min(ba.nb, 64), (unsigned)ba.nplanes), 256, 0, st>>>(ba);
+        ++g_launches;
+    }
+    auto warps_grid = [](int64_t tasks) { return (unsigned)((tasks + kHullWarps - 1) / kHullWarps); };
+    const int nwin = (ba.Ww + 31) / 32;
+    k_objcol_runs<<<dim3((unsigned)((ba.Ww + 127) / 128), (unsigned)ba.ncoarse, (unsigned)ba.nplanes), 128, 0, st>>>(ba);
+    k_hull<0><<<warps_grid((int64_t)ba.nplanes * ba.ncoarse * 2 * nwin), 32 * kHullWarps, hsm0, st>>>(ba);
+    k_hull<1><<<warps_grid((int64_t)ba.nplanes * ba.ncoarse * 2), 32 * kHullWarps, hsm, st>>>(ba);
     g_launches += 3;
+
+    int S = ba.nplanes == 1 ? std::min(band_slices(), ba.ngroups / 8) : 1;
+    BandPipe* bp = S > 1 ? band_pipe() : nullptr;
+    if (!bp) S = 1;
+    std::unique_lock<std::mutex> lock;
+    if (bp) {
+        lock = std::unique_lock<std::mutex>(bp->mu);
+        if ((e = cudaEventRecord(bp->fork, st)) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaStreamWaitEvent(bp->aux, bp->fork, 0)) != cudaSuccess) return cuda_fail(e);
+    }
+    cudaStream_t cs = bp ? bp->aux : st;  // hull filter + per-row stacks
+    for (int s = 0; s < S; ++s) {
+        BandArgs hb = ba;
+        const int g0 = (int)((int64_t)ba.ngroups * s / S), g1 = (int)((int64_t)ba.ngroups * (s + 1) / S);
+        const int b0 = bp ? g0 * ba.group : 0;
+        const int b1 = bp ? std::min(ba.nb, g1 * ba.group) : ba.nb;
+        hb.grp0 = bp ? g0 : 0;
+        hb.grp1 = bp ? g1 : ba.ngroups;
+        hb.task0 = b0;
+        hb.frow0 = bp ? (int64_t)32 * b0 : 0;
+        hb.frow1 = bp ? std::min<int64_t>(ba.H, (int64_t)32 * b1) : (int64_t)ba.nplanes * ba.H;
+        k_hull<2><<<warps_grid(bp ? (int64_t)(g1 - g0) * 2 : (int64_t)ba.nplanes * ba.ngroups * 2), 32 * kHullWarps, hsm, cs>>>(hb);
+        const int64_t tasks = bp ? b1 - b0 : (int64_t)ba.nplanes * ba.nb;
+        if (take_new)
+            k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, cs>>>(hb);
+        else
+            k_band_rows<false><<<(unsigned)tasks, 32 * kBandWarps, rsm, cs>>>(hb);
+        if (bp) {
+            if ((e = cudaEventRecord(bp->done[s], cs)) != cudaSuccess) return cuda_fail(e);
+            if ((e = cudaStreamWaitEvent(st, bp->done[s], 0)) != cudaSuccess) return cuda_fail(e);
+        }
+        const int64_t rows = hb.frow1 - hb.frow0;
+        const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * fill_ctas()));
+        if (donly == 1)
+            k_rows_fill<1><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
+        else if (donly == 2)
+            k_rows_fill<2><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
+        else
+            k_rows_fill<0><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
+        g_launches += 3;
+    }
     return DFC_OK;
 }
 
@@ -452,6 +615,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             ba.bmask = band.bmask;
             ba.above = band.above;
             ba.below = band.below;
+            ba.objcol = band.objcol;
             ba.ent = reinterpret_cast<uint32_t*>(base);
             ba.entr = reinterpret_cast<uint16_t*>(base + ent_bytes);
             ba.cand = reinterpret_cast<uint32_t*>(base + ent_bytes + entr_bytes);
@@ -594,9 +758,16 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
                                     reinterpret_cast<uintptr_t>(reinterpret_cast<char*>(counts + planes) +
                                                                 (pts_on ? (size_t)planes * kPtsCap * 4 : 0)), 16))
                               : nullptr;
+    const int64_t Ww = (W + 31) / 32;
+    Scratch so(st);  // object-column bits per (plane, band) for the band path's hull filter
+    if (sparse_band) {
+        e = so.alloc((size_t)(planes * nb * Ww) * 4);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    uint32_t* objcol = static_cast<uint32_t*>(so.p);
     prof(0, st);
     int rc = column_pass(img, n, H, W, pitch, istride, pol0, npol, nr, first, last, Wp, st, nullptr, counts, pts,
-                         bmask, band_on, false, sparse_band);
+                         bmask, band_on, false, sparse_band, objcol);
     if (rc != DFC_OK) return rc;
     prof(1, st);
 
@@ -621,6 +792,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
         bs.sparse = sparse_band;
         bs.above = last;
         bs.below = first;
+        bs.objcol = objcol;
         bs.nb = (int)nb;
         bs.n_img = (int)n;
         bs.pol0 = pol0;
@@ -644,6 +816,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
             bs.sparse = sparse_band;
             bs.above = last + (int64_t)s * nb * Wp;
             bs.below = first + (int64_t)s * nb * Wp;
+            bs.objcol = objcol ? objcol + (int64_t)s * nb * Ww : nullptr;
             bs.nb = (int)nb;
             bs.n_img = 1;
             bs.pol0 = pol0 + s;
@@ -1056,6 +1229,12 @@ int dfc_set_lr_chunk(int cols) {
 }
 
 int dfc_last_launch_count(void) { return g_launches; }
+
+long long dfc_debug_guard_violations(void) {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_guard_bad, sizeof(v)) != cudaSuccess) return -1;
+    return guard_on() ? (long long)v : -1;
+}
 
 int dfc_last_cuda_error(void) { return g_last_cuda; }
 

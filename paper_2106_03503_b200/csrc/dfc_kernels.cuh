@@ -28,6 +28,10 @@ struct ColArgs {
     // the band path (k_rows_band.cu) takes the sparse planes: no nearest-row
     // plane for them either
     bool skip_sparse;
+    // object-column bits per (plane, band) [slot][img][nb][ceil(W/32)], nullable:
+    // bit k of word w = column 32 w + k holds an object pixel in the band (the
+    // band path's hull filter, k_rows_band.cu)
+    uint32_t* objcol;
 };
 
 // Stage 2 (k_rows.cu)

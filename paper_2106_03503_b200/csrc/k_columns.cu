@@ -84,6 +84,17 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
             f[c] = mk[c] ? (uint16_t)(r0 + __ffs(mk[c]) - 1) : kNoRow;
             l[c] = mk[c] ? (uint16_t)(r0 + 31 - __clz(mk[c])) : kNoRow;
         }
+        if (a.objcol) {  // 4 bits per thread, 8 threads per 32-column word
+            const int lane = threadIdx.x & 31;
+            uint32_t v = ((uint32_t)(mk[0] != 0u) | ((uint32_t)(mk[1] != 0u) << 1) | ((uint32_t)(mk[2] != 0u) << 2) |
+                          ((uint32_t)(mk[3] != 0u) << 3)) << (4 * (lane & 7));
+            v |= __shfl_xor_sync(0xffffffffu, v, 1);
+            v |= __shfl_xor_sync(0xffffffffu, v, 2);
+            v |= __shfl_xor_sync(0xffffffffu, v, 4);
+            const int Ww = (a.W + 31) >> 5;
+            if ((lane & 7) == 0 && (j0 >> 5) < Ww)
+                a.objcol[(((int64_t)s * a.n_img + im) * a.nb + b) * Ww + (j0 >> 5)] = v;
+        }
         if (counts) {
             const unsigned mine = (unsigned)(__popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]));
             unsigned long long c = mine;

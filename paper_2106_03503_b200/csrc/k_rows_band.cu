@@ -22,12 +22,13 @@
 //              is exact (the row pass evaluates each candidate's true g_k(i)),
 //              so the hulls are taken per window of 1024 columns (a hull point
 //              of the row is a hull point of every window holding it):
-//  k_band_hull warp = (plane, band, side, window); lane = 32 columns: monotone
-//              chain with the stack as a 32-bit mask, then 5 levels of bridge
-//              merges (walk the lower common tangent) inside the warp; the
-//              side-above warps also add the band's object columns.  Output:
-//              candidate bit masks [plane][band][side][W/32].  C5: ~640
-//              candidates per band out of 32768 columns.
+//  k_hull      one warp prunes one compact point list towards its lower hull
+//              (data-parallel rounds: a point above the chord of two list
+//              neighbours goes, survivors are compacted); filters at coarse
+//              lines over all columns (per window, then per line), at the
+//              groups' lines over the coarse filter plus the object columns
+//              in between (see "hull filter" below).  Output: candidate bit
+//              masks [plane][group][side][W/32].
 //  k_band_rows warp = (plane, band), lane = row: the reference's stack algorithm
 //              over the band's candidates only (g from the band mask and the
 //              carries, the upper row on ties, exact_edt.cpp:351), the top
@@ -49,7 +50,8 @@ constexpr int kBandWarps = 8;       // k_band_rows: warps (column chunks) per ba
 constexpr int kBandCap = 16;        // ring entries per lane (power of two)
 constexpr int kCandCap = 2048;      // candidates of a band listed in shared memory
 constexpr int kFillWarps = 4;
-constexpr int kFillCap = 1536;      // list entries staged per warp (k_rows_fill)
+constexpr int kFillCap = 512;       // list entries staged per warp (k_rows_fill); a chunk of a listed
+                                    // band holds ~kCandCap / kBandWarps candidates
 
 struct BandArgs {
     const uint32_t* bmask;   // [img][nb][Wp] bit r = row 32 b + r nonzero
@@ -67,9 +69,19 @@ struct BandArgs {
     // an image of Hg rows; plane p's local rows are [0, H).  Single images:
     // band0 = 0, Hg = H.
     int band0, Hg;
-    int group, ngroups;      // bands per candidate group (k_band_hull), groups per plane
+    int group, ngroups;      // bands per candidate group (k_hull<2>), groups per plane
+    uint32_t* objcol = nullptr;  // [plane][nb][Ww] columns with an object in the band (null: built from bmask)
+    uint32_t* objpre;        // ... OR'ed over the bands from the start of the band's 32 (in its coarse group)
+    uint32_t* objsuf;        // ... OR'ed over the bands to the end of the band's 32
+    uint32_t* coarse;        // [plane][ncoarse][2][Ww] hulls at the coarse groups' first / last lines
+    int cbands, ncoarse;     // bands per coarse group (a multiple of group), coarse groups per plane
     bool pts_gate;           // point planes belong to k_rows_pts
     bool all_planes;         // every plane (the sharded path), not only the sparse ones
+    // one slice of a single plane's bands (launch_band_path pipelines slices
+    // over two streams): first group of k_band_hull's grid, first band of
+    // k_band_rows' grid, k_rows_fill's rows [frow0, frow1)
+    int grp0 = 0, grp1 = 0, task0 = 0;
+    int64_t frow0 = 0, frow1 = 0;
 };
 
 // The planes this path owns: sparse, not a point plane.
@@ -78,160 +90,292 @@ __device__ __forceinline__ bool band_plane(const BandArgs& a, int p) {
 }
 
 // ---------------------------------------------------------------- hull filter
-// Bands come in groups of G (a.group).  For band b of group [b0, b0 + G):
-//   A-candidates(b) <= hullA(b0) + {columns with an object in bands b0 .. b-1}
-// because an object above b0 whose cell (among the objects above b) crosses
-// the line 32 b also crosses the nearer line 32 b0 (convexity, the same
-// argument as above); symmetrically below with the group's last band.  So the
-// group's candidates = hullA(first band) + hullB(last band) + every column
-// with an object in the group, and one CTA per (group, side) builds one hull:
-// thread = 32 columns, a monotone chain with the stack as a 32-bit mask, then
-// log2(threads) levels of bridge merges (walk the lower common tangent) over
-// the mask words in shared memory.  C5, G = 4: ~340 candidates per band.
-__global__ void __launch_bounds__(1024) k_band_hull(BandArgs a) {
-    extern __shared__ uint32_t hsm[];
-    uint32_t* M = hsm;                                      // hull bits per thread [T]
-    uint16_t* D = reinterpret_cast<uint16_t*>(hsm + blockDim.x);  // distance to the line per column [T*32]
-    const int T = blockDim.x, tid = threadIdx.x;
-    const int grp = blockIdx.x, p = blockIdx.y >> 1, side = blockIdx.y & 1;
+// Bands come in groups of G (a.group), groups in coarse groups of a.cbands
+// bands.  For band b of group [gb0, gb1] inside coarse group [cb0, cb1]:
+//   A-candidates(b) <= hullA(line 32 gb0) + {columns with an object in bands gb0 .. b-1}
+//   hullA(line 32 gb0) <= hullA(line 32 cb0) + {columns with an object in bands cb0 .. gb0-1}
+// because an object above an earlier line whose cell (among the objects above
+// the later line) crosses the later line also crosses the earlier one
+// (convexity, the same argument as above); symmetrically below with the last
+// bands.  The hull of a point set that contains every hull point IS the hull,
+// so only the coarse lines see all W columns; a group line sees the coarse
+// hull plus the object columns in between (C5: ~10^3 points, not 32768).
+//
+// One warp filters one compact point list in shared memory (column, H = d^2 +
+// k^2 < 2^31) by warp_prune below: rounds of "a point strictly above the chord
+// of two list neighbours goes", survivors compacted in place.  The result is a
+// superset of the lower hull with collinear points kept (ties), which is all
+// the argument above needs -- a group line's list must CONTAIN the coarse
+// line's hull points, and the candidates must CONTAIN the group line's.
+//   K1a / k_band_objcols  object-column bits per band; k_objcol_runs their
+//                   running ORs over runs of 32 bands
+//   k_hull<0>       warp = (plane, coarse group, side, window of 1024 columns):
+//                   the window's filter over every column with a carry
+//   k_hull<1>       warp = (plane, coarse group, side): the windows' survivors
+//                   filtered together
+//   k_hull<2>       warp = (plane, group, side): the coarse line's survivors +
+//                   the object columns in between, filtered at the group's
+//                   line; side 0 also adds the group's own object columns.
+//                   Output: candidate bits [plane][group][side][W/32].
+// A list longer than kHullCap is passed through unfiltered (a superset).
+constexpr int kHullCap = 2048;     // points per warp (k_hull<1>, k_hull<2>)
+constexpr int kHullWinCap = 1024;  // k_hull<0>: a window of 32 words
+constexpr int kHullWarps = 8;
+constexpr int kCoarseBands = 32;   // bands per coarse group (rounded to a multiple of the group)
+constexpr int kPruneRounds = 10;
+
+// Object-column bits per band from the band masks (the sharded path, whose
+// masks are repacked column tiles; single images get them from K1a).
+__global__ void __launch_bounds__(256) k_band_objcols(BandArgs a) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int p = blockIdx.z;
     if (!band_plane(a, p)) return;  // CTA-uniform
-    const int nb = a.nb;
-    const int bfirst = grp * a.group, blast = min(nb - 1, bfirst + a.group - 1);
-    const int kb = side ? blast : bfirst;  // the key band of this side
-    const int gb = a.band0 + kb;
-    const int line = side ? min(32 * gb + 31, a.Hg - 1) : 32 * gb;
-    constexpr uint16_t kNone = 0xFFFF;      // d <= rows - 1 <= 65534
-    // ---- distances to the line, coalesced (8 columns per 16-byte load) ----
-    const uint16_t* car = (side ? a.below : a.above) + ((int64_t)p * nb + kb) * a.Wp;
-    for (int q = tid; 8 * q < 32 * T; q += T) {
-        uint32_t w[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-        if (8 * q + 8 <= a.Wp) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(car) + q);
-            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-        }
-        uint32_t o[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            uint32_t lo = w[t] & 0xffffu, hi = w[t] >> 16;
-            const int k = 8 * q + 2 * t;
-            lo = (lo == kNoRow || k >= a.W) ? kNone : (side ? lo - line : line - lo);
-            hi = (hi == kNoRow || k + 1 >= a.W) ? kNone : (side ? hi - line : line - hi);
-            o[t] = lo | (hi << 16);
-        }
-        *reinterpret_cast<uint4*>(D + 8 * q) = make_uint4(o[0], o[1], o[2], o[3]);
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = p / a.n_img, im = p - s * a.n_img;
+    const int pol = a.pol0 + s;
+    for (int b = blockIdx.y; b < a.nb; b += gridDim.y) {
+        const int nrows = min(32, a.Hg - 32 * (a.band0 + b));
+        const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
+        const bool on = k < a.W && pol_mask(__ldg(a.bmask + ((int64_t)im * a.nb + b) * a.Wp + k), pol, valid) != 0u;
+        const uint32_t word = __ballot_sync(FULL, on);
+        if ((threadIdx.x & 31) == 0 && (k >> 5) < a.Ww) a.objcol[((int64_t)p * a.nb + b) * a.Ww + (k >> 5)] = word;
     }
-    __syncthreads();
-    auto Hof = [&](int x) -> int {  // H_x = d^2 + x^2 < 2^31 (see below)
-        const int d = D[x];
-        return d * d + x * x;
-    };
-    // H <= (rows-1)^2 + (cols-1)^2 <= DFC_MAX_SQDIST < 2^31; differences fit
-    // int32, times column differences (< 2^15): one IMAD.WIDE each
-    auto above_seg = [](int ka, int Ha, int kb, int Hb, int kc, int Hc) {
-        return (long long)(Hb - Ha) * (kc - kb) > (long long)(Hc - Hb) * (kb - ka);
-    };
-
-    // ---- thread-local lower hull of 32 columns (monotone chain, stack = mask) ----
-    const int c0 = 32 * tid;
-    uint32_t st = 0;
-    int tc = -1, tH = 0;
-    for (int c = 0; c < 32; ++c) {
-        const int k = c0 + c;
-        if (D[k] == kNone) continue;
-        const int Hk = Hof(k);
-        while (st & (st - 1)) {  // at least two entries
-            const int sc = 31 - __clz(st & ((1u << tc) - 1u));
-            const int sH = Hof(c0 + sc);
-            if (!above_seg(c0 + sc, sH, c0 + tc, tH, k, Hk)) break;
-            st ^= 1u << tc;
-            tc = sc;
-            tH = sH;
-        }
-        st |= 1u << c;
-        tc = c;
-        tH = Hk;
-    }
-    M[tid] = st;
-    __syncthreads();
-
-    // ---- bridge merges: groups of g threads, leaders at multiples of 2g ----
-    for (int g = 1; g < T; g <<= 1) {
-        if ((tid & (2 * g - 1)) == 0 && tid + g < T) {
-            const int lead = tid, mid = tid + g, end = min(T, tid + 2 * g);
-            int xa = -1, xb = -1;
-            for (int l = mid - 1; l >= lead; --l)
-                if (M[l]) { xa = 32 * l + 31 - __clz(M[l]); break; }
-            for (int l = mid; l < end; ++l)
-                if (M[l]) { xb = 32 * l + __ffs(M[l]) - 1; break; }
-            if (xa >= 0 && xb >= 0) {
-                int Ha = Hof(xa), Hb = Hof(xb);
-                for (;;) {
-                    bool moved = false;
-                    for (;;) {  // the predecessor of xa in the left group
-                        int l = xa >> 5;
-                        uint32_t m = M[l] & ((1u << (xa & 31)) - 1u);
-                        while (!m && l > lead) m = M[--l];
-                        if (!m) break;
-                        const int xp = 32 * l + 31 - __clz(m);
-                        const int Hp = Hof(xp);
-                        if (!above_seg(xp, Hp, xa, Ha, xb, Hb)) break;
-                        M[xa >> 5] &= ~(1u << (xa & 31));
-                        xa = xp;
-                        Ha = Hp;
-                        moved = true;
-                    }
-                    for (;;) {  // the successor of xb in the right group
-                        int l = xb >> 5;
-                        uint32_t m = (xb & 31) == 31 ? 0u : M[l] & ~((2u << (xb & 31)) - 1u);
-                        while (!m && l < end - 1) m = M[++l];
-                        if (!m) break;
-                        const int xs = 32 * l + __ffs(m) - 1;
-                        const int Hs = Hof(xs);
-                        if (!above_seg(xa, Ha, xb, Hb, xs, Hs)) break;
-                        M[xb >> 5] &= ~(1u << (xb & 31));
-                        xb = xs;
-                        Hb = Hs;
-                        moved = true;
-                    }
-                    if (!moved) break;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    uint32_t word = M[tid];
-
-    // ---- side 0 adds every column with an object in the group's bands ----
-    if (side == 0 && c0 < a.W) {
-        const int s = p / a.n_img, im = p - s * a.n_img;
-        const int pol = a.pol0 + s;
-        for (int b = bfirst; b <= blast; ++b) {
-            const int gbb = a.band0 + b;
-            const int nrows = min(32, a.Hg - 32 * gbb);
-            const uint32_t valid = nrows == 32 ? 0xffffffffu : ((1u << nrows) - 1u);
-            const uint32_t* mrow = a.bmask + ((int64_t)im * nb + b) * a.Wp;
-            if (c0 + 32 <= a.Wp) {
-                const uint4* q = reinterpret_cast<const uint4*>(mrow + c0);
-#pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    const uint4 x = __ldg(q + v);
-                    word |= (uint32_t)(pol_mask(x.x, pol, valid) != 0u) << (4 * v);
-                    word |= (uint32_t)(pol_mask(x.y, pol, valid) != 0u) << (4 * v + 1);
-                    word |= (uint32_t)(pol_mask(x.z, pol, valid) != 0u) << (4 * v + 2);
-                    word |= (uint32_t)(pol_mask(x.w, pol, valid) != 0u) << (4 * v + 3);
-                }
-            } else {
-                for (int c = 0; c < 32 && c0 + c < a.Wp; ++c)
-                    word |= (uint32_t)(pol_mask(__ldg(mrow + c0 + c), pol, valid) != 0u) << c;
-            }
-        }
-        if (a.W - c0 < 32) word &= (1u << (a.W - c0)) - 1u;  // columns past the row end
-    }
-    if (tid < a.Ww) a.cand[(((int64_t)p * a.ngroups + grp) * 2 + side) * a.Ww + tid] = word;
 }
 
-inline int hull_threads(int W) { return std::max(32, (int)(((W + 31) / 32 + 31) / 32 * 32)); }
-inline int hull_smem_bytes(int W) { const int T = hull_threads(W); return T * 4 + T * 32 * 2; }
+// Running ORs of the object-column words inside each run of 32 bands of a
+// coarse group: pre[b] = OR over the run's bands up to b, suf[b] = from b on.
+// Thread = (word, run of 32 bands), 32 independent loads.
+__global__ void __launch_bounds__(128) k_objcol_runs(BandArgs a) {
+    const int p = blockIdx.z, cg = blockIdx.y;
+    if (!band_plane(a, p)) return;  // CTA-uniform
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= a.Ww) return;
+    const int cb0 = cg * a.cbands, cb1 = min(a.nb - 1, cb0 + a.cbands - 1);
+    for (int bb = cb0; bb <= cb1; bb += 32) {
+        const int nbb = min(32, cb1 - bb + 1);
+        const int64_t at = ((int64_t)p * a.nb + bb) * a.Ww + w;
+        uint32_t x[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) x[t] = t < nbb ? a.objcol[at + (int64_t)t * a.Ww] : 0u;
+        uint32_t run = 0;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            run |= x[t];
+            if (t < nbb) a.objpre[at + (int64_t)t * a.Ww] = run;
+        }
+        run = 0;
+#pragma unroll
+        for (int t = 31; t >= 0; --t) {
+            run |= x[t];
+            if (t < nbb) a.objsuf[at + (int64_t)t * a.Ww] = run;
+        }
+    }
+}
+
+// b strictly above the segment a-c (H differences fit int32, column
+// differences < 2^15: one IMAD.WIDE each)
+__device__ __forceinline__ bool hull_above(int ka, int Ha, int kb, int Hb, int kc, int Hc) {
+    return (long long)(Hb - Ha) * (kc - kb) > (long long)(Hc - Hb) * (kb - ka);
+}
+
+// Prune the compact point list c / H [0, n) (ascending columns) towards its
+// lower hull, data-parallel: in every round point i goes if it lies strictly
+// above the chord of its list neighbours i - s and i + s for some stride s =
+// 1, 2, .., 64 (a point above a chord of two points of the set is no hull
+// point, whatever happens to those two), then the survivors are compacted in
+// place.  Any number of rounds leaves a superset of the hull (collinear points
+// kept); on C5's lines 5 rounds reach the hull itself (10^4 -> ~10^2 points,
+// profiles/r02/prune_study.txt).  Lane = point i = 32 t + lane.  Returns the new n.
+template <int CAP>
+__device__ __forceinline__ int warp_prune(uint16_t* c, int32_t* H, int n, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int NT = CAP / 32;
+    for (int round = 0; round < kPruneRounds && n >= 3; ++round) {
+        uint64_t gone = 0;  // bit t: point 32 t + lane goes
+        for (int t = 0; 32 * t < n; ++t) {
+            const int i = 32 * t + lane;
+            if (i >= n) break;
+            const int ki = c[i], Hi = H[i];
+            bool ab = false;
+#pragma unroll
+            for (int s = 1; s <= 64; s <<= 1)
+                if (i >= s && i + s < n) ab |= hull_above(c[i - s], H[i - s], ki, Hi, c[i + s], H[i + s]);
+            gone |= (uint64_t)ab << t;
+        }
+        static_assert(NT <= 64, "one bit per chunk");
+        __syncwarp();
+        int m = 0;
+        for (int t = 0; 32 * t < n; ++t) {
+            const int i = 32 * t + lane;
+            const bool keep = i < n && !((gone >> t) & 1);
+            const int ki = i < n ? c[i] : 0, Hi = i < n ? H[i] : 0;
+            __syncwarp();  // the chunk's reads before its writes (positions <= the chunk's)
+            const uint32_t bal = __ballot_sync(FULL, keep);
+            if (keep) {
+                const int pos = m + __popc(bal & ((1u << lane) - 1u));
+                c[pos] = (uint16_t)ki;
+                H[pos] = Hi;
+            }
+            m += __popc(bal);
+        }
+        __syncwarp();
+        if (m == n) break;
+        n = m;
+    }
+    return n;
+}
+
+// MODE 0: window filters of the coarse lines; 1: the coarse lines' filters
+// from their windows' (in place); 2: the group lines' filters.
+template <int MODE>
+__global__ void __launch_bounds__(32 * kHullWarps) k_hull(BandArgs a) {
+    extern __shared__ uint4 hull_raw[];
+    constexpr int CAP = MODE == 0 ? kHullWinCap : kHullCap;
+    char* wbase = reinterpret_cast<char*>(hull_raw) + (size_t)(threadIdx.x >> 5) * (CAP * 6);
+    int32_t* const H0 = reinterpret_cast<int32_t*>(wbase);             // [CAP]
+    uint16_t* const c0 = reinterpret_cast<uint16_t*>(wbase + CAP * 4);  // [CAP]
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int nwin = (a.Ww + 31) / 32;
+    const int64_t per_plane = MODE == 0 ? (int64_t)a.ncoarse * 2 * nwin : MODE == 1 ? (int64_t)a.ncoarse * 2
+                                                                                    : (int64_t)a.ngroups * 2;
+    int64_t task = (int64_t)blockIdx.x * kHullWarps + (threadIdx.x >> 5);
+    if (MODE == 2) task += (int64_t)a.grp0 * 2;
+    const int p = (int)(task / per_plane);
+    if (p >= a.nplanes || !band_plane(a, p)) return;  // warp-uniform
+    int t = (int)(task - (int64_t)p * per_plane);
+    int win = 0;
+    if (MODE == 0) {
+        win = t % nwin;
+        t /= nwin;
+    }
+    const int side = t & 1, grp = t >> 1;  // coarse group (MODE 0, 1) or group (MODE 2)
+    if (grp >= (MODE == 2 ? a.grp1 : a.ncoarse)) return;
+    const int nb = a.nb;
+    const int bper = MODE == 2 ? a.group : a.cbands;
+    const int gb0 = grp * bper, gb1 = min(nb - 1, gb0 + bper - 1);
+    const int kb = side ? gb1 : gb0;  // the key band of this side
+    const int line = side ? min(32 * (a.band0 + kb) + 31, a.Hg - 1) : 32 * (a.band0 + kb);
+    const uint16_t* car = (side ? a.below : a.above) + ((int64_t)p * nb + kb) * a.Wp;
+    const int w0 = MODE == 0 ? 32 * win : 0, w1 = MODE == 0 ? min(a.Ww, w0 + 32) : a.Ww;
+    const int cg = MODE == 2 ? gb0 / a.cbands : grp;
+    uint32_t* coarse = a.coarse + (((int64_t)p * a.ncoarse + cg) * 2 + side) * a.Ww;
+    uint32_t* out = MODE == 2 ? a.cand + (((int64_t)p * a.ngroups + grp) * 2 + side) * a.Ww : coarse;
+    const uint32_t* oc = a.objcol + (int64_t)p * nb * a.Ww;
+    // object columns between the coarse line and this group's line
+    const int cb0 = cg * a.cbands, cb1 = min(nb - 1, cb0 + a.cbands - 1);
+    const int r0 = side ? gb1 + 1 : cb0, r1 = side ? cb1 : gb0 - 1;
+
+    auto in_word = [&](int w) -> uint32_t {  // the input points of word w
+        if (MODE == 0) {                     // every column with a carry
+            uint32_t x = 0;
+            const int c0w = 32 * w;
+            if (c0w + 32 <= a.Wp) {
+                const uint4* q = reinterpret_cast<const uint4*>(car + c0w);
+                uint4 y[4];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) y[v] = __ldg(q + v);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const uint32_t u[4] = {y[v].x, y[v].y, y[v].z, y[v].w};
+#pragma unroll
+                    for (int z = 0; z < 4; ++z) {
+                        x |= (uint32_t)((u[z] & 0xffffu) != kNoRow) << (8 * v + 2 * z);
+                        x |= (uint32_t)((u[z] >> 16) != kNoRow) << (8 * v + 2 * z + 1);
+                    }
+                }
+            } else {
+                for (int c = 0; c < 32 && c0w + c < a.Wp; ++c) x |= (uint32_t)(__ldg(car + c0w + c) != kNoRow) << c;
+            }
+            if (a.W - c0w < 32) x &= a.W > c0w ? (1u << (a.W - c0w)) - 1u : 0u;
+            return x;
+        }
+        uint32_t x = coarse[w];
+        if (MODE == 2) {  // bands r0 .. r1 of the coarse group: running ORs, restarted every 32 bands
+            const uint32_t* run = (side ? a.objsuf : a.objpre) + (int64_t)p * nb * a.Ww;
+            if (side) {
+                x |= __ldg(run + (int64_t)r0 * a.Ww + w);  // r0 .. the end of r0's 32 bands
+                for (int b = cb0 + ((r0 - cb0) | 31) + 1; b <= r1; b += 32) x |= __ldg(run + (int64_t)b * a.Ww + w);
+            } else {
+                x |= __ldg(run + (int64_t)r1 * a.Ww + w);  // the start of r1's 32 bands .. r1
+                for (int b = cb0 + ((r1 - cb0) & ~31) - 1; b >= r0; b -= 32) x |= __ldg(run + (int64_t)b * a.Ww + w);
+            }
+        }
+        return x;
+    };
+    auto base_word = [&](int w) -> uint32_t {  // side 0 of a group: its own object columns
+        uint32_t x = 0;
+        if (MODE == 2 && side == 0)
+            for (int b = gb0; b <= gb1; ++b) x |= __ldg(oc + (int64_t)b * a.Ww + w);
+        return x;
+    };
+
+    if (MODE == 2 && r1 < r0) {  // the group's line is the coarse line: already filtered
+        for (int w = lane; w < a.Ww; w += 32) out[w] = coarse[w] | base_word(w);
+        return;
+    }
+    // ---- gather the points (compact, ascending columns): lane = a run of
+    // consecutive words, 8 words loaded before any is used ----
+    const int per = (w1 - w0 + 31) / 32;                  // words per lane
+    const int lw0 = min(w1, w0 + lane * per), lw1 = min(w1, lw0 + per);
+    int cnt = 0;
+    for (int w = lw0; w < lw1; w += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = w + u < lw1 ? in_word(w + u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cnt += __popc(x[u]);
+    }
+    int pre = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, pre, o);
+        if (lane >= o) pre += v;
+    }
+    int n = __shfl_sync(FULL, pre, 31);
+    if (n > CAP) {  // too many points for one warp: unfiltered (a superset of the hull)
+        for (int w = w0 + lane; w < w1; w += 32) {
+            const uint32_t x = in_word(w) | base_word(w);
+            out[w] = x;
+        }
+        return;
+    }
+    {
+        int pos = pre - cnt;
+        for (int w = lw0; w < lw1; ++w) {
+            uint32_t y = in_word(w);  // L1 / L2 hit
+            while (y) {               // four carries in flight
+                int kk[4], cr[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    kk[u] = y ? 32 * w + __ffs(y) - 1 : -1;
+                    y &= y - 1;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) cr[u] = kk[u] >= 0 ? (int)__ldg(car + kk[u]) : 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (kk[u] >= 0) {
+                        const int d = side ? cr[u] - line : line - cr[u];  // a listed column has a carry
+                        c0[pos] = (uint16_t)kk[u];
+                        H0[pos] = d * d + kk[u] * kk[u];
+                        ++pos;
+                    }
+            }
+        }
+    }
+    __syncwarp();
+    n = warp_prune<CAP>(c0, H0, n, lane);
+    // ---- the survivors' bits over the base words ----
+    for (int w = w0 + lane; w < w1; w += 32) out[w] = base_word(w);
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+        const int k = c0[i];
+        atomicOr(out + (k >> 5), 1u << (k & 31));
+    }
+}
+
+inline int hull_smem_bytes(int mode) { return kHullWarps * (mode == 0 ? kHullWinCap : kHullCap) * 6; }
 
 // ------------------------------------------------------------ per-row stacks
 // CTA = (plane, band), kBandWarps warps.  The band's candidates (the group's
@@ -267,7 +411,7 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int MASK = kBandCap - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t task = blockIdx.x;
+    const int64_t task = (int64_t)a.task0 + blockIdx.x;
     const int p = (int)(task / a.nb), b = (int)(task - (int64_t)p * a.nb);
     if (!band_plane(a, p)) return;  // CTA-uniform
     const int s = p / a.n_img, im = p - s * a.n_img;
@@ -525,16 +669,16 @@ struct FillSmem {
     uint16_t r[kFillCap];
 };
 
+template <int DONLY>  // lr_fill_row's mode
 __global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandArgs a) {
     extern __shared__ uint4 fill_raw[];
     FillSmem& sm = reinterpret_cast<FillSmem*>(fill_raw)[threadIdx.x >> 5];
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int W = a.W;
-    const int64_t total = (int64_t)a.nplanes * a.H;
+    const int64_t total = a.frow1;
     const int64_t nw = (int64_t)gridDim.x * kFillWarps;
-    const bool donly = ra.D && !ra.S && !ra.LB && !ra.NC;
-    for (int64_t row = (int64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5); row < total; row += nw) {
+    for (int64_t row = a.frow0 + (int64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5); row < total; row += nw) {
         const int p = (int)(row / a.H);
         if (!band_plane(a, p)) continue;  // warp-uniform
         const int64_t iR = row - (int64_t)p * a.H;
@@ -557,10 +701,7 @@ __global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandA
                     sm.r[q] = __ldcg(gR + q);
                 }
                 __syncwarp();
-                if (donly)
-                    lr_fill_row<true>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
-                else
-                    lr_fill_row<false>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+                lr_fill_row<DONLY>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
                 continue;
             }
             // a long list (dense stretches): 32-column blocks straight from L2

@@ -63,11 +63,11 @@ __device__ __forceinline__ const uint16_t* lr_col_ptr(const RowArgs& a, const ui
 
 // Fill one row's columns [c0, c1) from its entry list (column | start << 16,
 // plus the column's nearest row), lane = column; shared by k_rows_lr and
-// k_rows_pts.  rE / rR are in shared memory.  DONLY: only Drow is written
-// (the caller checked S, LB and NC are null), so a block with few owners
-// needs no owner per column: D(j) is the minimum of the block's owners'
-// parabolas (each is >= the envelope, and j's owner is among them).
-template <bool DONLY = false>
+// k_rows_pts.  rE / rR are in shared memory.  DONLY: only values are written
+// (Drow, optionally Srow; the caller checked LB and NC are null), so a block
+// needs no owner per column: D(j) is the minimum of the parabolas of the
+// owners around j (each is >= the envelope, and j's owner is among them).
+template <int DONLY = 0>  // 0: owners per column; 1: values only, D; 2: values only, D and sqrt D
 __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE, const uint16_t* rR, int nE,
                                             uint32_t giR, int32_t* Drow, float* Srow, int32_t* Lrow,
                                             int32_t* Nrow, int c0, int c1, int lane) {
@@ -80,6 +80,22 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
         if (Srow) __stcs(Srow + j, dist_f32(d));
         if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(r * (uint32_t)W + k));
         if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+    };
+    auto put4 = [&](int j, bool fast, uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3) {  // values only
+        if (fast || (vec4 && j + 3 < c1)) {
+            __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d0, (int)d1, (int)d2, (int)d3));
+            if (DONLY == 2)
+                __stcs(reinterpret_cast<float4*>(Srow + j),
+                       make_float4(dist_f32(d0), dist_f32(d1), dist_f32(d2), dist_f32(d3)));
+        } else {
+            const uint32_t d[4] = {d0, d1, d2, d3};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (j + t < c1) {
+                    __stcs(Drow + j + t, (int32_t)d[t]);
+                    if (DONLY == 2) __stcs(Srow + j + t, dist_f32(d[t]));
+                }
+        }
     };
     auto dval = [&](uint32_t g, uint32_t k, int j) -> uint32_t {
         const int dj = j - (int)k;
@@ -97,93 +113,64 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
         const uint32_t wav = giR > wr ? giR - wr : wr - giR;
         const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
         if (DONLY) {
-            // ---- D only, a 512-column block with at most 3 owner changes (the
-            // usual case on sparse planes): lane l owns columns b + 128 h + 4 l
-            // + t (coalesced 16-byte stores per h); D(j) is the minimum of the
-            // block's owners' parabolas g + (j - k)^2 (uint32: each of them is
-            // an owner of a column of this block, so its value at any column of
-            // the block is < 2^31 + 2^26) ----
+            // ---- values only, a 512-column block whose owners all sit in the
+            // window (the usual case on sparse planes): lane l owns columns
+            // b + 128 h + 4 l + t (coalesced 16-byte stores per h).  cnt[h] =
+            // entries starting at or before b + 128 h, so sub-block h is owned
+            // by entries cnt[h] .. cnt[h+1] (warp-uniform), and D(j) is the
+            // minimum of THEIR parabolas g + (j - k)^2: each is >= the
+            // envelope and j's owner is among them (uint32: an entry that owns
+            // a column within 512 of j has a value < 2^31 + 2^26 at j) ----
             constexpr int kH = 4;
-            const int nbig = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 128 * kH - 1));
-            if (nbig <= 3) {
-                const uint32_t g0 = __shfl_sync(FULL, wg, 0);
-                const int k0 = (int)__shfl_sync(FULL, wk, 0);
-                uint32_t d[kH][4];
-                if (g0 == kInfU) {  // featureless row: its only entry
+            const int s31 = __shfl_sync(FULL, s, 31);
+            if (s31 > b + 128 * kH) {  // the window holds every start up to b + 512
+                int cnt[kH + 1];
+                cnt[0] = 0;
 #pragma unroll
-                    for (int h = 0; h < kH; ++h)
+                for (int h = 1; h <= kH; ++h) cnt[h] = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 128 * h));
+                const bool fast = vec4 && b + 128 * kH <= c1;
+                if (__shfl_sync(FULL, wk, 0) == kLrInfK) {  // featureless row: its only entry
 #pragma unroll
-                        for (int t = 0; t < 4; ++t) d[h][t] = (uint32_t)DFC_INF_I32;
+                    for (int h = 0; h < kH; ++h) {
+                        const int j = b + 128 * h + 4 * lane;
+                        const uint32_t di = (uint32_t)DFC_INF_I32;
+                        put4(j, fast, di, di, di, di);
+                    }
                 } else {
 #pragma unroll
                     for (int h = 0; h < kH; ++h) {
-                        const int dj = b + 128 * h + 4 * lane - k0;
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) d[h][t] = g0 + (uint32_t)((dj + t) * (dj + t));
-                    }
-                    for (int e = 1; e <= nbig; ++e) {  // warp-uniform trip count
-                        const uint32_t ge = __shfl_sync(FULL, wg, e);
-                        const int ke = (int)__shfl_sync(FULL, wk, e);
-#pragma unroll
-                        for (int h = 0; h < kH; ++h) {
-                            const int dj = b + 128 * h + 4 * lane - ke;
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) d[h][t] = min(d[h][t], ge + (uint32_t)((dj + t) * (dj + t)));
+                        const int j = b + 128 * h + 4 * lane;
+                        uint32_t d0, d1, d2, d3;
+                        {
+                            const uint32_t ge = __shfl_sync(FULL, wg, cnt[h]);
+                            const int dj = j - (int)__shfl_sync(FULL, wk, cnt[h]);
+                            const uint32_t inc = (uint32_t)(2 * dj + 1);
+                            d0 = ge + (uint32_t)(dj * dj);
+                            d1 = d0 + inc;
+                            d2 = d1 + inc + 2u;
+                            d3 = d2 + inc + 4u;
                         }
+                        for (int e = cnt[h] + 1; e <= cnt[h + 1]; ++e) {  // warp-uniform trip count
+                            const uint32_t ge = __shfl_sync(FULL, wg, e);
+                            const int dj = j - (int)__shfl_sync(FULL, wk, e);
+                            const uint32_t inc = (uint32_t)(2 * dj + 1);
+                            const uint32_t v0 = ge + (uint32_t)(dj * dj);
+                            const uint32_t v1 = v0 + inc, v2 = v1 + inc + 2u, v3 = v2 + inc + 4u;
+                            d0 = min(d0, v0);
+                            d1 = min(d1, v1);
+                            d2 = min(d2, v2);
+                            d3 = min(d3, v3);
+                        }
+                        put4(j, fast, d0, d1, d2, d3);
                     }
                 }
-#pragma unroll
-                for (int h = 0; h < kH; ++h) {
-                    const int j = b + 128 * h + 4 * lane;
-                    if (vec4 && j + 3 < c1) {
-                        __stcs(reinterpret_cast<int4*>(Drow + j),
-                               make_int4((int)d[h][0], (int)d[h][1], (int)d[h][2], (int)d[h][3]));
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 4; ++t)
-                            if (j + t < c1) __stcs(Drow + j + t, (int32_t)d[h][t]);
-                    }
-                }
-                // the next block's first owner: the last entry starting <= b + 128 kH
-                const int sn = __shfl_sync(FULL, s, nbig + 1);
-                base += nbig + (sn == b + 128 * kH ? 1 : 0);
+                base += cnt[kH];  // the last entry starting at or before b + 512
                 b += 128 * kH;
                 continue;
             }
         }
         const int nin = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 127));
-        if (DONLY && nin <= 3) {
-            // ---- D only, at most 3 owner changes: minimum over the block's
-            // owners' parabolas g + (j - k)^2 (uint32: every value of an owner
-            // of this block is < 2^31 + 2^24 at its columns) ----
-            const int j = b + 4 * lane;
-            const uint32_t g0 = __shfl_sync(FULL, wg, 0);
-            uint32_t d[4];
-            if (g0 == kInfU) {  // featureless row: its only entry
-#pragma unroll
-                for (int t = 0; t < 4; ++t) d[t] = (uint32_t)DFC_INF_I32;
-            } else {
-                const int dj0 = j - (int)__shfl_sync(FULL, wk, 0);
-#pragma unroll
-                for (int t = 0; t < 4; ++t) d[t] = g0 + (uint32_t)((dj0 + t) * (dj0 + t));
-                for (int e = 1; e <= nin; ++e) {  // warp-uniform trip count
-                    const uint32_t ge = __shfl_sync(FULL, wg, e);
-                    const int dje = j - (int)__shfl_sync(FULL, wk, e);
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) d[t] = min(d[t], ge + (uint32_t)((dje + t) * (dje + t)));
-                }
-            }
-            if (vec4 && j + 3 < c1) {
-                __stcs(reinterpret_cast<int4*>(Drow + j), make_int4((int)d[0], (int)d[1], (int)d[2], (int)d[3]));
-            } else {
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (j + t < c1) __stcs(Drow + j + t, (int32_t)d[t]);
-            }
-            const int sn = __shfl_sync(FULL, s, nin + 1);
-            base += nin + (sn == b + 128 ? 1 : 0);
-            b += 128;
-        } else if (nin <= 3) {
+        if (nin <= 3) {
             // ---- 128-column block with at most 3 owner changes (sparse rows):
             // broadcast the block's owners, each column keeps the last one
             // starting at or before it ----
@@ -576,9 +563,9 @@ __global__ void __launch_bounds__(32 * kLrWarps, 8) k_rows_lr(RowArgs a, uint32_
             const uint32_t* rE = sE + (rho - r0) * S;
             const uint16_t* rR = sR + (rho - r0) * S;
             if (Drow && !Srow && !Lrow && !Nrow)
-                lr_fill_row<true>(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+                lr_fill_row<1>(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
             else
-                lr_fill_row<false>(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+                lr_fill_row<0>(a, rE, rR, nE, giR, Drow, Srow, Lrow, Nrow, c0, c1, lane);
         }
     }
     // rows whose list exceeds the staging capacity (chunks wider than kStage

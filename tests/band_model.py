@@ -1,5 +1,5 @@
 """Pure-Python model of the band-candidate row pass for sparse planes
-(csrc/k_rows_band.cu): k_band_hull + k_band_rows + k_rows_fill.
+(csrc/k_rows_band.cu): k_hull (hull filter) + k_band_rows + k_rows_fill.
 
 Test infrastructure only; statement-level mirror of the kernels, fuzzed
 against brute force in tests/test_band_model.py.
@@ -188,6 +188,69 @@ def window_hull(car, line, w0, lane_cols=32, lanes=32, W=None, cap=None):
     return out
 
 
+def list_prune(pts, rounds=10, strides=(1, 2, 4, 8, 16, 32, 64)):
+    """warp_prune (k_rows_band.cu): a compact ascending point list [(k, H)]
+    pruned towards its lower hull.  Each round marks point i when it lies
+    strictly above the chord of its list neighbours i - s and i + s for some
+    stride s (all marks from the same snapshot), then compacts the survivors.
+    Returns the surviving columns: a superset of the hull, collinear points
+    kept."""
+    col = [p[0] for p in pts]
+    Hh = [p[1] for p in pts]
+    for _ in range(rounds):
+        n = len(col)
+        if n < 3:
+            break
+        gone = [False] * n
+        for i in range(n):
+            for s in strides:
+                if i >= s and i + s < n and _strictly_above(col[i - s], Hh[i - s], col[i], Hh[i], col[i + s], Hh[i + s]):
+                    gone[i] = True
+        if not any(gone):
+            break
+        col = [c for c, g in zip(col, gone) if not g]
+        Hh = [h for h, g in zip(Hh, gone) if not g]
+    return set(col)
+
+
+def hier_group_candidates(above, below, masks, g0, g1, cb0, cb1, H, W, lanes=32, win=None, cap=None):
+    """The candidate columns of bands g0..g1 (a group) inside the coarse group
+    cb0..cb1, as k_hull<0/1/2> compute them: filters (list_prune) at the coarse
+    lines over all columns (per window of `win` columns, then over the windows'
+    survivors), then at the group's line over the coarse survivors plus the
+    object columns in between; plus the group's own object columns.  A list
+    longer than `cap` is passed through unfiltered.  `lanes` = prune rounds."""
+    win = W if win is None else win
+
+    def hull_of(cols, car, line):
+        cols = sorted(c for c in cols if car[c] is not None)
+        if cap is not None and len(cols) > cap:
+            return set(cols)
+        return list_prune([(k, (line - car[k]) ** 2 + k * k) for k in cols], rounds=lanes)
+
+    def objcols(b0, b1):
+        return set(k for bb in range(b0, b1 + 1) for k in range(W) if masks[bb][k])
+
+    out = objcols(g0, g1)
+    for side in (0, 1):
+        ckb = cb1 if side else cb0
+        car_c = below[ckb] if side else above[ckb]
+        cline = min(32 * ckb + 31, H - 1) if side else 32 * ckb
+        wins = set()
+        for w0 in range(0, W, win):
+            wins |= hull_of(range(w0, min(W, w0 + win)), car_c, cline)
+        coarse = hull_of(wins, car_c, cline)
+        gkb = g1 if side else g0
+        car_g = below[gkb] if side else above[gkb]
+        gline = min(32 * gkb + 31, H - 1) if side else 32 * gkb
+        if (side == 0 and g0 == cb0) or (side == 1 and g1 == cb1):
+            out |= coarse
+        else:
+            between = objcols(g1 + 1, cb1) if side else objcols(cb0, g0 - 1)
+            out |= hull_of(coarse | between, car_g, gline)
+    return out
+
+
 def band_candidates(above, below, masks, b, H, W, lane_cols=32, lanes=32, hcap=None):
     i0, i1 = 32 * b, min(32 * b + 31, H - 1)
     cand = set(k for k in range(W) if masks[b][k])
@@ -342,7 +405,7 @@ def fill(lst, i, W):
     return D, K, R
 
 
-def band_transform_chunked(img, take_new=False, nch=8, cap=16, group=1):
+def band_transform_chunked(img, take_new=False, nch=8, cap=16, group=1, coarse=None, lanes=32, win=None, hcap=None):
     """(D, K, R) via grouped candidates (k_band_hull: hullA of the group's first
     band + hullB of its last + the group's object columns) and chunked stacks."""
     H, W = len(img), len(img[0])
@@ -353,10 +416,15 @@ def band_transform_chunked(img, take_new=False, nch=8, cap=16, group=1):
         g0 = b // group * group
         g1 = min(nb - 1, g0 + group - 1)
         cand = set()
-        for bb in range(g0, g1 + 1):
-            cand |= set(k for k in range(W) if masks[bb][k])
-        cand |= window_hull(above[g0], 32 * g0, 0, W, 1, W)
-        cand |= window_hull(below[g1], min(32 * g1 + 31, H - 1), 0, W, 1, W)
+        if coarse is not None:  # k_hull: coarse lines, then the group's lines
+            cb0 = g0 // coarse * coarse
+            cand = hier_group_candidates(above, below, masks, g0, g1, cb0, min(nb - 1, cb0 + coarse - 1), H, W,
+                                         lanes, win, hcap)
+        else:
+            for bb in range(g0, g1 + 1):
+                cand |= set(k for k in range(W) if masks[bb][k])
+            cand |= window_hull(above[g0], 32 * g0, 0, W, 1, W)
+            cand |= window_hull(below[g1], min(32 * g1 + 31, H - 1), 0, W, 1, W)
         cand = sorted(cand)
         for i in range(32 * b, min(32 * b + 32, H)):
             D, K, R = [None] * W, [None] * W, [None] * W

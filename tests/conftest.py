@@ -27,3 +27,13 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _debug_guards(request):
+    """DFC_DEBUG_GUARD=1: after every GPU test, check the canary zones around
+    the outputs and the library's scratch allocations (tools/guard_run.sh)."""
+    yield
+    if os.environ.get("DFC_DEBUG_GUARD") == "1" and "gpu" in request.keywords:
+        import paper_2106_03503_b200 as dfc
+        dfc.check_guards()

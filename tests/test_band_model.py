@@ -97,3 +97,61 @@ def test_band_model_grouped_chunked(take_new):
         assert K == bK, (it, mode, H, W)
         if not take_new:
             assert R == bR, (it, mode, H, W)
+
+
+def test_list_prune_is_superset_of_hull_and_converges():
+    """warp_prune: never drops a hull point (collinear ones included), whatever
+    the number of rounds; with enough rounds it reaches the hull itself."""
+    rnd = random.Random(8)
+    for _ in range(150):
+        W = rnd.randint(1, 160)
+        line = rnd.randint(0, 300)
+        car = [rnd.randint(0, line) if rnd.random() < rnd.choice([0.1, 0.6, 1.0]) else None for _ in range(W)]
+        r = rnd.random()
+        if r < 0.15:    # equal carries on a column lattice
+            car = [line - 3 if k % 2 == 0 else None for k in range(W)]
+        elif r < 0.3:   # bowls between deep minima
+            car = [line - rnd.randint(40, 60) for _ in range(W)]
+            for _ in range(rnd.randint(1, 4)):
+                car[rnd.randrange(W)] = line
+        glob = bm.window_hull(car, line, 0, lane_cols=W, lanes=1)
+        pts = [(k, (line - car[k]) ** 2 + k * k) for k in range(W) if car[k] is not None]
+        for rounds in (0, 1, 2, 10):
+            got = bm.list_prune(pts, rounds)
+            assert glob <= got <= set(k for k, _ in pts)
+        assert bm.list_prune(pts, 10 ** 6, strides=(1,)) == glob  # the fixed point of stride 1 is the hull
+
+
+@pytest.mark.parametrize("take_new", [False, True])
+def test_band_model_hierarchical_hulls(take_new):
+    """Coarse lines over all columns, group lines over the coarse survivors plus
+    the object columns in between (k_hull<0/1/2>, any number of prune rounds),
+    then the chunked stacks: equal to brute force; and the group lines' filters
+    contain the hulls over all columns."""
+    rnd = random.Random(31 + take_new)
+    for it in range(30):
+        H = rnd.randint(1, 300)
+        W = rnd.randint(1, 70)
+        mode = rnd.choice(["bern", "bern", "rowline", "few", "lattice"])
+        img = _img(rnd, H, W, rnd.choice([0.0, 0.003, 0.02, 0.1]), mode)
+        group = rnd.choice([1, 2])
+        coarse = group * rnd.choice([1, 2, 4])
+        D, K, R = bm.band_transform_chunked(img, take_new, nch=rnd.choice([1, 3, 8]), cap=rnd.choice([2, 16]),
+                                            group=group, coarse=coarse, lanes=rnd.choice([0, 1, 3, 10]),
+                                            win=rnd.choice([None, 8, 32]), hcap=rnd.choice([None, 3, 10]))
+        bD, bK, bR = bm.brute(img, take_new)
+        assert D == bD, (it, mode, H, W)
+        assert K == bK, (it, mode, H, W)
+        if not take_new:
+            assert R == bR, (it, mode, H, W)
+        if it % 5 == 0:  # the hierarchy loses no hull point
+            above, below, masks = bm.carries(img, H, W)
+            nb = (H + 31) // 32
+            for g0 in range(0, nb, group):
+                g1 = min(nb - 1, g0 + group - 1)
+                cb0 = g0 // coarse * coarse
+                got = bm.hier_group_candidates(above, below, masks, g0, g1, cb0, min(nb - 1, cb0 + coarse - 1), H, W)
+                want = set(k for bb in range(g0, g1 + 1) for k in range(W) if masks[bb][k])
+                want |= bm.window_hull(above[g0], 32 * g0, 0, W, 1, W)
+                want |= bm.window_hull(below[g1], min(32 * g1 + 31, H - 1), 0, W, 1, W)
+                assert got >= want

@@ -1,0 +1,25 @@
+#!/bin/bash
+# round-2 experiments: new D-only fill + sliced/pipelined band path
+O=gpurun_out/exp2; mkdir -p $O
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "band or sharded or sparse or tall or tiles or point or lr_" > $O/tests.log 2>&1; echo rc=$? >> $O/tests.log
+tail -3 $O/tests.log
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -x -k "c5" > $O/tests_c5.log 2>&1; echo rc=$? >> $O/tests_c5.log
+tail -3 $O/tests_c5.log
+B="python bench.py --config c5 --steps 10 --warmup 3 --no-cpu-baseline"
+for s in 1 2 4 8 16; do for f in 3 4 6; do
+  DFC_BAND_SLICES=$s DFC_FILL_CTAS=$f timeout 300 $B > $O/c5_s${s}_f$f.json 2> $O/c5_s${s}_f$f.err
+  echo "slices=$s fill_ctas=$f $(python -c "import json;print(json.load(open('$O/c5_s${s}_f$f.json'))['ms_per_step'])")"
+done; done | tee $O/sweep.txt
+for g in 2 8 16; do
+  DFC_BAND_GROUP=$g timeout 300 $B > $O/c5_g$g.json 2> $O/c5_g$g.err
+  echo "group=$g $(python -c "import json;print(json.load(open('$O/c5_g$g.json'))['ms_per_step'])")"
+done | tee -a $O/sweep.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv -c 80 \
+  python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline > $O/launches.csv 2>&1
+python profiles/launch_summary.py $O/launches.csv > $O/launches.txt; cat $O/launches.txt
+# C2 background plane through the band path
+for d in 8 4; do
+  DFC_SPARSE_DIV=$d timeout 300 python -m pytest tests/test_gpu_fullsize.py -q -x -k "c2_full or c1_full" > $O/c2_div$d.tests 2>&1; echo rc=$? >> $O/c2_div$d.tests
+  DFC_SPARSE_DIV=$d timeout 300 python bench.py --config c2 --steps 50 --warmup 5 --no-cpu-baseline > $O/c2_div$d.json 2> $O/c2_div$d.err
+  echo "c2 div=$d $(tail -1 $O/c2_div$d.tests) $(python -c "import json;print(json.load(open('$O/c2_div$d.json'))['ms_per_step'])")"
+done | tee -a $O/sweep.txt
