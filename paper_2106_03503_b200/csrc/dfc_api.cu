@@ -280,19 +280,7 @@ bool band_sparse_on() {
     return on;
 }
 
-// Slices of the band path (DFC_BAND_SLICES, tuning; 1 = no pipelining).
-int band_slices() {
-    static const int n = [] {
-        const char* v = getenv("DFC_BAND_SLICES");
-        const int x = v ? atoi(v) : 0;
-        return x >= 1 && x <= 16 ? x : 1;
-    }();
-    return n;
-}
-
-// k_rows_fill CTAs per SM (DFC_FILL_CTAS, tuning): few enough that the next
-// slice's k_hull / k_band_rows CTAs find registers and shared memory
-// beside the resident fill CTAs.
+// k_rows_fill CTAs per SM (DFC_FILL_CTAS, tuning) of the unfused launch.
 int fill_ctas() {
     static const int n = [] {
         const char* v = getenv("DFC_FILL_CTAS");
@@ -302,66 +290,32 @@ int fill_ctas() {
     return n;
 }
 
-// Per-device helper stream and events of the pipelined band path: a
-// high-priority stream runs the hull filter and the per-row stacks of slice
-// s + 1 while the caller's stream fills slice s (the fill is HBM-bound, the
-// other two latency-bound).  Fork/join by events only -- no host
-// synchronisation, legal under stream capture.  The mutex serialises the
-// host-side enqueue per device (the events are shared).
-constexpr int kMaxSlices = 16;
-struct BandPipe {
-    std::mutex mu;
-    cudaStream_t aux = nullptr;
-    cudaEvent_t fork = nullptr;
-    cudaEvent_t done[kMaxSlices] = {};
-    bool ok = false;
-};
-BandPipe* band_pipe() {
-    constexpr int kMaxDev = 64;
-    static BandPipe pipes[kMaxDev];
-    static std::once_flag flags[kMaxDev];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
-    BandPipe* bp = &pipes[dev];
-    std::call_once(flags[dev], [bp] {
-        int least = 0, greatest = 0;
-        cudaDeviceGetStreamPriorityRange(&least, &greatest);
-        bool ok = cudaStreamCreateWithPriority(&bp->aux, cudaStreamNonBlocking, greatest) == cudaSuccess;
-        ok = ok && cudaEventCreateWithFlags(&bp->fork, cudaEventDisableTiming) == cudaSuccess;
-        for (int i = 0; i < kMaxSlices && ok; ++i)
-            ok = cudaEventCreateWithFlags(&bp->done[i], cudaEventDisableTiming) == cudaSuccess;
-        bp->ok = ok;
-        if (!ok) cudaGetLastError();
-    });
-    return bp->ok ? bp : nullptr;
+// DFC_BAND_FUSED=0 (A/B): k_band_rows and k_rows_fill as two launches instead
+// of one CTA per band doing both
+bool band_fused() {
+    static const bool on = [] {
+        const char* v = getenv("DFC_BAND_FUSED");
+        return !(v && v[0] == '0');
+    }();
+    return on;
 }
 
-// The band path (k_rows_band.cu) over the sparse planes of `ba`: hull filter,
-// per-row stacks, fill into a's outputs.  A single plane with enough bands is
-// cut into slices of whole candidate groups, pipelined over two streams.
-int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cudaStream_t st) {
-    const int hsm0 = hull_smem_bytes(0), hsm = hull_smem_bytes(1);
-    cudaError_t e = cudaFuncSetAttribute(k_hull<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm0);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hull<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_hull<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsm);
-    if (e != cudaSuccess) return cuda_fail(e);
-    const int rsm = band_rows_smem_bytes();
-    const void* rfn = take_new ? (const void*)k_band_rows<true> : (const void*)k_band_rows<false>;
-    e = cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
-    if (e != cudaSuccess) return cuda_fail(e);
-    const int donly = a.D && !a.LB && !a.NC ? (a.S ? 2 : 1) : 0;  // values only (D, optionally sqrt D)
-    const void* ffn = donly == 1 ? (const void*)k_rows_fill<1> : donly == 2 ? (const void*)k_rows_fill<2>
-                                                                            : (const void*)k_rows_fill<0>;
-    const int fsm = fill_smem_bytes();
-    e = cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
-    if (e != cudaSuccess) return cuda_fail(e);
+template <bool TN, int DO>
+cudaError_t launch_rows_fill(const RowArgs& a, const BandArgs& ba, unsigned grid, int smem, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute(k_band_rows_fill<TN, DO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k_band_rows_fill<TN, DO><<<grid, 32 * kBandWarps, smem, st>>>(a, ba);
+    return cudaSuccess;
+}
 
-    // object columns per band and the coarse lines' hulls (all columns) first
+// The band path (k_rows_band.cu) over the sparse planes of `ba`: object-column
+// runs, hull filter (coarse lines, then the groups' lines), per-row stacks and
+// fill into a's outputs.
+int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
     BandArgs ba = ba_in;
     ba.cbands = ba.group >= kCoarseBands ? ba.group : kCoarseBands / ba.group * ba.group;
     ba.ncoarse = (ba.nb + ba.cbands - 1) / ba.cbands;
-    ba.grp0 = 0;
-    ba.grp1 = ba.ngroups;
     Scratch hs(st);
     const size_t oc_bytes = (size_t)round_up((int64_t)ba.nplanes * ba.nb * ba.Ww * 4, 256);
     const size_t co_bytes = (size_t)round_up((int64_t)ba.nplanes * ba.ncoarse * 2 * ba.Ww * 4, 256);
@@ -376,53 +330,58 @@ int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cud
         k_band_objcols<<<dim3((unsigned)((ba.Ww * 32 + 255) / 256), (unsigned)std::min(ba.nb, 64), (unsigned)ba.nplanes), 256, 0, st>>>(ba);
         ++g_launches;
     }
-    auto warps_grid = [](int64_t tasks) { return (unsigned)((tasks + kHullWarps - 1) / kHullWarps); };
     const int nwin = (ba.Ww + 31) / 32;
     k_objcol_runs<<<dim3((unsigned)((ba.Ww + 127) / 128), (unsigned)ba.ncoarse, (unsigned)ba.nplanes), 128, 0, st>>>(ba);
-    k_hull<0><<<warps_grid((int64_t)ba.nplanes * ba.ncoarse * 2 * nwin), 32 * kHullWarps, hsm0, st>>>(ba);
-    k_hull<1><<<warps_grid((int64_t)ba.nplanes * ba.ncoarse * 2), 32 * kHullWarps, hsm, st>>>(ba);
-    g_launches += 3;
+    k_hull<0><<<(unsigned)((int64_t)ba.nplanes * ba.ncoarse * 2 * nwin), kHullThreads, 0, st>>>(ba);
+    k_hull<1><<<(unsigned)((int64_t)ba.nplanes * ba.ncoarse * 2), kHullThreads, 0, st>>>(ba);
+    k_hull<2><<<(unsigned)((int64_t)ba.nplanes * ba.ngroups * 2), kHullThreads, 0, st>>>(ba);
+    g_launches += 4;
 
-    int S = ba.nplanes == 1 ? std::min(band_slices(), ba.ngroups / 8) : 1;
-    BandPipe* bp = S > 1 ? band_pipe() : nullptr;
-    if (!bp) S = 1;
-    std::unique_lock<std::mutex> lock;
-    if (bp) {
-        lock = std::unique_lock<std::mutex>(bp->mu);
-        if ((e = cudaEventRecord(bp->fork, st)) != cudaSuccess) return cuda_fail(e);
-        if ((e = cudaStreamWaitEvent(bp->aux, bp->fork, 0)) != cudaSuccess) return cuda_fail(e);
-    }
-    cudaStream_t cs = bp ? bp->aux : st;  // hull filter + per-row stacks
-    for (int s = 0; s < S; ++s) {
-        BandArgs hb = ba;
-        const int g0 = (int)((int64_t)ba.ngroups * s / S), g1 = (int)((int64_t)ba.ngroups * (s + 1) / S);
-        const int b0 = bp ? g0 * ba.group : 0;
-        const int b1 = bp ? std::min(ba.nb, g1 * ba.group) : ba.nb;
-        hb.grp0 = bp ? g0 : 0;
-        hb.grp1 = bp ? g1 : ba.ngroups;
-        hb.task0 = b0;
-        hb.frow0 = bp ? (int64_t)32 * b0 : 0;
-        hb.frow1 = bp ? std::min<int64_t>(ba.H, (int64_t)32 * b1) : (int64_t)ba.nplanes * ba.H;
-        k_hull<2><<<warps_grid(bp ? (int64_t)(g1 - g0) * 2 : (int64_t)ba.nplanes * ba.ngroups * 2), 32 * kHullWarps, hsm, cs>>>(hb);
-        const int64_t tasks = bp ? b1 - b0 : (int64_t)ba.nplanes * ba.nb;
+    const int donly = a.D && !a.LB && !a.NC ? (a.S ? 2 : 1) : 0;  // values only (D, optionally sqrt D)
+    const int64_t tasks = (int64_t)ba.nplanes * ba.nb;
+    const int rsm = band_rows_smem_bytes();
+    if (band_fused()) {
+        const unsigned g = (unsigned)tasks;
+        // CTAs per SM of the fused kernel, by shared memory (DFC_BAND_OCC, tuning):
+        // measured on C5: 4 (the stack phases need the parallelism) 1.356 ms, 3 1.451, 2 1.533, 1 2.082
+        static const int occ = [] {
+            const char* v = getenv("DFC_BAND_OCC");
+            const int x = v ? atoi(v) : 0;
+            return x >= 1 && x <= 4 ? x : 4;
+        }();
+        const int rsm_occ = std::max(rsm, std::min(227 * 1024, (228 * 1024) / occ - 1024 - 1024) / 16 * 16);
+        const int rsm = rsm_occ;
         if (take_new)
-            k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, cs>>>(hb);
+            e = donly == 1 ? launch_rows_fill<true, 1>(a, ba, g, rsm, st)
+                           : donly == 2 ? launch_rows_fill<true, 2>(a, ba, g, rsm, st) : launch_rows_fill<true, 0>(a, ba, g, rsm, st);
         else
-            k_band_rows<false><<<(unsigned)tasks, 32 * kBandWarps, rsm, cs>>>(hb);
-        if (bp) {
-            if ((e = cudaEventRecord(bp->done[s], cs)) != cudaSuccess) return cuda_fail(e);
-            if ((e = cudaStreamWaitEvent(st, bp->done[s], 0)) != cudaSuccess) return cuda_fail(e);
-        }
-        const int64_t rows = hb.frow1 - hb.frow0;
-        const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * fill_ctas()));
-        if (donly == 1)
-            k_rows_fill<1><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
-        else if (donly == 2)
-            k_rows_fill<2><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
-        else
-            k_rows_fill<0><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, hb);
-        g_launches += 3;
+            e = donly == 1 ? launch_rows_fill<false, 1>(a, ba, g, rsm, st)
+                           : donly == 2 ? launch_rows_fill<false, 2>(a, ba, g, rsm, st) : launch_rows_fill<false, 0>(a, ba, g, rsm, st);
+        if (e != cudaSuccess) return cuda_fail(e);
+        ++g_launches;
+        return DFC_OK;
     }
+    const void* rfn = take_new ? (const void*)k_band_rows<true> : (const void*)k_band_rows<false>;
+    e = cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const void* ffn = donly == 1 ? (const void*)k_rows_fill<1> : donly == 2 ? (const void*)k_rows_fill<2>
+                                                                            : (const void*)k_rows_fill<0>;
+    const int fsm = fill_smem_bytes();
+    e = cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (take_new)
+        k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(ba);
+    else
+        k_band_rows<false><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(ba);
+    const int64_t rows = (int64_t)ba.nplanes * ba.H;
+    const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * fill_ctas()));
+    if (donly == 1)
+        k_rows_fill<1><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
+    else if (donly == 2)
+        k_rows_fill<2><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
+    else
+        k_rows_fill<0><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
+    g_launches += 2;
     return DFC_OK;
 }
 

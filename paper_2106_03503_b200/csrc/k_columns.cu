@@ -35,6 +35,11 @@ __device__ __forceinline__ void band_masks(const uint8_t* __restrict__ base, int
 #pragma unroll
         for (int r = 0; r < kBand; ++r, p += pitch)
             v[r] = r < nrows ? __ldg(reinterpret_cast<const uint32_t*>(p)) : 0u;
+        // sparse images: most threads see 128 zero bytes (16 three-input ORs)
+        uint32_t any = 0u;
+#pragma unroll
+        for (int r = 0; r < kBand; r += 2) any |= v[r] | v[r + 1];
+        if (any == 0u) return;
         // 4 x 32 bit transpose: x[g] byte c bit b = row 8g + b of column c
         // (one 0xff-per-nonzero-byte compare and one masked OR per row), then
         // each column's word gathers byte c of x[0..3] with three byte permutes

@@ -22,7 +22,7 @@
 //              is exact (the row pass evaluates each candidate's true g_k(i)),
 //              so the hulls are taken per window of 1024 columns (a hull point
 //              of the row is a hull point of every window holding it):
-//  k_hull      one warp prunes one compact point list towards its lower hull
+//  k_hull      one CTA prunes one compact point list towards its lower hull
 //              (data-parallel rounds: a point above the chord of two list
 //              neighbours goes, survivors are compacted); filters at coarse
 //              lines over all columns (per window, then per line), at the
@@ -77,11 +77,6 @@ struct BandArgs {
     int cbands, ncoarse;     // bands per coarse group (a multiple of group), coarse groups per plane
     bool pts_gate;           // point planes belong to k_rows_pts
     bool all_planes;         // every plane (the sharded path), not only the sparse ones
-    // one slice of a single plane's bands (launch_band_path pipelines slices
-    // over two streams): first group of k_band_hull's grid, first band of
-    // k_band_rows' grid, k_rows_fill's rows [frow0, frow1)
-    int grp0 = 0, grp1 = 0, task0 = 0;
-    int64_t frow0 = 0, frow1 = 0;
 };
 
 // The planes this path owns: sparse, not a point plane.
@@ -101,26 +96,26 @@ __device__ __forceinline__ bool band_plane(const BandArgs& a, int p) {
 // so only the coarse lines see all W columns; a group line sees the coarse
 // hull plus the object columns in between (C5: ~10^3 points, not 32768).
 //
-// One warp filters one compact point list in shared memory (column, H = d^2 +
-// k^2 < 2^31) by warp_prune below: rounds of "a point strictly above the chord
+// One CTA filters one compact point list in shared memory (column, H = d^2 +
+// k^2 < 2^31) by cta_prune below: rounds of "a point strictly above the chord
 // of two list neighbours goes", survivors compacted in place.  The result is a
 // superset of the lower hull with collinear points kept (ties), which is all
 // the argument above needs -- a group line's list must CONTAIN the coarse
 // line's hull points, and the candidates must CONTAIN the group line's.
 //   K1a / k_band_objcols  object-column bits per band; k_objcol_runs their
 //                   running ORs over runs of 32 bands
-//   k_hull<0>       warp = (plane, coarse group, side, window of 1024 columns):
+//   k_hull<0>       CTA = (plane, coarse group, side, window of 1024 columns):
 //                   the window's filter over every column with a carry
-//   k_hull<1>       warp = (plane, coarse group, side): the windows' survivors
+//   k_hull<1>       CTA = (plane, coarse group, side): the windows' survivors
 //                   filtered together
-//   k_hull<2>       warp = (plane, group, side): the coarse line's survivors +
+//   k_hull<2>       CTA = (plane, group, side): the coarse line's survivors +
 //                   the object columns in between, filtered at the group's
 //                   line; side 0 also adds the group's own object columns.
 //                   Output: candidate bits [plane][group][side][W/32].
 // A list longer than kHullCap is passed through unfiltered (a superset).
 constexpr int kHullCap = 2048;     // points per warp (k_hull<1>, k_hull<2>)
 constexpr int kHullWinCap = 1024;  // k_hull<0>: a window of 32 words
-constexpr int kHullWarps = 8;
+constexpr int kHullThreads = 256;  // one CTA per line (window)
 constexpr int kCoarseBands = 32;   // bands per coarse group (rounded to a multiple of the group)
 constexpr int kPruneRounds = 10;
 
@@ -179,70 +174,100 @@ __device__ __forceinline__ bool hull_above(int ka, int Ha, int kb, int Hb, int k
 }
 
 // Prune the compact point list c / H [0, n) (ascending columns) towards its
-// lower hull, data-parallel: in every round point i goes if it lies strictly
-// above the chord of its list neighbours i - s and i + s for some stride s =
-// 1, 2, .., 64 (a point above a chord of two points of the set is no hull
-// point, whatever happens to those two), then the survivors are compacted in
-// place.  Any number of rounds leaves a superset of the hull (collinear points
-// kept); on C5's lines 5 rounds reach the hull itself (10^4 -> ~10^2 points,
-// profiles/r02/prune_study.txt).  Lane = point i = 32 t + lane.  Returns the new n.
+// lower hull, data-parallel over the CTA: in every round point i goes if it
+// lies strictly above the chord of its list neighbours i - s and i + s for
+// some stride s = 1, 2, .., 64 (a point above a chord of two points of the set
+// is no hull point, whatever happens to those two), then the survivors are
+// compacted in place (every thread holds its points in registers across the
+// barrier).  Any number of rounds leaves a superset of the hull (collinear
+// points kept); on C5's lines 5 rounds reach the hull itself (10^4 -> ~10^2
+// points, profiles/r02/prune_study.txt).  Thread = points tid + kHullThreads t.
+// Returns the new n (CTA-uniform).
 template <int CAP>
-__device__ __forceinline__ int warp_prune(uint16_t* c, int32_t* H, int n, int lane) {
+__device__ __forceinline__ int cta_prune(uint16_t* c, int32_t* H, int* wsum, int n, int tid) {
     constexpr unsigned FULL = 0xffffffffu;
-    constexpr int NT = CAP / 32;
+    constexpr int NT = CAP / kHullThreads;  // points per thread
+    constexpr int NW = kHullThreads / 32;
+    const int lane = tid & 31, warp = tid >> 5;
     for (int round = 0; round < kPruneRounds && n >= 3; ++round) {
-        uint64_t gone = 0;  // bit t: point 32 t + lane goes
-        for (int t = 0; 32 * t < n; ++t) {
-            const int i = 32 * t + lane;
-            if (i >= n) break;
-            const int ki = c[i], Hi = H[i];
-            bool ab = false;
+        int ki[NT], Hi[NT];
+        uint32_t keep = 0;
 #pragma unroll
-            for (int s = 1; s <= 64; s <<= 1)
-                if (i >= s && i + s < n) ab |= hull_above(c[i - s], H[i - s], ki, Hi, c[i + s], H[i + s]);
-            gone |= (uint64_t)ab << t;
-        }
-        static_assert(NT <= 64, "one bit per chunk");
-        __syncwarp();
-        int m = 0;
-        for (int t = 0; 32 * t < n; ++t) {
-            const int i = 32 * t + lane;
-            const bool keep = i < n && !((gone >> t) & 1);
-            const int ki = i < n ? c[i] : 0, Hi = i < n ? H[i] : 0;
-            __syncwarp();  // the chunk's reads before its writes (positions <= the chunk's)
-            const uint32_t bal = __ballot_sync(FULL, keep);
-            if (keep) {
-                const int pos = m + __popc(bal & ((1u << lane) - 1u));
-                c[pos] = (uint16_t)ki;
-                H[pos] = Hi;
+        for (int t = 0; t < NT; ++t) {
+            const int i = kHullThreads * t + tid;
+            ki[t] = 0;
+            Hi[t] = 0;
+            if (i < n) {
+                ki[t] = c[i];
+                Hi[t] = H[i];
+                bool ab = false;
+#pragma unroll
+                for (int s = 1; s <= 64; s <<= 1)
+                    if (i >= s && i + s < n) ab |= hull_above(c[i - s], H[i - s], ki[t], Hi[t], c[i + s], H[i + s]);
+                keep |= (uint32_t)!ab << t;
             }
-            m += __popc(bal);
         }
-        __syncwarp();
-        if (m == n) break;
-        n = m;
+        // order-preserving positions: counts per (t, warp), t-major
+        uint32_t bal[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            bal[t] = __ballot_sync(FULL, (keep >> t) & 1u);
+            if (lane == 0) wsum[t * NW + warp] = __popc(bal[t]);
+        }
+        __syncthreads();  // every read of this round's list is done; the counts are visible
+        int base[NT], total = 0;
+        {
+            // NT * NW <= 64 counts: every warp scans them with two per lane
+            const int e0 = 2 * lane, e1 = 2 * lane + 1;
+            const int v0 = e0 < NT * NW ? wsum[e0] : 0, v1 = e1 < NT * NW ? wsum[e1] : 0;
+            int incl = v0 + v1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            total = __shfl_sync(FULL, incl, 31);
+            const int ex0 = incl - v0 - v1, ex1 = ex0 + v0;  // exclusive prefixes of entries e0, e1
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int e = t * NW + warp;
+                const int a0 = __shfl_sync(FULL, ex0, e >> 1), a1 = __shfl_sync(FULL, ex1, e >> 1);
+                base[t] = (e & 1) ? a1 : a0;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            if ((keep >> t) & 1u) {
+                const int pos = base[t] + __popc(bal[t] & ((1u << lane) - 1u));
+                c[pos] = (uint16_t)ki[t];
+                H[pos] = Hi[t];
+            }
+        __syncthreads();
+        if (total == n) break;
+        n = total;
     }
     return n;
 }
 
 // MODE 0: window filters of the coarse lines; 1: the coarse lines' filters
-// from their windows' (in place); 2: the group lines' filters.
+// from their windows' (in place); 2: the group lines' filters.  One CTA per
+// line (window).
 template <int MODE>
-__global__ void __launch_bounds__(32 * kHullWarps) k_hull(BandArgs a) {
-    extern __shared__ uint4 hull_raw[];
+__global__ void __launch_bounds__(kHullThreads) k_hull(BandArgs a) {
     constexpr int CAP = MODE == 0 ? kHullWinCap : kHullCap;
-    char* wbase = reinterpret_cast<char*>(hull_raw) + (size_t)(threadIdx.x >> 5) * (CAP * 6);
-    int32_t* const H0 = reinterpret_cast<int32_t*>(wbase);             // [CAP]
-    uint16_t* const c0 = reinterpret_cast<uint16_t*>(wbase + CAP * 4);  // [CAP]
+    constexpr int NW = kHullThreads / 32;
+    __shared__ int32_t H0[CAP];
+    __shared__ uint16_t c0[CAP];
+    __shared__ int wsum[64];
+    __shared__ int wcnt[NW];
     constexpr unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwin = (a.Ww + 31) / 32;
     const int64_t per_plane = MODE == 0 ? (int64_t)a.ncoarse * 2 * nwin : MODE == 1 ? (int64_t)a.ncoarse * 2
                                                                                     : (int64_t)a.ngroups * 2;
-    int64_t task = (int64_t)blockIdx.x * kHullWarps + (threadIdx.x >> 5);
-    if (MODE == 2) task += (int64_t)a.grp0 * 2;
+    const int64_t task = blockIdx.x;
     const int p = (int)(task / per_plane);
-    if (p >= a.nplanes || !band_plane(a, p)) return;  // warp-uniform
+    if (p >= a.nplanes || !band_plane(a, p)) return;  // CTA-uniform
     int t = (int)(task - (int64_t)p * per_plane);
     int win = 0;
     if (MODE == 0) {
@@ -250,7 +275,7 @@ __global__ void __launch_bounds__(32 * kHullWarps) k_hull(BandArgs a) {
         t /= nwin;
     }
     const int side = t & 1, grp = t >> 1;  // coarse group (MODE 0, 1) or group (MODE 2)
-    if (grp >= (MODE == 2 ? a.grp1 : a.ncoarse)) return;
+    if (grp >= (MODE == 2 ? a.ngroups : a.ncoarse)) return;
     const int nb = a.nb;
     const int bper = MODE == 2 ? a.group : a.cbands;
     const int gb0 = grp * bper, gb1 = min(nb - 1, gb0 + bper - 1);
@@ -311,20 +336,19 @@ __global__ void __launch_bounds__(32 * kHullWarps) k_hull(BandArgs a) {
     };
 
     if (MODE == 2 && r1 < r0) {  // the group's line is the coarse line: already filtered
-        for (int w = lane; w < a.Ww; w += 32) out[w] = coarse[w] | base_word(w);
+        for (int w = tid; w < a.Ww; w += kHullThreads) out[w] = coarse[w] | base_word(w);
         return;
     }
-    // ---- gather the points (compact, ascending columns): lane = a run of
-    // consecutive words, 8 words loaded before any is used ----
-    const int per = (w1 - w0 + 31) / 32;                  // words per lane
-    const int lw0 = min(w1, w0 + lane * per), lw1 = min(w1, lw0 + per);
+    // ---- gather the points (compact, ascending columns): thread = a run of
+    // consecutive words, all of them loaded before any is used ----
+    constexpr int PER = MODE == 0 ? 1 : 4;  // words per thread: 32 (a window) or <= 1024 (W <= 32768)
+    const int lw0 = w0 + tid * PER;
+    uint32_t x[PER];
     int cnt = 0;
-    for (int w = lw0; w < lw1; w += 8) {
-        uint32_t x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = w + u < lw1 ? in_word(w + u) : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) cnt += __popc(x[u]);
+    for (int u = 0; u < PER; ++u) {
+        x[u] = lw0 + u < w1 ? in_word(lw0 + u) : 0u;
+        cnt += __popc(x[u]);
     }
     int pre = cnt;
 #pragma unroll
@@ -332,50 +356,54 @@ __global__ void __launch_bounds__(32 * kHullWarps) k_hull(BandArgs a) {
         const int v = __shfl_up_sync(FULL, pre, o);
         if (lane >= o) pre += v;
     }
-    int n = __shfl_sync(FULL, pre, 31);
-    if (n > CAP) {  // too many points for one warp: unfiltered (a superset of the hull)
-        for (int w = w0 + lane; w < w1; w += 32) {
-            const uint32_t x = in_word(w) | base_word(w);
-            out[w] = x;
-        }
+    if (lane == 31) wcnt[warp] = pre;
+    __syncthreads();
+    int pos = pre - cnt, n = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const int v = wcnt[w];
+        if (w < warp) pos += v;
+        n += v;
+    }
+    if (n > CAP) {  // too many points for one CTA: unfiltered (a superset of the hull)
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+            if (lw0 + u < w1) out[lw0 + u] = x[u] | base_word(lw0 + u);
         return;
     }
-    {
-        int pos = pre - cnt;
-        for (int w = lw0; w < lw1; ++w) {
-            uint32_t y = in_word(w);  // L1 / L2 hit
-            while (y) {               // four carries in flight
-                int kk[4], cr[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    kk[u] = y ? 32 * w + __ffs(y) - 1 : -1;
-                    y &= y - 1;
-                }
+    for (int u = 0; u < PER; ++u)
+        for (uint32_t y = x[u]; y; y &= y - 1) c0[pos++] = (uint16_t)(32 * (lw0 + u) + __ffs(y) - 1);
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += 4 * kHullThreads) {  // H = d^2 + k^2, four carries in flight
+        int cr[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) cr[u] = kk[u] >= 0 ? (int)__ldg(car + kk[u]) : 0;
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kHullThreads + tid;
+            cr[u] = i < n ? (int)__ldg(car + c0[i]) : 0;
+        }
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (kk[u] >= 0) {
-                        const int d = side ? cr[u] - line : line - cr[u];  // a listed column has a carry
-                        c0[pos] = (uint16_t)kk[u];
-                        H0[pos] = d * d + kk[u] * kk[u];
-                        ++pos;
-                    }
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kHullThreads + tid;
+            if (i < n) {
+                const int k = c0[i];
+                const int d = side ? cr[u] - line : line - cr[u];  // a listed column has a carry
+                H0[i] = d * d + k * k;
             }
         }
     }
-    __syncwarp();
-    n = warp_prune<CAP>(c0, H0, n, lane);
+    __syncthreads();
+    n = cta_prune<CAP>(c0, H0, wsum, n, tid);
     // ---- the survivors' bits over the base words ----
-    for (int w = w0 + lane; w < w1; w += 32) out[w] = base_word(w);
-    __syncwarp();
-    for (int i = lane; i < n; i += 32) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u)
+        if (lw0 + u < w1) out[lw0 + u] = base_word(lw0 + u);
+    __syncthreads();
+    for (int i = tid; i < n; i += kHullThreads) {
         const int k = c0[i];
         atomicOr(out + (k >> 5), 1u << (k & 31));
     }
 }
-
-inline int hull_smem_bytes(int mode) { return kHullWarps * (mode == 0 ? kHullWinCap : kHullCap) * 6; }
 
 // ------------------------------------------------------------ per-row stacks
 // CTA = (plane, band), kBandWarps warps.  The band's candidates (the group's
@@ -404,16 +432,15 @@ struct BandSmem {
     int n;
 };
 
+// The stacks of band `task` (= plane * nb + band).  Warps leave at different
+// points after the last CTA barrier inside; the caller adds its own barrier
+// before anything that reads the lists.
 template <bool TAKE_NEW>
-__global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
-    extern __shared__ uint4 band_raw[];
-    BandSmem& sm = *reinterpret_cast<BandSmem*>(band_raw);
+__device__ __forceinline__ void band_rows_body(const BandArgs& a, BandSmem& sm, int64_t task) {
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int MASK = kBandCap - 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t task = (int64_t)a.task0 + blockIdx.x;
     const int p = (int)(task / a.nb), b = (int)(task - (int64_t)p * a.nb);
-    if (!band_plane(a, p)) return;  // CTA-uniform
     const int s = p / a.n_img, im = p - s * a.n_img;
     const int pol = a.pol0 + s;
     const int gb = a.band0 + b;  // global band; rows of the image [32 gb, 32 gb + nrows)
@@ -661,6 +688,14 @@ __global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
     a.nent[row * kBandWarps + warp] = ng;
 }
 
+template <bool TAKE_NEW>
+__global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
+    extern __shared__ uint4 band_raw[];
+    const int64_t task = blockIdx.x;
+    if (!band_plane(a, (int)(task / a.nb))) return;  // CTA-uniform
+    band_rows_body<TAKE_NEW>(a, *reinterpret_cast<BandSmem*>(band_raw), task);
+}
+
 inline int band_rows_smem_bytes() { return (int)sizeof(BandSmem); }
 
 // ------------------------------------------------------------------- fill
@@ -669,71 +704,129 @@ struct FillSmem {
     uint16_t r[kFillCap];
 };
 
+// One row of a band-path plane from its per-chunk owner lists (warp = row).
 template <int DONLY>  // lr_fill_row's mode
+__device__ __forceinline__ void band_fill_row(const RowArgs& ra, const BandArgs& a, FillSmem& sm, int64_t row,
+                                              int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int W = a.W;
+    const int p = (int)(row / a.H);
+    const int64_t iR = row - (int64_t)p * a.H;
+    const uint32_t gi = (uint32_t)(iR + 32 * a.band0);  // global row
+    const int* bounds = a.cbound + ((int64_t)p * a.nb + iR / 32) * (kBandWarps + 1);
+    int32_t* Drow = ra.D ? reinterpret_cast<int32_t*>(ra.D + p * ra.sD) + iR * W : nullptr;
+    float* Srow = ra.S ? reinterpret_cast<float*>(ra.S + p * ra.sS) + iR * W : nullptr;
+    int32_t* Lrow = ra.LB ? reinterpret_cast<int32_t*>(ra.LB + p * ra.sL) + iR * W : nullptr;
+    int32_t* Nrow = ra.NC ? reinterpret_cast<int32_t*>(ra.NC + p * ra.sN) + iR * W : nullptr;
+    // one round trip for the row's chunk bounds and list lengths, a second
+    // one for all its lists (staged back to back when they fit together)
+    const int bnd = lane <= kBandWarps ? __ldcg(bounds + lane) : 0;
+    const int bnx = __shfl_down_sync(FULL, bnd, 1);
+    const int ne = (lane < kBandWarps && bnd < bnx) ? __ldcg(a.nent + row * kBandWarps + lane) : 0;
+    int off = ne;  // exclusive prefix over the chunks
+#pragma unroll
+    for (int o = 1; o < kBandWarps; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, off, o);
+        if (lane >= o) off += v;
+    }
+    const int all = __shfl_sync(FULL, off, kBandWarps - 1);
+    off -= ne;
+    const bool staged = all <= kFillCap;
+    __syncwarp();
+    if (staged) {
+#pragma unroll
+        for (int w = 0; w < kBandWarps; ++w) {
+            const int nE = __shfl_sync(FULL, ne, w), o = __shfl_sync(FULL, off, w);
+            const int64_t at = row * a.Ws + __shfl_sync(FULL, bnd, w);
+            for (int q = lane; q < nE; q += 32) {
+                sm.e[o + q] = __ldcg(a.ent + at + q);
+                sm.r[o + q] = __ldcg(a.entr + at + q);
+            }
+        }
+        __syncwarp();
+    }
+    for (int w = 0; w < kBandWarps; ++w) {
+        const int c0 = __shfl_sync(FULL, bnd, w), c1 = __shfl_sync(FULL, bnx, w);
+        if (c0 >= c1) continue;
+        const int nE = __shfl_sync(FULL, ne, w);
+        const uint32_t* gE = a.ent + row * a.Ws + c0;
+        const uint16_t* gR = a.entr + row * a.Ws + c0;
+        if (staged) {
+            const int o = __shfl_sync(FULL, off, w);
+            lr_fill_row<DONLY>(ra, sm.e + o, sm.r + o, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+            continue;
+        }
+        if (nE <= kFillCap) {
+            __syncwarp();
+            for (int q = lane; q < nE; q += 32) {
+                sm.e[q] = __ldcg(gE + q);
+                sm.r[q] = __ldcg(gR + q);
+            }
+            __syncwarp();
+            lr_fill_row<DONLY>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+            continue;
+        }
+        // a long list (dense stretches): 32-column blocks straight from L2
+        int base = 0;
+        for (int b = c0; b < c1; b += 32) {
+            const int idx = base + lane;
+            const uint32_t we = idx < nE ? __ldcg(gE + idx) : FULL;
+            const uint32_t wr = idx < nE ? (uint32_t)__ldcg(gR + idx) : kNoRow;
+            const int s = (int)(we >> 16);
+            const bool in = lane >= 1 && s <= b + 31;
+            const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
+            const int ow = __popc(Z & ((2u << lane) - 1u));
+            const uint32_t ke = __shfl_sync(FULL, we, ow);
+            const uint32_t kr = __shfl_sync(FULL, wr, ow);
+            const int j = b + lane;
+            if (j < c1) {
+                const uint32_t k = ke & 0xffffu;
+                const bool inf = k == kLrInfK;
+                const uint32_t av = gi > kr ? gi - kr : kr - gi;
+                const int dj = j - (int)k;
+                const uint32_t d = inf ? (uint32_t)DFC_INF_I32 : av * av + (uint32_t)(dj * dj);
+                if (Drow) __stcs(Drow + j, (int32_t)d);
+                if (Srow) __stcs(Srow + j, dist_f32(d));
+                if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(kr * (uint32_t)W + k));
+                if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
+            }
+            const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (__ldcg(gE + base + 32) >> 16) : 0xffffu;
+            base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
+                    ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
+        }
+    }
+}
+
+template <int DONLY>
 __global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandArgs a) {
     extern __shared__ uint4 fill_raw[];
     FillSmem& sm = reinterpret_cast<FillSmem*>(fill_raw)[threadIdx.x >> 5];
-    constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int W = a.W;
-    const int64_t total = a.frow1;
+    const int64_t total = (int64_t)a.nplanes * a.H;
     const int64_t nw = (int64_t)gridDim.x * kFillWarps;
-    for (int64_t row = a.frow0 + (int64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5); row < total; row += nw) {
-        const int p = (int)(row / a.H);
-        if (!band_plane(a, p)) continue;  // warp-uniform
-        const int64_t iR = row - (int64_t)p * a.H;
-        const uint32_t gi = (uint32_t)(iR + 32 * a.band0);  // global row
-        const int* bounds = a.cbound + ((int64_t)p * a.nb + iR / 32) * (kBandWarps + 1);
-        int32_t* Drow = ra.D ? reinterpret_cast<int32_t*>(ra.D + p * ra.sD) + iR * W : nullptr;
-        float* Srow = ra.S ? reinterpret_cast<float*>(ra.S + p * ra.sS) + iR * W : nullptr;
-        int32_t* Lrow = ra.LB ? reinterpret_cast<int32_t*>(ra.LB + p * ra.sL) + iR * W : nullptr;
-        int32_t* Nrow = ra.NC ? reinterpret_cast<int32_t*>(ra.NC + p * ra.sN) + iR * W : nullptr;
-        for (int w = 0; w < kBandWarps; ++w) {
-            const int c0 = __ldcg(bounds + w), c1 = __ldcg(bounds + w + 1);
-            if (c0 >= c1) continue;
-            const int nE = __ldcg(a.nent + row * kBandWarps + w);
-            const uint32_t* gE = a.ent + row * a.Ws + c0;
-            const uint16_t* gR = a.entr + row * a.Ws + c0;
-            if (nE <= kFillCap) {
-                __syncwarp();
-                for (int q = lane; q < nE; q += 32) {
-                    sm.e[q] = __ldcg(gE + q);
-                    sm.r[q] = __ldcg(gR + q);
-                }
-                __syncwarp();
-                lr_fill_row<DONLY>(ra, sm.e, sm.r, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
-                continue;
-            }
-            // a long list (dense stretches): 32-column blocks straight from L2
-            int base = 0;
-            for (int b = c0; b < c1; b += 32) {
-                const int idx = base + lane;
-                const uint32_t we = idx < nE ? __ldcg(gE + idx) : FULL;
-                const uint32_t wr = idx < nE ? (uint32_t)__ldcg(gR + idx) : kNoRow;
-                const int s = (int)(we >> 16);
-                const bool in = lane >= 1 && s <= b + 31;
-                const uint32_t Z = __reduce_or_sync(FULL, in ? 1u << (s - b) : 0u);
-                const int ow = __popc(Z & ((2u << lane) - 1u));
-                const uint32_t ke = __shfl_sync(FULL, we, ow);
-                const uint32_t kr = __shfl_sync(FULL, wr, ow);
-                const int j = b + lane;
-                if (j < c1) {
-                    const uint32_t k = ke & 0xffffu;
-                    const bool inf = k == kLrInfK;
-                    const uint32_t av = gi > kr ? gi - kr : kr - gi;
-                    const int dj = j - (int)k;
-                    const uint32_t d = inf ? (uint32_t)DFC_INF_I32 : av * av + (uint32_t)(dj * dj);
-                    if (Drow) __stcs(Drow + j, (int32_t)d);
-                    if (Srow) __stcs(Srow + j, dist_f32(d));
-                    if (Lrow) __stcs(Lrow + j, inf ? -1 : (int32_t)(kr * (uint32_t)W + k));
-                    if (Nrow) __stcs(Nrow + j, inf ? -1 : (int32_t)k);
-                }
-                const uint32_t s32 = (lane == 0 && base + 32 < nE) ? (__ldcg(gE + base + 32) >> 16) : 0xffffu;
-                base += __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 32)) +
-                        ((int)__shfl_sync(FULL, s32, 0) <= b + 32 ? 1 : 0);
-            }
-        }
+    for (int64_t row = (int64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5); row < total; row += nw) {
+        if (!band_plane(a, (int)(row / a.H))) continue;  // warp-uniform
+        band_fill_row<DONLY>(ra, a, sm, row, lane);
     }
+}
+
+// Stacks and fill of one band in one CTA: the band's 8 warps build its rows'
+// lists, then each writes 4 of its 32 rows.  The lists stay in L2; a CTA in
+// its (latency-bound) stack phase shares the SM with CTAs in their (HBM-bound)
+// fill phase, which a separate k_band_rows launch in front of k_rows_fill
+// cannot (C5: 156 + 766 us as two launches).
+template <bool TAKE_NEW, int DONLY>
+__global__ void __launch_bounds__(32 * kBandWarps) k_band_rows_fill(RowArgs ra, BandArgs a) {
+    extern __shared__ uint4 band_raw[];
+    const int64_t task = blockIdx.x;
+    const int p = (int)(task / a.nb), b = (int)(task - (int64_t)p * a.nb);
+    if (!band_plane(a, p)) return;  // CTA-uniform
+    band_rows_body<TAKE_NEW>(a, *reinterpret_cast<BandSmem*>(band_raw), task);
+    __syncthreads();  // the band's lists are written (global) and its shared memory is free
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    FillSmem& fs = reinterpret_cast<FillSmem*>(band_raw)[warp];
+    const int nrows = min(32, a.H - 32 * b);
+    for (int r = warp; r < nrows; r += kBandWarps) band_fill_row<DONLY>(ra, a, fs, (int64_t)p * a.H + 32 * b + r, lane);
 }
 
 inline int fill_smem_bytes() { return kFillWarps * (int)sizeof(FillSmem); }
