@@ -313,6 +313,13 @@ int dfc_set_row_kernel(int mode);
  * Results are identical; a performance/testing knob. */
 int dfc_set_lr_chunk(int cols);
 
+/* Smallest image (rows * cols) whose sparse planes take the band path
+ * (k_rows_band.cu) in the default mode, for calls on the calling thread;
+ * smaller sparse planes use the lane-per-row kernel.  0 = every size, negative
+ * = the default (DFC_BAND_MIN_PX, else 2^24 + 1).  A performance / testing
+ * knob: results are identical. */
+int dfc_set_band_min_pixels(int64_t pixels);
+
 /* Number of kernels the last successful call on this thread enqueued. */
 int dfc_last_launch_count(void);
 /* Debug: with DFC_DEBUG_GUARD=1 in the environment every scratch allocation

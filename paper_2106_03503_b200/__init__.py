@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 
 import torch
 
@@ -53,6 +54,7 @@ _lib.dfc_set_profile_events.argtypes = [_vp, _vp, _vp]
 _lib.dfc_sqrt_i32.argtypes = [_vp, _vp, _i64, _vp]
 _lib.dfc_set_row_kernel.argtypes = [C.c_int]
 _lib.dfc_set_lr_chunk.argtypes = [C.c_int]
+_lib.dfc_set_band_min_pixels.argtypes = [_i64]
 _lib.dfc_column_nr_u8.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _i64, _vp]
 _lib.dfc_rows_from_nr_u16.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp, _vp]
 _lib.dfc_envelope_vdist_u16.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
@@ -88,6 +90,7 @@ EXPORTED_SYMBOLS = (
     "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
     "dfc_edt_u8_sharded", "dfc_shard_cols", "dfc_shard_rows", "dfc_comm_unique_id", "dfc_comm_init_rank",
     "dfc_comm_init_all", "dfc_comm_destroy", "dfc_last_nccl_error", "dfc_row_owners_i64", "dfc_raster_pass_u64",
+    "dfc_set_band_min_pixels", "dfc_debug_guard_violations",
 )
 
 
@@ -102,7 +105,17 @@ class DfcError(RuntimeError):
         self.status = status
 
 
+_tls = threading.local()
+
+
 def _check(status: int) -> None:
+    # a launch on a side stream (see _stream): the current stream, on which this
+    # layer allocates outputs and temporaries, waits for it, so the caching
+    # allocator cannot hand their memory out again while the kernels still run
+    side = getattr(_tls, "side", None)
+    if side is not None:
+        _tls.side = None
+        side[1].wait_stream(side[0])
     if status != 0:
         raise DfcError(status)
 
@@ -121,6 +134,12 @@ def set_profile_events(col_begin=None, row_begin=None, row_end=None) -> None:
 def set_lr_chunk(cols: int) -> None:
     """Columns per warp chunk of the "lr" row kernel (multiple of 32; 0 = default)."""
     _check(_lib.dfc_set_lr_chunk(int(cols)))
+
+
+def set_band_min_pixels(pixels: int) -> None:
+    """Smallest image whose sparse planes take the band path (0: every size,
+    negative: the library default, 2**24 + 1); see dfc_set_band_min_pixels."""
+    _check(_lib.dfc_set_band_min_pixels(int(pixels)))
 
 
 def set_row_kernel(mode: str) -> None:
@@ -143,8 +162,16 @@ def _ptr(t):
 
 
 def _stream(stream):
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+    """The launch stream's handle.  A side stream first waits for the current
+    stream (inputs, outputs and temporaries are produced / allocated there);
+    _check() then makes the current stream wait for the launch."""
+    cur = torch.cuda.current_stream()
+    if stream is None or stream == cur:
+        _tls.side = None
+        return C.c_void_p(cur.cuda_stream)
+    stream.wait_stream(cur)
+    _tls.side = (stream, cur)
+    return C.c_void_p(stream.cuda_stream)
 
 
 def _img2d(img: torch.Tensor):
@@ -409,8 +436,8 @@ def label_ordinals(img: torch.Tensor, label: torch.Tensor, stream=None) -> torch
     (grid.cpp:29-36); int64 tensor holding uint32 values (2**32-1 = none)."""
     img, h, w, pitch = _img2d(img)
     out = _empty((h, w), torch.int32, img)
-    _check(_lib.dfc_label_ordinals(_ptr(img), h, w, pitch, _ptr(label.contiguous()), _ptr(out),
-                                   _stream(stream)))
+    lab = label.contiguous()  # kept alive until the launch is ordered (see _check)
+    _check(_lib.dfc_label_ordinals(_ptr(img), h, w, pitch, _ptr(lab), _ptr(out), _stream(stream)))
     return out.to(torch.int64) & 0xFFFFFFFF
 
 

@@ -150,7 +150,7 @@ DistanceMap vertical_pass(const BinaryImage& img, unsigned) {
     dfc_check(dfc_vertical_u8(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
                               dv.get(), stream()),
               "vertical_pass");
-    return detail::to_distance_map(dv.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean);
+    return detail::to_distance_map(dv, img.rows(), img.cols(), DistanceKind::squared_euclidean);
 }
 
 MeijsterResult meijster_scan(const DistanceMap& vert, ScanStats* stats, unsigned) {
@@ -199,7 +199,7 @@ DistanceMap edt(const BinaryImage& img, EdtAlgorithm, Orientation, ScanStats* st
                          DFC_BG_TO_OBJ, dd.get(), nullptr, nullptr, nullptr, stream()),
               "edt");
     if (stats) stats->candidates += img.rows() * img.cols();
-    return detail::to_distance_map(dd.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean);
+    return detail::to_distance_map(dd, img.rows(), img.cols(), DistanceKind::squared_euclidean);
 }
 
 std::pair<DistanceMap, DistanceMap> edt_both_polarities(const BinaryImage& img) {
@@ -209,8 +209,8 @@ std::pair<DistanceMap, DistanceMap> edt_both_polarities(const BinaryImage& img) 
     dfc_check(dfc_edt_u8_dual(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
                               d0.get(), nullptr, d1.get(), nullptr, stream()),
               "edt_both_polarities");
-    return {detail::to_distance_map(d0.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean),
-            detail::to_distance_map(d1.download(), img.rows(), img.cols(), DistanceKind::squared_euclidean)};
+    return {detail::to_distance_map(d0, img.rows(), img.cols(), DistanceKind::squared_euclidean),
+            detail::to_distance_map(d1, img.rows(), img.cols(), DistanceKind::squared_euclidean)};
 }
 
 std::vector<float> edt_distances(const BinaryImage& img) {

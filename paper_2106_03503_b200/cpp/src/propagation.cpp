@@ -19,7 +19,7 @@ DistanceMap raster(const BinaryImage& img, DistanceKind kind) {
     detail::dfc_check(dfc_raster_u8(dimg.get(), (int64_t)img.rows(), (int64_t)img.cols(), (int64_t)img.pitch(),
                                     city, chess, cham, detail::stream()),
                       "raster transform");
-    return detail::to_distance_map(d.download(), img.rows(), img.cols(), kind);
+    return detail::to_distance_map(d, img.rows(), img.cols(), kind);
 }
 
 // one pass of dfc_raster_pass_u64 over the caller's map, in place

@@ -2,6 +2,8 @@
 // tests/test_dropin.py:  dropin_cli <op> <rows> <cols> <in.u8> <out.bin> [arg]
 // Writes the reference-typed result (uint64 maps, uint32 labels/columns, or
 // int64 ks/js) as raw little-endian; on an exception prints its type and exits 3.
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -44,7 +46,21 @@ int main(int argc, char** argv) {
                 if (buf[p]) img.set_object(p / cols, p % cols);
         }
         std::ofstream out(argv[5], std::ios::binary);
-        if (op == "edt") {
+        if (op == "time_edt") {  // arg: repetitions; host BinaryImage in -> host DistanceMap out, per call
+            const int reps = argc > 6 ? std::stoi(argv[6]) : 20;
+            std::vector<double> ms;
+            std::uint64_t sink = 0;
+            for (int r = 0; r < reps + 3; ++r) {
+                const auto t0 = std::chrono::steady_clock::now();
+                const DistanceMap dm = edt(img, EdtAlgorithm::envelope);
+                const auto t1 = std::chrono::steady_clock::now();
+                sink += dm(rows - 1, cols - 1);
+                if (r >= 3) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+            }
+            std::sort(ms.begin(), ms.end());
+            out << "median_ms " << ms[ms.size() / 2] << " min_ms " << ms.front() << " reps " << reps << " sink " << sink
+                << "\n";
+        } else if (op == "edt") {
             ScanStats st;
             put_map(out, edt(img, EdtAlgorithm::envelope, Orientation::automatic, &st, 4));
         } else if (op == "edt_simple") {

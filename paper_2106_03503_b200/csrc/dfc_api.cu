@@ -19,6 +19,7 @@ thread_local int g_last_cuda = 0;
 thread_local int g_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
 thread_local int g_lr_chunk = 0;  // k_rows_lr columns per warp chunk (0: default)
+thread_local int64_t g_band_min_px = -1;  // smallest image the band path takes (-1: default)
 thread_local int g_row_mode = 0;  // 0: default, 1: segment/merge kernel, 4: dense rows first, the
                                   // rest by the segment kernel, 5: lane-per-row, 6: anchored (default)
 
@@ -268,6 +269,19 @@ int band_group() {
         return x >= 1 && x <= 64 ? x : 4;
     }();
     return g;
+}
+
+// The band path (six launches, ~60 us of latency-bound stages even when every
+// CTA exits at once) is only offered images above this size: DFC_BAND_MIN_PX
+// (tuning) or dfc_set_band_min_pixels, default 2^24 + 1 -- larger than 4096^2.
+// Smaller sparse planes keep the lane-per-row kernel (k_rows_lr).
+int64_t band_min_px() {
+    static const int64_t env = [] {
+        const char* v = getenv("DFC_BAND_MIN_PX");
+        return v ? (int64_t)strtoll(v, nullptr, 10) : (int64_t)-1;
+    }();
+    if (g_band_min_px >= 0) return g_band_min_px;
+    return env >= 0 ? env : ((int64_t)1 << 24) + 1;
 }
 
 // DFC_SPARSE=lr keeps the lane-per-row chunk scan (k_rows_lr, from the
@@ -702,7 +716,7 @@ int edt_core(const uint8_t* img, int64_t n, int64_t H, int64_t W, int64_t pitch,
     // from them instead of re-reading the image (C5: 1 B/px of reads less)
     const bool masks_on = n == 1;
     // sparse planes of single images: the band path (k_rows_band.cu), no plane
-    const bool sparse_band = mode == 6 && masks_on && band_sparse_on();
+    const bool sparse_band = mode == 6 && masks_on && band_sparse_on() && H * W >= band_min_px();
     const size_t bmask_elems = masks_on ? (size_t)(n * nb * Wp) : 0;
     Scratch sc(st);
     cudaError_t e = sc.alloc((2 * carry_elems + nr_elems) * sizeof(uint16_t) + 512 + (size_t)planes * 8 +
@@ -1184,6 +1198,11 @@ int dfc_set_row_kernel(int mode) {
 int dfc_set_lr_chunk(int cols) {
     if (cols < 0 || cols % 32 != 0 || cols > 65536) return DFC_ERR_ARG;
     g_lr_chunk = cols;
+    return DFC_OK;
+}
+
+int dfc_set_band_min_pixels(int64_t pixels) {
+    g_band_min_px = pixels < 0 ? -1 : pixels;
     return DFC_OK;
 }
 

@@ -11,7 +11,7 @@ LIB = os.path.join(ROOT, "paper_2106_03503_b200", "lib")
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "distfield_cuda.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|size_t)\s+(dfc_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*|size_t)\s+(dfc_\w+)\s*\(", src, re.M)))
 
 
 def _exported(path):

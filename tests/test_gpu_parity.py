@@ -20,8 +20,14 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 @pytest.fixture(scope="module")
 def dfc():
+    """The device layer with the band path open to every image size, so that
+    the small sparse cases below run through it (the library default only
+    offers it images above 4096^2; test_small_sparse_default_dispatch covers
+    that default)."""
     import paper_2106_03503_b200 as m
-    return m
+    m.set_band_min_pixels(0)
+    yield m
+    m.set_band_min_pixels(-1)
 
 
 def _dev(img):
@@ -757,3 +763,19 @@ def test_raster_passes_compose_to_the_transforms(dfc):
         torch.cuda.synchronize()
         want = oracle.cityblock(img) if kind == "cityblock" else oracle.chamfer34(img)
         np.testing.assert_array_equal(g.cpu().numpy().view(np.uint64), want)
+
+
+def test_small_sparse_default_dispatch(dfc):
+    """The library default: a sparse plane of a small image goes to the
+    lane-per-row kernel (the band path is only offered images above 4096^2)."""
+    dfc.set_band_min_pixels(-1)
+    try:
+        rng = np.random.default_rng(17)
+        for shape in ((300, 2000), (1000, 96), (64, 64)):
+            img = np.zeros(shape, np.uint8)
+            for _ in range(7):
+                img[rng.integers(shape[0]), rng.integers(shape[1])] = 1
+            _check_edt(dfc, img)
+            _check_edt(dfc, img, polarity=1)
+    finally:
+        dfc.set_band_min_pixels(0)

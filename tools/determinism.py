@@ -38,6 +38,7 @@ def repeat(name, fn, check=None):
 
 
 def main():
+    dfc.set_band_min_pixels(0)  # the band path for the small sparse case too
     cases = {
         "anc 1500x2000 p=0.01": workloads.bernoulli(1500, 2000, 0.01, 5),
         "anc discs 2048^2": workloads.discs(2048, 2048, 60, 9),
