@@ -363,7 +363,7 @@ int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cud
             const int x = v ? atoi(v) : 0;
             return x >= 1 && x <= 4 ? x : 4;
         }();
-        const int rsm_occ = std::max(rsm, std::min(227 * 1024, (228 * 1024) / occ - 1024 - 1024) / 16 * 16);
+        const int rsm_occ = std::max(band_fused_smem_bytes(), std::min(227 * 1024, (228 * 1024) / occ - 1024 - 1024) / 16 * 16);
         const int rsm = rsm_occ;
         if (take_new)
             e = donly == 1 ? launch_rows_fill<true, 1>(a, ba, g, rsm, st)

@@ -810,23 +810,137 @@ __global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandA
     }
 }
 
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) with an mbarrier per buffer ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra DONE_%=;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// global -> shared, 16-byte aligned both sides, bytes a multiple of 16; completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // Stacks and fill of one band in one CTA: the band's 8 warps build its rows'
 // lists, then each writes 4 of its 32 rows.  The lists stay in L2; a CTA in
 // its (latency-bound) stack phase shares the SM with CTAs in their (HBM-bound)
 // fill phase, which a separate k_band_rows launch in front of k_rows_fill
-// cannot (C5: 156 + 766 us as two launches).
+// cannot (C5: 156 + 766 us as two launches).  Fill phase per warp: the band's
+// chunk bounds and the list lengths of its 4 rows in one round trip, then the
+// rows' lists by TMA bulk copies into two buffers (row k + 2 is in flight while
+// row k is written): no load latency between the rows' store streams.
+struct FusedFill {
+    uint32_t e[2][kFillCap];
+    uint16_t r[2][kFillCap];
+};
+
 template <bool TAKE_NEW, int DONLY>
-__global__ void __launch_bounds__(32 * kBandWarps) k_band_rows_fill(RowArgs ra, BandArgs a) {
+__global__ void __launch_bounds__(32 * kBandWarps, 4) k_band_rows_fill(RowArgs ra, BandArgs a) {
     extern __shared__ uint4 band_raw[];
+    constexpr unsigned FULL = 0xffffffffu;
     const int64_t task = blockIdx.x;
     const int p = (int)(task / a.nb), b = (int)(task - (int64_t)p * a.nb);
     if (!band_plane(a, p)) return;  // CTA-uniform
     band_rows_body<TAKE_NEW>(a, *reinterpret_cast<BandSmem*>(band_raw), task);
     __syncthreads();  // the band's lists are written (global) and its shared memory is free
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    FillSmem& fs = reinterpret_cast<FillSmem*>(band_raw)[warp];
+    FusedFill& fs = reinterpret_cast<FusedFill*>(band_raw)[warp];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<FusedFill*>(band_raw) + kBandWarps) + 2 * warp;
     const int nrows = min(32, a.H - 32 * b);
-    for (int r = warp; r < nrows; r += kBandWarps) band_fill_row<DONLY>(ra, a, fs, (int64_t)p * a.H + 32 * b + r, lane);
+    const int nk = warp < nrows ? (nrows - warp + kBandWarps - 1) / kBandWarps : 0;  // this warp's rows (<= 4)
+    static_assert(kBandWarps == 8, "lane = 8 * (row slot) + chunk");
+    if (nk == 0) return;
+    if (lane == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
+    }
+    __syncwarp();
+    const int64_t row0 = (int64_t)p * a.H + 32 * b + warp;  // rows row0 + 8 k
+    const int* bounds = a.cbound + task * (kBandWarps + 1);
+    const int bnd = lane <= kBandWarps ? __ldcg(bounds + lane) : 0;
+    const int bnx = __shfl_down_sync(FULL, bnd, 1);
+    // lane 8 k + w: row slot k, chunk w
+    const int myk = lane >> 3, myw = lane & 7;
+    const int wc0 = __shfl_sync(FULL, bnd, myw), wc1 = __shfl_sync(FULL, bnx, myw);
+    const int ne = (myk < nk && wc0 < wc1) ? __ldcg(a.nent + (row0 + 8 * myk) * kBandWarps + myw) : 0;
+    // staged offsets inside the row's buffer: multiples of 8 entries (16-byte aligned for both arrays)
+    const int ne8 = (ne + 7) & ~7;
+    int off = ne8;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, off, o, 8);
+        if (myw >= o) off += v;
+    }
+    const int tot = __shfl_sync(FULL, off, (lane & ~7) | 7);  // the row slot's total
+    off -= ne8;
+    if (__any_sync(FULL, tot > kFillCap)) {  // a row's lists do not fit a buffer: the synchronous path
+        for (int k = 0; k < nk; ++k)
+            band_fill_row<DONLY>(ra, a, *reinterpret_cast<FillSmem*>(&fs), row0 + 8 * k, lane);
+        return;
+    }
+    auto issue = [&](int k, int buf) {  // row slot k's lists -> buffer buf
+        const int t = __shfl_sync(FULL, tot, 8 * k);
+        if (lane == 0) mbar_expect_tx(bars + buf, (uint32_t)t * 6u);
+        __syncwarp();
+        if (myk == k && ne > 0) {
+            const int64_t at = (row0 + 8 * k) * a.Ws + wc0;
+            bulk_g2s(fs.e[buf] + off, a.ent + at, (uint32_t)ne8 * 4u, bars + buf);
+            bulk_g2s(fs.r[buf] + off, a.entr + at, (uint32_t)ne8 * 2u, bars + buf);
+        }
+    };
+    issue(0, 0);
+    if (nk > 1) issue(1, 1);
+    int32_t* const Dp = ra.D ? reinterpret_cast<int32_t*>(ra.D + p * ra.sD) : nullptr;
+    float* const Sp = ra.S ? reinterpret_cast<float*>(ra.S + p * ra.sS) : nullptr;
+    int32_t* const Lp = ra.LB ? reinterpret_cast<int32_t*>(ra.LB + p * ra.sL) : nullptr;
+    int32_t* const Np = ra.NC ? reinterpret_cast<int32_t*>(ra.NC + p * ra.sN) : nullptr;
+    int waits[2] = {0, 0};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k >= nk) break;
+        const int buf = k & 1;
+        const int64_t row = row0 + 8 * k;
+        {
+            mbar_wait(bars + buf, (uint32_t)(waits[buf]++ & 1));  // the buffer's n-th armed use: phase parity n & 1
+            const int64_t iR = row - (int64_t)p * a.H;
+            const uint32_t gi = (uint32_t)(iR + 32 * a.band0);
+            int32_t* Drow = Dp ? Dp + iR * a.W : nullptr;
+            float* Srow = Sp ? Sp + iR * a.W : nullptr;
+            int32_t* Lrow = Lp ? Lp + iR * a.W : nullptr;
+            int32_t* Nrow = Np ? Np + iR * a.W : nullptr;
+            for (int w = 0; w < kBandWarps; ++w) {
+                const int c0 = __shfl_sync(FULL, bnd, w), c1 = __shfl_sync(FULL, bnx, w);
+                if (c0 >= c1) continue;
+                const int nE = __shfl_sync(FULL, ne, 8 * k + w), o = __shfl_sync(FULL, off, 8 * k + w);
+                lr_fill_row<DONLY>(ra, fs.e[buf] + o, fs.r[buf] + o, nE, gi, Drow, Srow, Lrow, Nrow, c0, c1, lane);
+            }
+        }
+        __syncwarp();  // the buffer's readers are done
+        if (k + 2 < nk) issue(k + 2, buf);
+    }
+}
+
+inline int band_fused_smem_bytes() {
+    return std::max((int)sizeof(BandSmem), kBandWarps * ((int)sizeof(FusedFill) + 16));
 }
 
 inline int fill_smem_bytes() { return kFillWarps * (int)sizeof(FillSmem); }
