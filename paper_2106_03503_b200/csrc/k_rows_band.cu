@@ -816,6 +816,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// generic-proxy accesses of shared memory before this point are ordered before
+// later async-proxy (bulk copy) accesses of it
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -869,6 +875,7 @@ __global__ void __launch_bounds__(32 * kBandWarps, 4) k_band_rows_fill(RowArgs r
     const int nk = warp < nrows ? (nrows - warp + kBandWarps - 1) / kBandWarps : 0;  // this warp's rows (<= 4)
     static_assert(kBandWarps == 8, "lane = 8 * (row slot) + chunk");
     if (nk == 0) return;
+    fence_proxy_async();  // this memory held the stack phase's lists (generic stores)
     if (lane == 0) {
         mbar_init(bars, 1);
         mbar_init(bars + 1, 1);
