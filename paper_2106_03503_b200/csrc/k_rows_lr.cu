@@ -42,6 +42,8 @@
 //
 // tests/lr_model.py is the statement-level model (fuzzed against brute force
 // for both tie rules, chunk widths 1..40).
+#include <type_traits>
+
 #include "dfc_kernels.cuh"
 
 namespace dfc {
@@ -124,22 +126,29 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
             constexpr int kH = 4;
             const int s31 = __shfl_sync(FULL, s, 31);
             if (s31 > b + 128 * kH) {  // the window holds every start up to b + 512
-                int cnt[kH + 1];
-                cnt[0] = 0;
-#pragma unroll
-                for (int h = 1; h <= kH; ++h) cnt[h] = __popc(__ballot_sync(FULL, lane >= 1 && s <= b + 128 * h));
+                // cnt[h] = entries (lanes >= 1) starting at or before b + 128 h: an entry
+                // counts from sub-block ceil((s - b) / 128) on; one REDUX.ADD of a byte
+                // per sub-block, prefix sums by a multiply (at most 31 entries: no carries)
+                const int cf = (s - b + 127) >> 7;  // >= 1 for lanes >= 1 (they start after b)
+                const uint32_t byt = __reduce_add_sync(FULL, (lane >= 1 && cf <= kH) ? 1u << (8 * (cf - 1)) : 0u);
+                const uint32_t pre = byt * 0x01010101u;
+                const int cnt[kH + 1] = {0, (int)(pre & 0xffu), (int)((pre >> 8) & 0xffu), (int)((pre >> 16) & 0xffu),
+                                         (int)(pre >> 24)};
                 const bool fast = vec4 && b + 128 * kH <= c1;
-                if (__shfl_sync(FULL, wk, 0) == kLrInfK) {  // featureless row: its only entry
+                const int j0 = b + 4 * lane;
+                auto block = [&](auto FAST) {
+                    constexpr bool kFast = decltype(FAST)::value;
+                    if (__shfl_sync(FULL, wk, 0) == kLrInfK) {  // featureless row: its only entry
 #pragma unroll
-                    for (int h = 0; h < kH; ++h) {
-                        const int j = b + 128 * h + 4 * lane;
-                        const uint32_t di = (uint32_t)DFC_INF_I32;
-                        put4(j, fast, di, di, di, di);
+                        for (int h = 0; h < kH; ++h) {
+                            const uint32_t di = (uint32_t)DFC_INF_I32;
+                            put4(j0 + 128 * h, kFast, di, di, di, di);
+                        }
+                        return;
                     }
-                } else {
 #pragma unroll
                     for (int h = 0; h < kH; ++h) {
-                        const int j = b + 128 * h + 4 * lane;
+                        const int j = j0 + 128 * h;
                         uint32_t d0, d1, d2, d3;
                         {
                             const uint32_t ge = __shfl_sync(FULL, wg, cnt[h]);
@@ -161,9 +170,13 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
                             d2 = min(d2, v2);
                             d3 = min(d3, v3);
                         }
-                        put4(j, fast, d0, d1, d2, d3);
+                        put4(j, kFast, d0, d1, d2, d3);
                     }
-                }
+                };
+                if (fast)
+                    block(std::true_type{});
+                else
+                    block(std::false_type{});
                 base += cnt[kH];  // the last entry starting at or before b + 512
                 b += 128 * kH;
                 continue;
