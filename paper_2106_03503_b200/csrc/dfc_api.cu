@@ -294,6 +294,63 @@ bool band_sparse_on() {
     return on;
 }
 
+// Per-device helper stream of the default row pass: when the band path is on,
+// the kernel families of the planes it does NOT take (point planes, the rows of
+// non-sparse planes) are enqueued on it, beside the band path on the caller's
+// stream -- for a sparse image those launches find no plane of theirs, and
+// their launch latencies no longer sit in front of the band path (C5: ~25 us).
+// Fork / join by events only: no host synchronisation, legal under stream
+// capture.  The mutex serialises the host-side enqueue per device (the events
+// are shared).  DFC_AUX_STREAM=0 keeps everything on the caller's stream.
+struct AuxPipe {
+    std::mutex mu;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    bool ok = false;
+};
+AuxPipe* aux_pipe() {
+    static const bool on = [] {
+        const char* v = getenv("DFC_AUX_STREAM");
+        return !(v && v[0] == '0');
+    }();
+    if (!on) return nullptr;
+    constexpr int kMaxDev = 64;
+    static AuxPipe pipes[kMaxDev];
+    static std::once_flag flags[kMaxDev];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    AuxPipe* ap = &pipes[dev];
+    std::call_once(flags[dev], [ap] {
+        bool ok = cudaStreamCreateWithFlags(&ap->aux, cudaStreamNonBlocking) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&ap->fork, cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&ap->join, cudaEventDisableTiming) == cudaSuccess;
+        ap->ok = ok;
+        if (!ok) cudaGetLastError();
+    });
+    return ap->ok ? ap : nullptr;
+}
+// fork at construction, join (the caller's stream waits for the helper) at scope exit
+struct AuxScope {
+    AuxPipe* ap;
+    cudaStream_t st;
+    std::unique_lock<std::mutex> lock;
+    AuxScope(AuxPipe* p, cudaStream_t s) : ap(p), st(s) {
+        if (!ap) return;
+        lock = std::unique_lock<std::mutex>(ap->mu);
+        if (cudaEventRecord(ap->fork, st) != cudaSuccess || cudaStreamWaitEvent(ap->aux, ap->fork, 0) != cudaSuccess) {
+            cudaGetLastError();
+            lock.unlock();
+            ap = nullptr;
+        }
+    }
+    cudaStream_t stream() const { return ap ? ap->aux : st; }
+    ~AuxScope() {
+        if (!ap) return;
+        cudaEventRecord(ap->join, ap->aux);
+        cudaStreamWaitEvent(st, ap->join, 0);
+    }
+};
+
 // k_rows_fill CTAs per SM (DFC_FILL_CTAS, tuning) of the unfused launch.
 int fill_ctas() {
     static const int n = [] {
@@ -557,11 +614,15 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         if (e != cudaSuccess) return cuda_fail(e);
         a.lr_gate = lr_on;
         a.pts_gate = pts != nullptr && plane_counts != nullptr && H % 32 == 0;
+        // the families beside the band path go to the helper stream (joined at scope exit,
+        // before `fl` is released)
+        AuxScope aux(band_on ? aux_pipe() : nullptr, st);
+        const cudaStream_t os = aux.stream();
         if (a.pts_gate) {  // point planes: from K1a's object list, no nearest-row plane
             const void* pfn = take_new ? pts_kernel_ptr<true>() : pts_kernel_ptr<false>();
             const int64_t pblocks = ((a.total_rows + 31) / 32 + kPtsWarps - 1) / kPtsWarps;
             void* pargs[] = {&a, &pts};
-            e = cudaLaunchKernel(pfn, dim3((unsigned)pblocks), dim3(32 * kPtsWarps), pargs, 0, st);
+            e = cudaLaunchKernel(pfn, dim3((unsigned)pblocks), dim3(32 * kPtsWarps), pargs, 0, os);
             if (e != cudaSuccess) return cuda_fail(e);
             ++g_launches;
         }
@@ -573,7 +634,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             if (e != cudaSuccess) return cuda_fail(e);
             const int64_t dblocks = std::min<int64_t>((a.total_rows + kDenseWarps - 1) / kDenseWarps, 148 * 16);
             void* dargs[] = {&a};
-            e = cudaLaunchKernel(dfn, dim3((unsigned)dblocks), dim3(32 * kDenseWarps), dargs, (size_t)dsm, st);
+            e = cudaLaunchKernel(dfn, dim3((unsigned)dblocks), dim3(32 * kDenseWarps), dargs, (size_t)dsm, os);
             if (e != cudaSuccess) return cuda_fail(e);
             ++g_launches;
         }
@@ -632,7 +693,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
                 // many rows, some owned by other kernels (C3: every plane a point
                 // plane): a compact list first, so that skipped rows cost nothing
                 const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
-                k_rows_rest<<<(unsigned)rblocks, 256, 0, st>>>(a.row_done, plane_counts, a.total_rows, (int)H,
+                k_rows_rest<<<(unsigned)rblocks, 256, 0, os>>>(a.row_done, plane_counts, a.total_rows, (int)H,
                                                                (int)W, a.lr_gate, a.pts_gate, rest_rows, rest_count);
                 ++g_launches;
                 aa.row_list = rest_rows;
@@ -649,7 +710,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             const int64_t ablocks =
                 (anc_cap <= 0 && !aa.row_list) ? a.total_rows : std::min<int64_t>(a.total_rows, 148 * (anc_cap > 0 ? anc_cap : 16));
             void* aargs[] = {&aa};
-            e = cudaLaunchKernel(afn, dim3((unsigned)ablocks), dim3(32 * kAncWarps), aargs, (size_t)asm_bytes, st);
+            e = cudaLaunchKernel(afn, dim3((unsigned)ablocks), dim3(32 * kAncWarps), aargs, (size_t)asm_bytes, os);
             if (e != cudaSuccess) return cuda_fail(e);
             ++g_launches;
             return DFC_OK;
@@ -659,13 +720,13 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         // list first, so that skipped rows cost no CTA launch
         if (a.total_rows <= 16384) {
             void* args[] = {&a};
-            e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+            e = cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, os);
             if (e != cudaSuccess) return cuda_fail(e);
             ++g_launches;
             return DFC_OK;
         }
         const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
-        k_rows_rest<<<(unsigned)rblocks, 256, 0, st>>>(a.row_done, plane_counts, a.total_rows, (int)H, (int)W,
+        k_rows_rest<<<(unsigned)rblocks, 256, 0, os>>>(a.row_done, plane_counts, a.total_rows, (int)H, (int)W,
                                                        a.lr_gate, a.pts_gate, rest_rows, rest_count);
         ++g_launches;
         RowArgs ra = a;
@@ -674,7 +735,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         ra.row_done = nullptr;
         void* args[] = {&ra};
         const int64_t sblocks = std::min<int64_t>(blocks, 148 * 8);  // grid-stride over the list (often empty)
-        e = cudaLaunchKernel(fn, dim3((unsigned)sblocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, st);
+        e = cudaLaunchKernel(fn, dim3((unsigned)sblocks), dim3(g.R * g.T), args, (size_t)g.smem_bytes, os);
         if (e != cudaSuccess) return cuda_fail(e);
         ++g_launches;
         return DFC_OK;
