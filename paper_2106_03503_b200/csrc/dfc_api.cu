@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 
 #include "dfc_kernels.cuh"
 
@@ -102,6 +103,24 @@ __global__ void k_guard_check(const uint8_t* lo, const uint8_t* hi, size_t n) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
         bad += (lo[i] != 0xA5) + (hi[i] != 0xA5);
     if (bad) atomicAdd(&g_guard_bad, (unsigned long long)bad);
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize, raised once per (device,
+// kernel) instead of on every call (the attribute is per context; a call only
+// needs it to be at least its own request).
+cudaError_t set_dyn_smem(const void* fn, int bytes) {
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cur[kMaxDev];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev)
+        return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    std::lock_guard<std::mutex> lock(mu);
+    int& have = cur[dev][fn];
+    if (bytes <= have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
 }
 
 struct Scratch {
@@ -373,7 +392,7 @@ bool band_fused() {
 
 template <bool TN, int DO>
 cudaError_t launch_rows_fill(const RowArgs& a, const BandArgs& ba, unsigned grid, int smem, cudaStream_t st) {
-    cudaError_t e = cudaFuncSetAttribute(k_band_rows_fill<TN, DO>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = set_dyn_smem((const void*)(k_band_rows_fill<TN, DO>), smem);
     if (e != cudaSuccess) return e;
     k_band_rows_fill<TN, DO><<<grid, 32 * kBandWarps, smem, st>>>(a, ba);
     return cudaSuccess;
@@ -433,12 +452,12 @@ int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cud
         return DFC_OK;
     }
     const void* rfn = take_new ? (const void*)k_band_rows<true> : (const void*)k_band_rows<false>;
-    e = cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, rsm);
+    e = set_dyn_smem((const void*)(rfn), rsm);
     if (e != cudaSuccess) return cuda_fail(e);
     const void* ffn = donly == 1 ? (const void*)k_rows_fill<1> : donly == 2 ? (const void*)k_rows_fill<2>
                                                                             : (const void*)k_rows_fill<0>;
     const int fsm = fill_smem_bytes();
-    e = cudaFuncSetAttribute(ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
+    e = set_dyn_smem((const void*)(ffn), fsm);
     if (e != cudaSuccess) return cuda_fail(e);
     if (take_new)
         k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(ba);
@@ -505,7 +524,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     const int64_t blocks = (a.total_rows + g.R - 1) / g.R;
     if (blocks > 0x7fffffff) return DFC_ERR_SHAPE;
     const void* fn = take_new ? rows_kernel_ptr<true>(g.L) : rows_kernel_ptr<false>(g.L);
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes);
+    cudaError_t e = set_dyn_smem((const void*)(fn), g.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e);
 
     // Lane-per-row chunk scan (k_rows_lr.cu): needs 16-byte nr loads.
@@ -538,7 +557,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         uint16_t* entr = reinterpret_cast<uint16_t*>(static_cast<char*>(scratch) + ent_bytes);
         const void* lfn = take_new ? lr_kernel_ptr<true>() : lr_kernel_ptr<false>();
         const int lsm = lr_smem_bytes();
-        cudaError_t le = cudaFuncSetAttribute(lfn, cudaFuncAttributeMaxDynamicSharedMemorySize, lsm);
+        cudaError_t le = set_dyn_smem((const void*)(lfn), lsm);
         if (le != cudaSuccess) return cuda_fail(le);
         int Cc = lrC, Wsc = lrWs;
         void* largs[] = {&la, &ent, &entr, &Wsc, &Cc, &fail_rows, &fail_count};
@@ -630,7 +649,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             a.vec_nr = aligned(nr, 16) && Wp % 8 == 0 && a.nr_img_stride % 8 == 0 && a.tile_cols >= W;
             const void* dfn = take_new ? dense_kernel_ptr<true>() : dense_kernel_ptr<false>();
             const int dsm = dense_smem_bytes((int)W);
-            e = cudaFuncSetAttribute(dfn, cudaFuncAttributeMaxDynamicSharedMemorySize, dsm);
+            e = set_dyn_smem((const void*)(dfn), dsm);
             if (e != cudaSuccess) return cuda_fail(e);
             const int64_t dblocks = std::min<int64_t>((a.total_rows + kDenseWarps - 1) / kDenseWarps, 148 * 16);
             void* dargs[] = {&a};
@@ -687,7 +706,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             const void* afn = take_new ? (owners ? anc_kernel_ptr<true, true>() : anc_kernel_ptr<true, false>())
                                        : (owners ? anc_kernel_ptr<false, true>() : anc_kernel_ptr<false, false>());
             const int asm_bytes = anc_smem_bytes((int)W);
-            e = cudaFuncSetAttribute(afn, cudaFuncAttributeMaxDynamicSharedMemorySize, asm_bytes);
+            e = set_dyn_smem((const void*)(afn), asm_bytes);
             if (e != cudaSuccess) return cuda_fail(e);
             if (a.total_rows > 16384 && (a.pts_gate || a.lr_gate)) {
                 // many rows, some owned by other kernels (C3: every plane a point
@@ -1003,7 +1022,7 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
         const bool p16 = rows <= kRa16MaxDim && cols <= kRa16MaxDim;
         const void* fn = p16 ? (const void*)k_raster_anc<true> : (const void*)k_raster_anc<false>;
         const int smem = ra_smem_bytes((int)cols, p16);
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = set_dyn_smem((const void*)(fn), smem);
         if (e != cudaSuccess) return cuda_fail(e);
         static const int ra_cap = [] {  // DFC_RA_CAP (tuning): CTAs per SM, 0 = one CTA per row
             const char* v = getenv("DFC_RA_CAP");
@@ -1016,7 +1035,7 @@ int dfc_raster_u8(const uint8_t* d_img, int64_t rows, int64_t cols, int64_t pitc
     } else {
         const int padW = (int)(cols + cols / r.L + 1);
         const int smem = (2 * padW + 2 * r.T + 2) * 4;
-        e = cudaFuncSetAttribute(k_raster, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = set_dyn_smem((const void*)(k_raster), smem);
         if (e != cudaSuccess) return cuda_fail(e);
         k_raster<<<(unsigned)rows, r.T, smem, st>>>(r);
     }
