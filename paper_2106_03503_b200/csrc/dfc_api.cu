@@ -548,7 +548,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
     const int lrWs = (int)round_up(W, 32);  // scratch row stride (16-byte granules of both lists)
     const size_t ent_bytes = (size_t)round_up(a.total_rows * lrWs * 4, 256);
     const size_t entr_bytes = (size_t)round_up(a.total_rows * lrWs * 2, 256);
-    auto launch_lr = [&](RowArgs la, void* scratch, int* fail_rows, int* fail_count) -> int {
+    auto launch_lr = [&](RowArgs la, void* scratch, int* fail_rows, int* fail_count, cudaStream_t ls) -> int {
         const int64_t nchunks = (W + lrC - 1) / lrC;
         const int64_t warps = (la.total_rows + 31) / 32 * nchunks;
         const int64_t lblocks = (warps + kLrWarps - 1) / kLrWarps;
@@ -561,7 +561,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         if (le != cudaSuccess) return cuda_fail(le);
         int Cc = lrC, Wsc = lrWs;
         void* largs[] = {&la, &ent, &entr, &Wsc, &Cc, &fail_rows, &fail_count};
-        le = cudaLaunchKernel(lfn, dim3((unsigned)lblocks), dim3(32 * kLrWarps), largs, (size_t)lsm, st);
+        le = cudaLaunchKernel(lfn, dim3((unsigned)lblocks), dim3(32 * kLrWarps), largs, (size_t)lsm, ls);
         if (le != cudaSuccess) return cuda_fail(le);
         ++g_launches;
         return DFC_OK;
@@ -583,7 +583,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         RowArgs la = a;
         la.lr_gate = false;
         la.row_done = flags;
-        int rc = launch_lr(la, fl.p, nullptr, nullptr);
+        int rc = launch_lr(la, fl.p, nullptr, nullptr, st);
         if (rc != DFC_OK) return rc;
         const int64_t rblocks = std::min<int64_t>((a.total_rows + 255) / 256, 148 * 8);
         k_rows_failed<<<(unsigned)rblocks, 256, 0, st>>>(flags, a.total_rows, fail_rows, fail_count);
@@ -635,13 +635,16 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
         a.pts_gate = pts != nullptr && plane_counts != nullptr && H % 32 == 0;
         // the families beside the band path go to the helper stream (joined at scope exit,
         // before `fl` is released)
-        AuxScope aux(band_on ? aux_pipe() : nullptr, st);
+        // (batches of point planes, C3: the point kernel stays on the caller's stream and
+        // the families that find no plane of theirs go beside it)
+        const bool pts_main = !band_on && a.pts_gate && nimg > 1;
+        AuxScope aux(band_on || pts_main ? aux_pipe() : nullptr, st);
         const cudaStream_t os = aux.stream();
         if (a.pts_gate) {  // point planes: from K1a's object list, no nearest-row plane
             const void* pfn = take_new ? pts_kernel_ptr<true>() : pts_kernel_ptr<false>();
             const int64_t pblocks = ((a.total_rows + 31) / 32 + kPtsWarps - 1) / kPtsWarps;
             void* pargs[] = {&a, &pts};
-            e = cudaLaunchKernel(pfn, dim3((unsigned)pblocks), dim3(32 * kPtsWarps), pargs, 0, os);
+            e = cudaLaunchKernel(pfn, dim3((unsigned)pblocks), dim3(32 * kPtsWarps), pargs, 0, pts_main ? st : os);
             if (e != cudaSuccess) return cuda_fail(e);
             ++g_launches;
         }
@@ -658,7 +661,7 @@ int row_pass(const uint16_t* nr, int64_t nimg, int64_t H, int64_t W, int Wp, boo
             ++g_launches;
         }
         if (lr_on) {  // rows of sparse planes; overflowed rows flagged 2
-            const int rc = launch_lr(a, static_cast<char*>(fl.p) + flag_bytes + list_bytes, nullptr, nullptr);
+            const int rc = launch_lr(a, static_cast<char*>(fl.p) + flag_bytes + list_bytes, nullptr, nullptr, os);
             if (rc != DFC_OK) return rc;
         }
         a.lr_gate = lr_on || band_on;  // the other kernels skip the sparse planes' rows

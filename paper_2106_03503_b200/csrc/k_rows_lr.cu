@@ -146,13 +146,21 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
                         }
                         return;
                     }
+                    // the four sub-blocks' first owners up front: eight independent shuffles
+                    uint32_t g0[kH];
+                    int k0[kH];
+#pragma unroll
+                    for (int h = 0; h < kH; ++h) {
+                        g0[h] = __shfl_sync(FULL, wg, cnt[h]);
+                        k0[h] = (int)__shfl_sync(FULL, wk, cnt[h]);
+                    }
 #pragma unroll
                     for (int h = 0; h < kH; ++h) {
                         const int j = j0 + 128 * h;
                         uint32_t d0, d1, d2, d3;
                         {
-                            const uint32_t ge = __shfl_sync(FULL, wg, cnt[h]);
-                            const int dj = j - (int)__shfl_sync(FULL, wk, cnt[h]);
+                            const uint32_t ge = g0[h];
+                            const int dj = j - k0[h];
                             const uint32_t inc = (uint32_t)(2 * dj + 1);
                             d0 = ge + (uint32_t)(dj * dj);
                             d1 = d0 + inc;
