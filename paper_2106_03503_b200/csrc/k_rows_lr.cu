@@ -115,7 +115,7 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
         const uint32_t wav = giR > wr ? giR - wr : wr - giR;
         const uint32_t wg = wk == kLrInfK ? kInfU : wav * wav;
         if (DONLY) {
-            // ---- values only, a 512-column block whose owners all sit in the
+            // ---- values only, a block of kH x 128 columns whose owners all sit in the
             // window (the usual case on sparse planes): lane l owns columns
             // b + 128 h + 4 l + t (coalesced 16-byte stores per h).  cnt[h] =
             // entries starting at or before b + 128 h, so sub-block h is owned
@@ -123,17 +123,33 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
             // minimum of THEIR parabolas g + (j - k)^2: each is >= the
             // envelope and j's owner is among them (uint32: an entry that owns
             // a column within 512 of j has a value < 2^31 + 2^26 at j) ----
-            constexpr int kH = 4;
+#ifndef DFC_FILL_KH
+#define DFC_FILL_KH 4
+#endif
+            constexpr int kH = DFC_FILL_KH;  // 128-column sub-blocks per block: 4 or 8
+            static_assert(kH == 4 || kH == 8, "one or two REDUX words of four byte counters");
             const int s31 = __shfl_sync(FULL, s, 31);
-            if (s31 > b + 128 * kH) {  // the window holds every start up to b + 512
+            if (s31 > b + 128 * kH) {  // the window holds every start up to the block's end
                 // cnt[h] = entries (lanes >= 1) starting at or before b + 128 h: an entry
-                // counts from sub-block ceil((s - b) / 128) on; one REDUX.ADD of a byte
-                // per sub-block, prefix sums by a multiply (at most 31 entries: no carries)
+                // counts from sub-block ceil((s - b) / 128) on; one REDUX.ADD of a byte per
+                // sub-block (four per word), prefix sums by a multiply (at most 31 entries:
+                // no carries)
                 const int cf = (s - b + 127) >> 7;  // >= 1 for lanes >= 1 (they start after b)
-                const uint32_t byt = __reduce_add_sync(FULL, (lane >= 1 && cf <= kH) ? 1u << (8 * (cf - 1)) : 0u);
-                const uint32_t pre = byt * 0x01010101u;
-                const int cnt[kH + 1] = {0, (int)(pre & 0xffu), (int)((pre >> 8) & 0xffu), (int)((pre >> 16) & 0xffu),
-                                         (int)(pre >> 24)};
+                int cnt[kH + 1];
+                cnt[0] = 0;
+                {
+                    const uint32_t lo = __reduce_add_sync(FULL, (lane >= 1 && cf <= 4) ? 1u << (8 * (cf - 1)) : 0u);
+                    const uint32_t pre = lo * 0x01010101u;
+#pragma unroll
+                    for (int h = 1; h <= 4; ++h) cnt[h] = (int)((pre >> (8 * (h - 1))) & 0xffu);
+                    if (kH == 8) {
+                        const uint32_t hi =
+                            __reduce_add_sync(FULL, (lane >= 1 && cf > 4 && cf <= 8) ? 1u << (8 * (cf - 5)) : 0u);
+                        const uint32_t pre2 = (hi + (pre >> 24)) * 0x01010101u;  // byte k: cnt[4] + n5 + .. + n(5+k)
+#pragma unroll
+                        for (int h = 5; h <= kH; ++h) cnt[h] = (int)((pre2 >> (8 * (h - 5))) & 0xffu);
+                    }
+                }
                 const bool fast = vec4 && b + 128 * kH <= c1;
                 const int j0 = b + 4 * lane;
                 auto block = [&](auto FAST) {
@@ -185,7 +201,7 @@ __device__ __forceinline__ void lr_fill_row(const RowArgs& a, const uint32_t* rE
                     block(std::true_type{});
                 else
                     block(std::false_type{});
-                base += cnt[kH];  // the last entry starting at or before b + 512
+                base += cnt[kH];  // the last entry starting at or before the next block's first column
                 b += 128 * kH;
                 continue;
             }
