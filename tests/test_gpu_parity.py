@@ -314,10 +314,17 @@ def _sharded_in_process(dfc, img, world, polarity=0, dist=False, label=False):
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("kind", ["tiles", "bern", "discs", "corner", "empty"])
+@pytest.mark.parametrize("kind", ["tiles", "bern", "discs", "corner", "empty", "tall"])
 def test_sharded_library_in_process(dfc, world, kind):
     import workloads
-    if kind == "tiles":
+    if kind == "tall":  # row stripes of several coarse groups of 32 bands, partial last ones
+        rng = np.random.default_rng(5 + world)
+        img = np.zeros((4200, 203), np.uint8)
+        for r in (0, 1023, 1024, 2047, 2048, 2111, 2112, 4199):
+            img[r, rng.integers(203)] = 1
+        for _ in range(12):
+            img[rng.integers(4200), rng.integers(203)] = 1
+    elif kind == "tiles":
         img = workloads.sparse_tiles(512, 1024, tile=32, n_on=64, p=0.004, seed=3 + world)
     elif kind == "bern":
         img = oracle.random_image(301, 517, 0.02, 40 + world)   # uneven stripes, partial last band
@@ -662,6 +669,26 @@ def test_band_sparse_random(dfc, shape, npts):
     img = _sparse(shape, npts, shape[0] * 7 + shape[1] + npts)
     if img.sum() * 256 >= img.size:
         pytest.skip("not a sparse plane")
+    _check_edt(dfc, img, 0)
+
+
+@pytest.mark.parametrize("shape", [(1125, 333), (2080, 97), (4133, 40)])
+def test_band_sparse_coarse_group_boundaries(dfc, shape):
+    """Several coarse groups of 32 bands with a partial last one (and a partial
+    last group and band): objects on the rows either side of the coarse and
+    group boundaries, a far corner, and a few random ones -- the hull hierarchy
+    (coarse lines, then the groups' lines over coarse survivors + the object
+    columns in between)."""
+    H, W = shape
+    rng = np.random.default_rng(H * 31 + W)
+    img = np.zeros(shape, np.uint8)
+    for r in (1023, 1024, 1055, 1056, 127, 128, 2047, 2048, 4095, 4096):
+        if r < H:
+            img[r, rng.integers(W)] = 1
+    img[H - 1, 0] = 1
+    for _ in range(6):
+        img[rng.integers(H), rng.integers(W)] = 1
+    assert img.sum() * 256 < img.size
     _check_edt(dfc, img, 0)
 
 
