@@ -79,6 +79,20 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
     if (live) band_masks(a.img + im * a.img_stride + (int64_t)r0 * a.pitch, a.pitch, nrows, j0, a.W, a.vec, m);
     if (a.bmask && live)
         *reinterpret_cast<uint4*>(a.bmask + ((int64_t)im * a.nb + b) * a.Wp + j0) = make_uint4(m[0], m[1], m[2], m[3]);
+    // a warp whose 128 columns x 32 rows hold no nonzero byte (most warps of a
+    // sparse image), object = nonzero only: no object row, no count, no point
+    if (a.npol == 1 && a.pol0 == 0 && !__any_sync(0xffffffffu, (m[0] | m[1] | m[2] | m[3]) != 0u)) {
+        if (!live) return;
+        const int64_t off = ((int64_t)im * a.nb + b) * a.Wp + j0;
+        const uint32_t none2 = (uint32_t)kNoRow | ((uint32_t)kNoRow << 16);
+        *reinterpret_cast<uint2*>(first + off) = make_uint2(none2, none2);
+        *reinterpret_cast<uint2*>(last + off) = make_uint2(none2, none2);
+        if (a.objcol && (threadIdx.x & 7) == 0) {
+            const int Ww = (a.W + 31) >> 5;
+            if ((j0 >> 5) < Ww) a.objcol[((int64_t)im * a.nb + b) * Ww + (j0 >> 5)] = 0u;
+        }
+        return;
+    }
     for (int s = 0; s < a.npol; ++s) {
         const int pol = a.pol0 + s;
         uint16_t f[4], l[4];
@@ -102,8 +116,7 @@ __global__ void k_band_summary(ColArgs a, uint16_t* __restrict__ first, uint16_t
         }
         if (counts) {
             const unsigned mine = (unsigned)(__popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]));
-            unsigned long long c = mine;
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            const unsigned long long c = __reduce_add_sync(0xffffffffu, mine);  // <= 32 x 128: one REDUX
             const int lane = threadIdx.x & 31;
             const int64_t plane = (int64_t)s * a.n_img + im;
             unsigned long long old = 0;
