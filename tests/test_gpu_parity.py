@@ -806,3 +806,35 @@ def test_small_sparse_default_dispatch(dfc):
             _check_edt(dfc, img, polarity=1)
     finally:
         dfc.set_band_min_pixels(0)
+
+
+def test_two_host_threads_two_streams(dfc):
+    """Two host threads driving the same device on their own streams at the
+    same time (the helper stream and its events are shared per device: the
+    enqueue is serialised by a mutex, the results must not mix)."""
+    import threading
+    imgs = [_sparse((700, 900), 9, 1), oracle.random_image(300, 500, 0.05, 2)]
+    wants = [oracle.to_i32(oracle.edt(i)) for i in imgs]
+    errs = []
+
+    def work(k):
+        try:
+            dfc.set_band_min_pixels(0)  # per thread
+            st = torch.cuda.Stream()
+            dev = _dev(imgs[k])
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                for _ in range(20):
+                    out = dfc.edt(dev, dist=False)
+                    st.synchronize()
+                    if not (out["sqdist"].cpu().numpy() == wants[k]).all():
+                        errs.append(k)
+        except Exception as e:  # pragma: no cover
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
