@@ -139,3 +139,20 @@ def test_c5_full_map_vs_reference(dfc, wl):
     dt = dfc.edt(dev.t().contiguous(), dist=False)["sqdist"]
     d0 = dfc.edt(dev, dist=False)["sqdist"]
     assert bool((dt == d0.t()).all())
+
+
+def test_dual_polarity_above_the_band_gate(dfc, wl):
+    """Both polarities of one sparse image above the band path's size gate
+    (4100 x 4200 > 2^24 pixels): the background->object plane takes the band
+    path on the caller's stream while the object->background plane (nearly
+    all object pixels) runs k_rows_anc on the helper stream at the same time."""
+    img = wl.sparse_tiles(4100, 4200, tile=128, n_on=300, p=3e-4, seed=12)
+    assert img.sum() * 256 < img.size
+    out = dfc.edt_dual(_dev(img))
+    torch.cuda.synchronize()
+    ref = oracle.ref_edt if oracle.ref_available() else oracle.edt
+    for key, src in (("bg", img), ("obj", (img == 0).astype(np.uint8))):
+        want = oracle.to_i32(ref(src))
+        np.testing.assert_array_equal(out["sqdist_" + key].cpu().numpy(), want)
+        np.testing.assert_array_equal(out["dist_" + key].cpu().numpy().view(np.uint32),
+                                      oracle.sqrt_f32(want).view(np.uint32))
