@@ -19,9 +19,7 @@
 //              lies on the lower convex hull of those points (collinear points
 //              kept, for ties).  Likewise below the band at i1, and otherwise
 //              column k* holds an object pixel inside the band.  Any superset
-//              is exact (the row pass evaluates each candidate's true g_k(i)),
-//              so the hulls are taken per window of 1024 columns (a hull point
-//              of the row is a hull point of every window holding it):
+//              is exact (the row pass evaluates each candidate's true g_k(i)).
 //  k_hull      one CTA prunes one compact point list towards its lower hull
 //              (data-parallel rounds: a point above the chord of two list
 //              neighbours goes, survivors are compacted); filters at coarse
@@ -29,16 +27,20 @@
 //              groups' lines over the coarse filter plus the object columns
 //              in between (see "hull filter" below).  Output: candidate bit
 //              masks [plane][group][side][W/32].
-//  k_band_rows warp = (plane, band), lane = row: the reference's stack algorithm
-//              over the band's candidates only (g from the band mask and the
-//              carries, the upper row on ties, exact_edt.cpp:351), the top
-//              kBandCap entries in a shared-memory ring that spills its bottom
-//              to the row's list in global memory and reloads from it -- the
-//              stack is unbounded, no row needs a fallback.  The final stack is
-//              the row's owner list (column | start << 16, nearest row).
-//  k_rows_fill warp = row: the list staged in shared memory (cp.async), then
-//              the shared lr_fill_row (k_rows_lr.cu): lane = column, 16-byte
-//              streaming stores -- the HBM-bound part (C5: 4 B/px).
+//  k_band_rows_fill  CTA = (plane, band), 8 warps.
+//              Stack phase (band_rows_body): warp = one of 8 column chunks of
+//              equal candidate counts, lane = row: the reference's stack
+//              algorithm over the chunk's candidates only (g from the band mask
+//              and the carries, the upper row on ties, exact_edt.cpp:351), the
+//              top kBandCap entries in a shared-memory ring that spills its
+//              bottom to the row's list in global memory and reloads from it --
+//              the stack is unbounded, no row needs a fallback.  The final
+//              stack is the row's owner list (column | start << 16, nearest row).
+//              Fill phase (band_fill_body): warp = 4 of the band's rows, the
+//              rows' lists staged by TMA bulk copies (two buffers, mbarriers),
+//              then the shared lr_fill_row (k_rows_lr.cu): lane = column,
+//              16-byte streaming stores -- the HBM-bound part (C5: 4 B/px).
+//  k_band_rows / k_rows_fill  the same two phases as two launches (DFC_BAND_FUSED=0).
 //
 // tests/band_model.py is the statement-level model (fuzzed against brute
 // force for both tie rules with small windows, lanes and ring capacities).
