@@ -370,26 +370,6 @@ struct AuxScope {
     }
 };
 
-// k_rows_fill CTAs per SM (DFC_FILL_CTAS, tuning) of the unfused launch.
-int fill_ctas() {
-    static const int n = [] {
-        const char* v = getenv("DFC_FILL_CTAS");
-        const int x = v ? atoi(v) : 0;
-        return x >= 1 && x <= 16 ? x : 4;
-    }();
-    return n;
-}
-
-// DFC_BAND_FUSED=0 (A/B): k_band_rows and k_rows_fill as two launches instead
-// of one CTA per band doing both
-bool band_fused() {
-    static const bool on = [] {
-        const char* v = getenv("DFC_BAND_FUSED");
-        return !(v && v[0] == '0');
-    }();
-    return on;
-}
-
 template <bool TN, int DO>
 cudaError_t launch_rows_fill(const RowArgs& a, const BandArgs& ba, unsigned grid, int smem, cudaStream_t st) {
     cudaError_t e = set_dyn_smem((const void*)(k_band_rows_fill<TN, DO>), smem);
@@ -429,8 +409,7 @@ int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cud
 
     const int donly = a.D && !a.LB && !a.NC ? (a.S ? 2 : 1) : 0;  // values only (D, optionally sqrt D)
     const int64_t tasks = (int64_t)ba.nplanes * ba.nb;
-    const int rsm = band_rows_smem_bytes();
-    if (band_fused()) {
+    {
         const unsigned g = (unsigned)tasks;
         // CTAs per SM of the fused kernel, by shared memory (DFC_BAND_OCC, tuning):
         // measured on C5: 4 (the stack phases need the parallelism) 1.356 ms, 3 1.451, 2 1.533, 1 2.082
@@ -439,8 +418,7 @@ int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cud
             const int x = v ? atoi(v) : 0;
             return x >= 1 && x <= 4 ? x : 4;
         }();
-        const int rsm_occ = std::max(band_fused_smem_bytes(), std::min(227 * 1024, (228 * 1024) / occ - 1024 - 1024) / 16 * 16);
-        const int rsm = rsm_occ;
+        const int rsm = std::max(band_fused_smem_bytes(), std::min(227 * 1024, (228 * 1024) / occ - 1024 - 1024) / 16 * 16);
         if (take_new)
             e = donly == 1 ? launch_rows_fill<true, 1>(a, ba, g, rsm, st)
                            : donly == 2 ? launch_rows_fill<true, 2>(a, ba, g, rsm, st) : launch_rows_fill<true, 0>(a, ba, g, rsm, st);
@@ -449,29 +427,7 @@ int launch_band_path(const RowArgs& a, const BandArgs& ba_in, bool take_new, cud
                            : donly == 2 ? launch_rows_fill<false, 2>(a, ba, g, rsm, st) : launch_rows_fill<false, 0>(a, ba, g, rsm, st);
         if (e != cudaSuccess) return cuda_fail(e);
         ++g_launches;
-        return DFC_OK;
     }
-    const void* rfn = take_new ? (const void*)k_band_rows<true> : (const void*)k_band_rows<false>;
-    e = set_dyn_smem((const void*)(rfn), rsm);
-    if (e != cudaSuccess) return cuda_fail(e);
-    const void* ffn = donly == 1 ? (const void*)k_rows_fill<1> : donly == 2 ? (const void*)k_rows_fill<2>
-                                                                            : (const void*)k_rows_fill<0>;
-    const int fsm = fill_smem_bytes();
-    e = set_dyn_smem((const void*)(ffn), fsm);
-    if (e != cudaSuccess) return cuda_fail(e);
-    if (take_new)
-        k_band_rows<true><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(ba);
-    else
-        k_band_rows<false><<<(unsigned)tasks, 32 * kBandWarps, rsm, st>>>(ba);
-    const int64_t rows = (int64_t)ba.nplanes * ba.H;
-    const int64_t fblocks = std::max<int64_t>(1, std::min<int64_t>((rows + kFillWarps - 1) / kFillWarps, 148 * fill_ctas()));
-    if (donly == 1)
-        k_rows_fill<1><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
-    else if (donly == 2)
-        k_rows_fill<2><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
-    else
-        k_rows_fill<0><<<(unsigned)fblocks, 32 * kFillWarps, fsm, st>>>(a, ba);
-    g_launches += 2;
     return DFC_OK;
 }
 

@@ -40,7 +40,6 @@
 //              rows' lists staged by TMA bulk copies (two buffers, mbarriers),
 //              then the shared lr_fill_row (k_rows_lr.cu): lane = column,
 //              16-byte streaming stores -- the HBM-bound part (C5: 4 B/px).
-//  k_band_rows / k_rows_fill  the same two phases as two launches (DFC_BAND_FUSED=0).
 //
 // tests/band_model.py is the statement-level model (fuzzed against brute
 // force for both tie rules with small windows, lanes and ring capacities).
@@ -51,8 +50,7 @@ namespace dfc {
 constexpr int kBandWarps = 8;       // k_band_rows: warps (column chunks) per band
 constexpr int kBandCap = 16;        // ring entries per lane (power of two)
 constexpr int kCandCap = 2048;      // candidates of a band listed in shared memory
-constexpr int kFillWarps = 4;
-constexpr int kFillCap = 512;       // list entries staged per warp (k_rows_fill); a chunk of a listed
+constexpr int kFillCap = 512;       // list entries staged per warp and buffer (the fill phase); a chunk of a listed
                                     // band holds ~kCandCap / kBandWarps candidates
 
 struct BandArgs {
@@ -690,15 +688,6 @@ __device__ __forceinline__ void band_rows_body(const BandArgs& a, BandSmem& sm, 
     a.nent[row * kBandWarps + warp] = ng;
 }
 
-template <bool TAKE_NEW>
-__global__ void __launch_bounds__(32 * kBandWarps) k_band_rows(BandArgs a) {
-    extern __shared__ uint4 band_raw[];
-    const int64_t task = blockIdx.x;
-    if (!band_plane(a, (int)(task / a.nb))) return;  // CTA-uniform
-    band_rows_body<TAKE_NEW>(a, *reinterpret_cast<BandSmem*>(band_raw), task);
-}
-
-inline int band_rows_smem_bytes() { return (int)sizeof(BandSmem); }
 
 // ------------------------------------------------------------------- fill
 struct FillSmem {
@@ -799,19 +788,6 @@ __device__ __forceinline__ void band_fill_row(const RowArgs& ra, const BandArgs&
     }
 }
 
-template <int DONLY>
-__global__ void __launch_bounds__(32 * kFillWarps) k_rows_fill(RowArgs ra, BandArgs a) {
-    extern __shared__ uint4 fill_raw[];
-    FillSmem& sm = reinterpret_cast<FillSmem*>(fill_raw)[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    const int64_t total = (int64_t)a.nplanes * a.H;
-    const int64_t nw = (int64_t)gridDim.x * kFillWarps;
-    for (int64_t row = (int64_t)blockIdx.x * kFillWarps + (threadIdx.x >> 5); row < total; row += nw) {
-        if (!band_plane(a, (int)(row / a.H))) continue;  // warp-uniform
-        band_fill_row<DONLY>(ra, a, sm, row, lane);
-    }
-}
-
 // ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) with an mbarrier per buffer ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
@@ -851,8 +827,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Stacks and fill of one band in one CTA: the band's 8 warps build its rows'
 // lists, then each writes 4 of its 32 rows.  The lists stay in L2; a CTA in
 // its (latency-bound) stack phase shares the SM with CTAs in their (HBM-bound)
-// fill phase, which a separate k_band_rows launch in front of k_rows_fill
-// cannot (C5: 156 + 766 us as two launches).  Fill phase per warp: the band's
+// fill phase (as two launches the phases took 156 + 766 us on C5, one launch gap more).  Fill phase per warp: the band's
 // chunk bounds and the list lengths of its 4 rows in one round trip, then the
 // rows' lists by TMA bulk copies into two buffers (row k + 2 is in flight while
 // row k is written): no load latency between the rows' store streams.
@@ -952,6 +927,5 @@ inline int band_fused_smem_bytes() {
     return std::max((int)sizeof(BandSmem), kBandWarps * ((int)sizeof(FusedFill) + 16));
 }
 
-inline int fill_smem_bytes() { return kFillWarps * (int)sizeof(FillSmem); }
 
 }  // namespace dfc
