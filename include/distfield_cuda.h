@@ -197,6 +197,21 @@ int dfc_raster_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pit
                         dfc_stream_t stream);
 
 /*
+ * Danielsson's vector transform (vector_dt.hpp:56-72, vector_dt.cpp:41-124):
+ * the approximate Euclidean transform that propagates offset magnitudes,
+ * bit-exact with the reference's downward + upward sweeps (first_sweep_only
+ * != 0: danielsson_first_sweep, the downward sweep alone).  Per image, dense
+ * rows x cols outputs: d_dist the squared lengths (UINT64_MAX = infinity,
+ * DistanceMap::kInfinity), d_dy / d_dx the offset components (0xFFFFFFFF =
+ * Offset::kUnset).  A strict raster recurrence: one warp per image, parallel
+ * over the images of a batch and over 32 cells of a row at a time (see
+ * csrc/k_vector.cu).  n_images >= 1; image_stride_bytes is ignored for 1.
+ */
+int dfc_danielsson_u8(const uint8_t* d_img, int64_t n_images, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                      int64_t image_stride_bytes, int first_sweep_only, uint64_t* d_dist, uint32_t* d_dy,
+                      uint32_t* d_dx, dfc_stream_t stream);
+
+/*
  * Float distances of a squared-distance map: (float)sqrt((double)D) for each
  * of n int32 values (DFC_INF_I32 -> +inf) -- the row pass's own epilogue
  * (grid.cpp:146 semantics), e.g. for a map from dfc_vertical_u8.

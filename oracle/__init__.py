@@ -70,6 +70,7 @@ def _bind_orc(lib):
         getattr(lib, f).argtypes = [_u8p, _sz, _sz, _u64p]
     lib.orc_brute.argtypes = [_u8p, _sz, _sz, C.c_int, _u64p]
     lib.orc_raster_pass.argtypes = [_u64p, _sz, _sz, C.c_int]
+    lib.orc_danielsson.argtypes = [_u8p, _sz, _sz, C.c_int, _u64p, _u32p, _u32p]
     return lib
 
 
@@ -98,6 +99,8 @@ def _bind_ref(lib):
     lib.dfref_build_row_envelope.restype = C.c_longlong
     lib.dfref_build_row_envelope.argtypes = [_i64p, _sz, C.c_int64, C.c_int, _i64p, _i64p]
     lib.dfref_raster_pass.argtypes = [_u64p, _sz, _sz, C.c_int]
+    if hasattr(lib, "dfref_danielsson"):
+        lib.dfref_danielsson.argtypes = [_u8p, _sz, _sz, C.c_int, _u64p, _u32p, _u32p]
     lib.dfref_kind_bound.restype = C.c_uint64
     lib.dfref_kind_bound.argtypes = [C.c_int, _sz, _sz]
     return lib
@@ -264,6 +267,27 @@ def brute(img, metric):
     out = np.empty((r, c), np.uint64)
     orc.orc_brute(img, r, c, metric, out)
     return out
+
+
+def danielsson(img, first_sweep=False):
+    """vector_dt.cpp:108-124 restated: (squared distances uint64, dy, dx uint32;
+    0xFFFFFFFF = unset offset, UINT64_MAX = infinity)."""
+    img, r, c = _img(img)
+    d = np.empty((r, c), np.uint64)
+    dy = np.empty((r, c), np.uint32)
+    dx = np.empty((r, c), np.uint32)
+    orc.orc_danielsson(img, r, c, int(first_sweep), d, dy, dx)
+    return d, dy, dx
+
+
+def ref_danielsson(img, first_sweep=False):
+    """The reference's own danielsson / danielsson_first_sweep (oracle/_ref)."""
+    img, r, c = _img(img)
+    d = np.empty((r, c), np.uint64)
+    dy = np.empty((r, c), np.uint32)
+    dx = np.empty((r, c), np.uint32)
+    ref.dfref_danielsson(img, r, c, int(first_sweep), d, dy, dx)
+    return d, dy, dx
 
 
 def to_i32(dm):

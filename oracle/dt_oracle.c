@@ -418,3 +418,55 @@ void orc_brute(const uint8_t* img, uint64_t rows, uint64_t cols, int metric, uin
     free(fr);
     free(fc);
 }
+
+/* ---- Danielsson vector transform (vector_dt.cpp:41-116) ----
+ * Offsets are magnitudes (dy, dx), ORC_UNSET where no feature was claimed yet
+ * (vector_dt.hpp:15-19); a cell is overwritten only on a strictly smaller
+ * squared distance (:58).  sweep_down (:64-79): per row, the vertical update,
+ * then left-to-right (from the left neighbour, then from the upper-left one),
+ * then right-to-left (from the upper-right one, then from the right
+ * neighbour).  sweep_up (:81-96) mirrors it with the row below, the in-row
+ * neighbour first in BOTH of its horizontal passes.  first_only = 1 is
+ * danielsson_first_sweep (:118-124). */
+#define ORC_UNSET 0xFFFFFFFFu
+static void dn_update(uint64_t* dist, uint32_t* dy, uint32_t* dx, uint64_t cols, uint64_t i, uint64_t j,
+                      uint64_t si, uint64_t sj, uint32_t ay, uint32_t ax) {
+    const uint64_t s = si * cols + sj, p = i * cols + j;
+    if (dy[s] == ORC_UNSET) return; /* :53 */
+    const uint32_t ny = dy[s] + ay, nx = dx[s] + ax;
+    const uint64_t d = (uint64_t)ny * ny + (uint64_t)nx * nx; /* :45-48 */
+    if (dist[p] > d) { /* :58 strict */
+        dist[p] = d;
+        dy[p] = ny;
+        dx[p] = nx;
+    }
+}
+
+void orc_danielsson(const uint8_t* img, uint64_t rows, uint64_t cols, int first_only, uint64_t* dist,
+                    uint32_t* dy, uint32_t* dx) {
+    orc_init_map(img, rows, cols, dist); /* init_state :98-106 */
+    for (uint64_t p = 0; p < rows * cols; ++p) dy[p] = dx[p] = img[p] ? 0u : ORC_UNSET;
+    for (uint64_t i = 1; i < rows; ++i) { /* sweep_down :64-79 */
+        for (uint64_t j = 0; j < cols; ++j) dn_update(dist, dy, dx, cols, i, j, i - 1, j, 1, 0);
+        for (uint64_t j = 1; j < cols; ++j) {
+            dn_update(dist, dy, dx, cols, i, j, i, j - 1, 0, 1);
+            dn_update(dist, dy, dx, cols, i, j, i - 1, j - 1, 1, 1);
+        }
+        for (uint64_t j = cols - 1; j-- > 0;) {
+            dn_update(dist, dy, dx, cols, i, j, i - 1, j + 1, 1, 1);
+            dn_update(dist, dy, dx, cols, i, j, i, j + 1, 0, 1);
+        }
+    }
+    if (first_only) return;
+    for (uint64_t i = rows - 1; i-- > 0;) { /* sweep_up :81-96 */
+        for (uint64_t j = 0; j < cols; ++j) dn_update(dist, dy, dx, cols, i, j, i + 1, j, 1, 0);
+        for (uint64_t j = 1; j < cols; ++j) {
+            dn_update(dist, dy, dx, cols, i, j, i, j - 1, 0, 1);
+            dn_update(dist, dy, dx, cols, i, j, i + 1, j - 1, 1, 1);
+        }
+        for (uint64_t j = cols - 1; j-- > 0;) {
+            dn_update(dist, dy, dx, cols, i, j, i, j + 1, 0, 1);
+            dn_update(dist, dy, dx, cols, i, j, i + 1, j + 1, 1, 1);
+        }
+    }
+}

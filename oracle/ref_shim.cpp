@@ -2,7 +2,7 @@
 //
 // A flat extern "C" shim over the UNMODIFIED reference library, compiled by
 // oracle/Makefile directly from the reference sources where they lie
-// (/root/reference/proj/core/src/{grid,exact_edt,propagation,random_image,netpbm}.cpp)
+// (/root/reference/proj/core/src/{grid,exact_edt,propagation,random_image,netpbm,vector_dt}.cpp)
 // into oracle/_ref/libdfref.so.  Used (a) to pin the C restatement
 // oracle/dt_oracle.c and (b) as bench.py's CPU baseline ("kind": "reference").
 // Each call copies the caller's uint8 buffer into a distfield::BinaryImage
@@ -20,6 +20,7 @@
 #include "distfield/netpbm.hpp"
 #include "distfield/propagation.hpp"
 #include "distfield/random_image.hpp"
+#include "distfield/vector_dt.hpp"
 
 using namespace distfield;
 
@@ -257,6 +258,21 @@ int dfref_labels_render(const std::uint8_t* img, std::size_t rows, std::size_t c
     } catch (const std::exception&) {
         return 1;
     }
+}
+
+// danielsson(img) / danielsson_first_sweep(img) (vector_dt.cpp:108-124): the
+// squared-distance map and the offset components (Offset::kUnset where unset).
+int dfref_danielsson(const std::uint8_t* img, std::size_t rows, std::size_t cols, int first_only, std::uint64_t* dist,
+                     std::uint32_t* dy, std::uint32_t* dx) {
+    const auto bi = to_image(img, rows, cols);
+    const auto r = first_only ? danielsson_first_sweep(bi) : danielsson(bi);
+    copy_map(r.distance, dist);
+    for (std::size_t i = 0; i < rows; ++i)
+        for (std::size_t j = 0; j < cols; ++j) {
+            dy[i * cols + j] = r.offsets(i, j).dy;
+            dx[i * cols + j] = r.offsets(i, j).dx;
+        }
+    return 0;
 }
 
 std::uint64_t dfref_kind_bound(int kind, std::size_t rows, std::size_t cols) {

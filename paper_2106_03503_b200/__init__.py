@@ -65,6 +65,7 @@ _lib.dfc_gray_i32.argtypes = [_vp, _i64, C.c_int, _vp, _vp, _vp, _vp]
 _lib.dfc_labels_gray.argtypes = [_vp, _i64, _i64, _vp, _vp]
 _lib.dfc_row_owners_i64.argtypes = [_vp, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp]
 _lib.dfc_raster_pass_u64.argtypes = [_vp, _i64, _i64, _i64, C.c_int, _vp]
+_lib.dfc_danielsson_u8.argtypes = [_vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp, _vp, _vp, _vp]
 
 
 class Shard(C.Structure):
@@ -90,7 +91,7 @@ EXPORTED_SYMBOLS = (
     "dfc_unpack_pbm", "dfc_binarize_u8", "dfc_count_objects_u8", "dfc_gray_i32", "dfc_labels_gray",
     "dfc_edt_u8_sharded", "dfc_shard_cols", "dfc_shard_rows", "dfc_comm_unique_id", "dfc_comm_init_rank",
     "dfc_comm_init_all", "dfc_comm_destroy", "dfc_last_nccl_error", "dfc_row_owners_i64", "dfc_raster_pass_u64",
-    "dfc_set_band_min_pixels", "dfc_debug_guard_violations",
+    "dfc_set_band_min_pixels", "dfc_debug_guard_violations", "dfc_danielsson_u8",
 )
 
 
@@ -471,6 +472,27 @@ def raster_pass(dm: torch.Tensor, which, stream=None) -> torch.Tensor:
 
 
 # ---------------------------------------------------------- multi-GPU (config 5)
+def danielsson(img: torch.Tensor, first_sweep: bool = False, stream=None):
+    """Danielsson's vector transform (vector_dt.cpp:108-124) of one image [H, W]
+    or a batch [n, H, W] (uint8 CUDA tensor): {"sqdist": int64 holding the
+    reference's uint64 values (-1 = infinity), "dy", "dx": int32 holding uint32
+    offset magnitudes (-1 = unset)}; see dfc_danielsson_u8."""
+    if not img.is_cuda or img.dtype not in (torch.uint8, torch.bool) or img.dim() not in (2, 3):
+        raise ValueError("image must be a 2-D or 3-D uint8 (or bool) CUDA tensor")
+    if img.dtype == torch.bool:
+        img = img.view(torch.uint8)
+    if img.stride(-1) != 1:
+        img = img.contiguous()
+    batch = img.dim() == 3
+    n = img.shape[0] if batch else 1
+    h, w = img.shape[-2], img.shape[-1]
+    o = {"sqdist": _empty(tuple(img.shape), torch.int64, img), "dy": _empty(tuple(img.shape), torch.int32, img),
+         "dx": _empty(tuple(img.shape), torch.int32, img)}
+    _check(_lib.dfc_danielsson_u8(_ptr(img), n, h, w, img.stride(-2), img.stride(0) if batch else 0,
+                                  int(first_sweep), _ptr(o["sqdist"]), _ptr(o["dy"]), _ptr(o["dx"]), _stream(stream)))
+    return o
+
+
 def shard_cols(cols: int, world: int, rank: int):
     """[col0, col0 + ncols): the column stripe rank `rank` holds (dfc_shard_cols)."""
     a, b = _i64(), _i64()

@@ -12,5 +12,6 @@
 #include "k_raster_anc.cu"
 #include "k_render.cu"
 #include "k_passes.cu"
+#include "k_vector.cu"
 #include "dfc_api.cu"
 #include "dfc_shard.cu"

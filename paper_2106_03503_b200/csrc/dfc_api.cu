@@ -1221,6 +1221,43 @@ int dfc_raster_pass_u64(uint64_t* d_map, int64_t rows, int64_t cols, int64_t pit
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);
 }
 
+int dfc_danielsson_u8(const uint8_t* d_img, int64_t n_images, int64_t rows, int64_t cols, int64_t pitch_bytes,
+                      int64_t image_stride_bytes, int first_sweep_only, uint64_t* d_dist, uint32_t* d_dy,
+                      uint32_t* d_dx, dfc_stream_t stream) {
+    if (!d_img || !d_dist || !d_dy || !d_dx || n_images < 1 || n_images > 0x7fffffff) return DFC_ERR_ARG;
+    if (rows < 1 || cols < 1 || rows > 65535 || cols > 65535) return DFC_ERR_SHAPE;
+    if (pitch_bytes < cols || (n_images > 1 && image_stride_bytes < rows * pitch_bytes)) return DFC_ERR_ARG;
+    init_pool_once();
+    g_launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    DanArgs a;
+    a.img = d_img;
+    a.pitch = pitch_bytes;
+    a.img_stride = image_stride_bytes;
+    a.rows = (int)rows;
+    a.cols = (int)cols;
+    a.Wb = (int)round_up(cols, 2);
+    a.first_only = first_sweep_only != 0;
+    a.dist = d_dist;
+    a.dy = d_dy;
+    a.dx = d_dx;
+    a.scratch = nullptr;
+    const size_t smem = (size_t)2 * 16 * a.Wb;  // two rows of (uint64 D, uint32 dy, uint32 dx)
+    Scratch sc(st);
+    if (smem > 200 * 1024) {  // rows too wide for shared memory: the same layout in global scratch
+        const cudaError_t e = sc.alloc(smem * (size_t)n_images);
+        if (e != cudaSuccess) return cuda_fail(e);
+        a.scratch = static_cast<char*>(sc.p);
+    } else {
+        const cudaError_t e = set_dyn_smem((const void*)k_danielsson, (int)smem);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    k_danielsson<<<(unsigned)n_images, 32, a.scratch ? 0 : smem, st>>>(a);
+    ++g_launches;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DFC_OK : cuda_fail(e);
+}
+
 int dfc_set_profile_events(void* ev_col_begin, void* ev_row_begin, void* ev_row_end) {
     g_ev[0] = static_cast<cudaEvent_t>(ev_col_begin);
     g_ev[1] = static_cast<cudaEvent_t>(ev_row_begin);

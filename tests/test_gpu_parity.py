@@ -867,3 +867,42 @@ def test_cuda_graph_capture_and_replay(dfc):
             np.testing.assert_array_equal(out["sqdist"].cpu().numpy(), want)
             np.testing.assert_array_equal(out["dist"].cpu().numpy().view(np.uint32),
                                           oracle.sqrt_f32(want).view(np.uint32))
+
+
+def _check_danielsson(dfc, img, first_sweep=False):
+    out = dfc.danielsson(_dev(img), first_sweep=first_sweep)
+    torch.cuda.synchronize()
+    d, dy, dx = oracle.danielsson(img, first_sweep)
+    np.testing.assert_array_equal(out["sqdist"].cpu().numpy().view(np.uint64), d)
+    np.testing.assert_array_equal(out["dy"].cpu().numpy().view(np.uint32), dy)
+    np.testing.assert_array_equal(out["dx"].cpu().numpy().view(np.uint32), dx)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 40), (37, 1), (2, 2), (9, 33), (33, 32), (64, 65), (50, 200), (200, 97),
+                                   (3, 1000), (130, 130)])
+@pytest.mark.parametrize("density", [0.0, 0.004, 0.05, 0.3, 0.9, 1.0])
+def test_danielsson_random(dfc, shape, density):
+    """vector_dt.cpp:108-124 on the device: squared lengths and both offset
+    components bit-exact with the restated (reference-pinned) sweeps, for both
+    danielsson and danielsson_first_sweep."""
+    img = oracle.random_image(shape[0], shape[1], density, shape[0] * 131 + shape[1] + int(density * 1000))
+    _check_danielsson(dfc, img)
+    _check_danielsson(dfc, img, first_sweep=True)
+
+
+def test_danielsson_ties_wide_and_batch(dfc):
+    img = np.zeros((90, 120), np.uint8)
+    img[::9, ::11] = 1                     # a lattice: equal-length candidates from both sides
+    _check_danielsson(dfc, img)
+    img2 = np.zeros((40, 7000), np.uint8)  # rows wider than the shared-memory buffers
+    img2[20, 10] = img2[3, 6990] = img2[39, 3500] = 1
+    _check_danielsson(dfc, img2)
+    _check_danielsson(dfc, img2, first_sweep=True)
+    batch = np.stack([oracle.random_image(70, 90, p, 9 + k) for k, p in enumerate((0.0, 0.01, 0.2, 0.6, 0.03))])
+    out = dfc.danielsson(_dev(batch))
+    torch.cuda.synchronize()
+    for k in range(batch.shape[0]):
+        d, dy, dx = oracle.danielsson(batch[k])
+        np.testing.assert_array_equal(out["sqdist"][k].cpu().numpy().view(np.uint64), d)
+        np.testing.assert_array_equal(out["dy"][k].cpu().numpy().view(np.uint32), dy)
+        np.testing.assert_array_equal(out["dx"][k].cpu().numpy().view(np.uint32), dx)
