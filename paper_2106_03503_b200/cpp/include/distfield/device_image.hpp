@@ -12,6 +12,7 @@
 #include <string>
 
 #include "distfield/grid.hpp"
+#include "distfield/vector_dt.hpp"
 #include "distfield/netpbm.hpp"
 
 namespace distfield {
@@ -55,6 +56,10 @@ private:
 
 // squared_euclidean (edt), cityblock, chessboard or chamfer3 of the image.
 DeviceMap transform(const DeviceImage& img, DistanceKind kind);
+
+// Danielsson's vector transform of an image already in device memory
+// (vector_dt.hpp; the CLI's --algorithm danielsson): host result.
+VectorDtResult danielsson(const DeviceImage& img);
 
 // Voronoi labels (ordinals, the reference LabelMap) on the device; throws
 // std::domain_error("no features: voronoi labels undefined") for an image

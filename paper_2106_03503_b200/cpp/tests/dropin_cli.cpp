@@ -15,6 +15,7 @@
 #include "distfield/exact_edt.hpp"
 #include "distfield/propagation.hpp"
 #include "distfield/random_image.hpp"
+#include "distfield/vector_dt.hpp"
 
 using namespace distfield;
 
@@ -100,6 +101,19 @@ int main(int argc, char** argv) {
             put_map(out, chamfer34(img));
         } else if (op == "chessboard") {
             put_map(out, chessboard(img));
+        } else if (op == "danielsson" || op == "danielsson_first") {  // map, then dy, dx (uint32), then to_text
+            const auto r = op == "danielsson" ? danielsson(img) : danielsson_first_sweep(img);
+            put_map(out, r.distance);
+            std::vector<std::uint32_t> dy(rows * cols), dx(rows * cols);
+            for (std::size_t i = 0; i < rows; ++i)
+                for (std::size_t j = 0; j < cols; ++j) {
+                    dy[i * cols + j] = r.offsets(i, j).dy;
+                    dx[i * cols + j] = r.offsets(i, j).dx;
+                }
+            put(out, dy);
+            put(out, dx);
+            const std::string t = to_text(r.offsets);
+            out.write(t.data(), static_cast<std::streamsize>(t.size()));
         } else if (op == "both") {
             const auto [a, b] = edt_both_polarities(img);
             put_map(out, a);

@@ -3,9 +3,9 @@
 // routed to the B200 path: a P4 input travels to the GPU as its packed raster
 // and is unpacked there; transforms, labels and gray renderings stay in HBM;
 // only the requested outputs come back.  Same options, defaults, messages and
-// exit codes ("error: <what>", exit 1).  Not provided: `chart` (reference
-// metric charts, not a transform) and the Danielsson vector DT
-// (--algorithm danielsson / --offsets), both outside the B200 hot path.
+// exit codes ("error: <what>", exit 1).  --algorithm danielsson / --offsets run
+// the vector transform's sweeps on the device (k_vector.cu).  Not provided:
+// `chart` (reference metric charts, not a transform).
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -160,9 +160,7 @@ int run_transform(const Args& a) {
     } else if (metric == "chessboard") {  // B200 addition (no reference transform)
         kind = DistanceKind::chessboard;
     } else if (metric == "euclidean") {
-        if (algorithm == "danielsson")
-            throw std::runtime_error("--algorithm danielsson is not part of the B200 build");
-        if (!parse_algorithm(algorithm))
+        if (algorithm != "danielsson" && !parse_algorithm(algorithm))
             throw std::runtime_error(
                 "euclidean supports --algorithm bruteforce|simple|improved|envelope|danielsson");
         kind = DistanceKind::squared_euclidean;  // every algorithm yields the same map (exact_edt.cpp:285-317)
@@ -172,9 +170,24 @@ int run_transform(const Args& a) {
 
     const DeviceImage img = load_image(a, true);
     if (img.object_count() == 0) std::cerr << "warning: no features, distances are infinite everywhere\n";
+    const bool vector_dt = metric == "euclidean" && algorithm == "danielsson";
+    if (!offsets.empty() && !vector_dt) throw std::runtime_error("--offsets requires --algorithm danielsson");
+    if (vector_dt) {  // distfield_cli.cpp:177-179, :192-220: the approximate vector transform
+        if (!labels.empty()) throw std::runtime_error("--labels requires an exact euclidean algorithm");
+        const VectorDtResult vec = danielsson(img);
+        if (!dump.empty()) write_file(dump, a.flag("--sqrt") ? to_text_sqrt(vec.distance) : to_text(vec.distance));
+        if (a.flag("--normalized")) throw std::runtime_error("--normalized applies to chamfer34 results only");
+        if (!gray.empty()) {
+            const std::string mode = a.get("--gray-mode", "auto");
+            write_file(gray, write_netpbm(to_gray(vec.distance, mode == "linear" ? GrayMapping::linear
+                                                                                  : GrayMapping::sqrt_linear),
+                                          PgmVariant::raw));
+        }
+        if (!offsets.empty()) write_file(offsets, to_text(vec.offsets));
+        return 0;
+    }
     const DeviceMap dm = transform(img, kind);
 
-    if (!offsets.empty()) throw std::runtime_error("--offsets requires --algorithm danielsson");
     const bool sqrt_dump = a.flag("--sqrt"), normalized = a.flag("--normalized");
     if (sqrt_dump && kind != DistanceKind::squared_euclidean)
         throw std::runtime_error("--sqrt applies to euclidean results only");

@@ -235,3 +235,31 @@ def test_bench_subcommand_csv(tmp_path):
     assert [(r[0], r[1], r[2], r[3]) for r in rows] == [
         (str(s * s), a, str(s), str(rep)) for s in (16, 33) for rep in (0, 1) for a in ("envelope", "simple")]
     assert all(int(r[4]) > 0 for r in rows)
+
+
+def _offsets_text(dy, dx):
+    """to_text(OffsetMap) (vector_dt.cpp:7-21): "dy,dx" or "inf", one line per row."""
+    return "".join(" ".join("inf" if dy[i, j] == 0xFFFFFFFF else f"{dy[i, j]},{dx[i, j]}" for j in range(dy.shape[1]))
+                   + "\n" for i in range(dy.shape[0]))
+
+
+@pytest.mark.gpu
+@needs_cli
+def test_danielsson_algorithm_and_offsets_dump(tmp_path):
+    """--algorithm danielsson / --offsets (distfield_cli.cpp:177-179, :192-220;
+    the reference's own test: test_cli.cpp:136-150): the squared-distance dump
+    and the offsets dump of the vector transform, and the option errors."""
+    img = oracle.random_image(23, 31, 0.04, 99)
+    f = tmp_path / "in.pbm"
+    f.write_bytes(pbm_plain(img))
+    p = run("transform", "--input", str(f), "--algorithm", "danielsson", "--dump", str(tmp_path / "d.txt"),
+            "--offsets", str(tmp_path / "o.txt"))
+    assert p.returncode == 0, p.stderr
+    d, dy, dx = oracle.danielsson(img)
+    assert (tmp_path / "o.txt").read_text() == _offsets_text(dy, dx)
+    want = "".join(" ".join("inf" if v == oracle.INF else str(int(v)) for v in row) + "\n" for row in d)
+    assert (tmp_path / "d.txt").read_text() == want
+    p = run("transform", "--input", str(f), "--offsets", str(tmp_path / "o2.txt"))
+    assert p.returncode == 1 and b"--offsets requires --algorithm danielsson" in p.stderr
+    p = run("transform", "--input", str(f), "--algorithm", "danielsson", "--labels", str(tmp_path / "l.pgm"))
+    assert p.returncode == 1 and b"--labels requires an exact euclidean algorithm" in p.stderr

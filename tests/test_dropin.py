@@ -140,3 +140,22 @@ def test_reference_acceptance_suite_relinked_against_dropin():
     lines = [l for l in p.stdout.splitlines() if l.startswith("criterion")]
     status = {int(l.split()[1].rstrip(":")): l.split()[2] for l in lines}
     assert status == {1: "PASS", 2: "PASS", 3: "PASS", 4: "FAIL", 5: "PASS", 6: "PASS", 7: "PASS"}, p.stdout
+
+
+def test_dropin_danielsson():
+    """distfield::danielsson / danielsson_first_sweep / to_text(OffsetMap)
+    (vector_dt.hpp) through the drop-in: maps and offsets as the oracle, the
+    text dump byte for byte."""
+    rng = np.random.default_rng(8)
+    for t in range(6):
+        img = (rng.random((int(rng.integers(1, 50)), int(rng.integers(1, 60)))) < [0.0, 0.02, 0.1, 0.5][t % 4]).astype(np.uint8)
+        n = img.size
+        for op, fs in (("danielsson", False), ("danielsson_first", True)):
+            raw = run(op, img, dtype=np.uint8)
+            d, dy, dx = oracle.danielsson(img, fs)
+            np.testing.assert_array_equal(raw[:8 * n].view(np.uint64), d.ravel())
+            np.testing.assert_array_equal(raw[8 * n:12 * n].view(np.uint32), dy.ravel())
+            np.testing.assert_array_equal(raw[12 * n:16 * n].view(np.uint32), dx.ravel())
+            want = "".join(" ".join("inf" if dy[i, j] == 0xFFFFFFFF else f"{dy[i, j]},{dx[i, j]}"
+                                    for j in range(img.shape[1])) + "\n" for i in range(img.shape[0]))
+            assert raw[16 * n:].tobytes().decode() == want

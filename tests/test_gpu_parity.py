@@ -906,3 +906,36 @@ def test_danielsson_ties_wide_and_batch(dfc):
         np.testing.assert_array_equal(out["sqdist"][k].cpu().numpy().view(np.uint64), d)
         np.testing.assert_array_equal(out["dy"][k].cpu().numpy().view(np.uint32), dy)
         np.testing.assert_array_equal(out["dx"][k].cpu().numpy().view(np.uint32), dx)
+
+
+def test_danielsson_goldens_on_device(dfc):
+    """goldens.hpp:144-190 through the CUDA path: the six-point offsets after
+    the first sweep and final, and the disrupted-region witness (one wrong
+    cell: 170 at (1, 0) with offset (1, 13), exact 169)."""
+    import json
+    with open(os.path.join(GOLD, "vector_dt.json")) as f:
+        g = json.load(f)
+    img = np.zeros(g["six_shape"], np.uint8)
+    for r, c in g["six_points"]:
+        img[r, c] = 1
+    for key, fs in (("kOffsetsSweep1", True), ("kOffsetsFinal", False)):
+        out = dfc.danielsson(_dev(img), first_sweep=fs)
+        want = np.array(g[key], np.int32)
+        np.testing.assert_array_equal(out["dy"].cpu().numpy(), want[:, :, 0])
+        np.testing.assert_array_equal(out["dx"].cpu().numpy(), want[:, :, 1])
+    wit = np.zeros(g["witness_shape"], np.uint8)
+    for r, c in g["witness_points"]:
+        wit[r, c] = 1
+    out = dfc.danielsson(_dev(wit))
+    d = out["sqdist"].cpu().numpy().view(np.uint64)
+    exact = oracle.edt(wit)
+    assert int((d != exact).sum()) == 1
+    qi, qj = g["witness_cell"]
+    assert d[qi, qj] == 170 and exact[qi, qj] == 169
+    assert (int(out["dy"][qi, qj]), int(out["dx"][qi, qj])) == (1, 13)
+    for c in g["reference_runs"]:
+        im = oracle.random_image(c["rows"], c["cols"], c["density"], c["seed"])
+        o = dfc.danielsson(_dev(im), first_sweep=c["first_sweep"])
+        np.testing.assert_array_equal(o["sqdist"].cpu().numpy().ravel(), np.array(c["dist"], np.int64))
+        np.testing.assert_array_equal(o["dy"].cpu().numpy().ravel(), np.array(c["dy"], np.int32))
+        np.testing.assert_array_equal(o["dx"].cpu().numpy().ravel(), np.array(c["dx"], np.int32))

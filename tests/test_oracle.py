@@ -255,3 +255,64 @@ def test_oracle_build_row_envelope_matches_reference_on_arbitrary_rows():
             a = oracle.build_row_envelope(v, lmax, tn)
             b = oracle.ref_build_row_envelope(v, lmax, tn)
             assert a[0].tolist() == b[0].tolist() and a[1].tolist() == b[1].tolist()
+
+
+# ---- Danielsson vector transform (vector_dt.cpp) ----
+def _vec_gold():
+    import json
+    with open(os.path.join(os.path.dirname(__file__), "golden", "vector_dt.json")) as f:
+        return json.load(f)
+
+
+def _points_image(shape, points):
+    img = np.zeros(shape, np.uint8)
+    for r, c in points:
+        img[r, c] = 1
+    return img
+
+
+def test_danielsson_goldens():
+    """The reference's frozen matrices (goldens.hpp:144-190): offsets after the
+    downward sweep and final offsets on the six-point sample; the
+    disrupted-region witness: exactly one wrong cell, 170 = 1^2 + 13^2 against
+    the exact 169 (test_vector_dt.cpp:23-55)."""
+    g = _vec_gold()
+    img = _points_image(g["six_shape"], g["six_points"])
+    for key, fs in (("kOffsetsSweep1", True), ("kOffsetsFinal", False)):
+        d, dy, dx = oracle.danielsson(img, fs)
+        want = np.array(g[key], np.int64)
+        np.testing.assert_array_equal(dy.astype(np.int32).astype(np.int64), want[:, :, 0])
+        np.testing.assert_array_equal(dx.astype(np.int32).astype(np.int64), want[:, :, 1])
+    d, _, _ = oracle.danielsson(img)
+    np.testing.assert_array_equal(d, oracle.edt(img))  # exact on this input
+    wit = _points_image(g["witness_shape"], g["witness_points"])
+    d, dy, dx = oracle.danielsson(wit)
+    exact = oracle.edt(wit)
+    assert int((d != exact).sum()) == 1
+    qi, qj = g["witness_cell"]
+    assert d[qi, qj] == 170 and exact[qi, qj] == 169 and (dy[qi, qj], dx[qi, qj]) == (1, 13)
+
+
+def test_danielsson_reference_runs_and_properties():
+    """The restatement against outputs of the reference itself (committed),
+    plus the reference's own properties: value = dy^2 + dx^2 wherever set, an
+    upper bound of the exact transform (test_vector_dt.cpp:57-92)."""
+    for c in _vec_gold()["reference_runs"]:
+        img = oracle.random_image(c["rows"], c["cols"], c["density"], c["seed"])
+        d, dy, dx = oracle.danielsson(img, c["first_sweep"])
+        np.testing.assert_array_equal(d.view(np.int64).ravel(), np.array(c["dist"], np.int64))
+        np.testing.assert_array_equal(dy.view(np.int32).ravel(), np.array(c["dy"], np.int32))
+        np.testing.assert_array_equal(dx.view(np.int32).ravel(), np.array(c["dx"], np.int32))
+        if not c["first_sweep"]:
+            exact = oracle.edt(img)
+            setm = dy != 0xFFFFFFFF
+            assert ((d == np.iinfo(np.uint64).max) == ~setm).all()
+            assert (d[setm] == dy[setm].astype(np.uint64) ** 2 + dx[setm].astype(np.uint64) ** 2).all()
+            assert (d >= exact).all()
+    if oracle.ref_available():
+        rng = np.random.default_rng(4)
+        for _ in range(40):
+            img = (rng.random((int(rng.integers(1, 50)), int(rng.integers(1, 50)))) < 0.07).astype(np.uint8)
+            for fs in (False, True):
+                for a, b in zip(oracle.danielsson(img, fs), oracle.ref_danielsson(img, fs)):
+                    np.testing.assert_array_equal(a, b)
