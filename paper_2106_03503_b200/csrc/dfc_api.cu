@@ -1252,7 +1252,7 @@ int dfc_danielsson_u8(const uint8_t* d_img, int64_t n_images, int64_t rows, int6
         const cudaError_t e = set_dyn_smem((const void*)k_danielsson, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e);
     }
-    k_danielsson<<<(unsigned)n_images, 32, a.scratch ? 0 : smem, st>>>(a);
+    k_danielsson<<<(unsigned)n_images, kDanThreads, a.scratch ? 0 : smem, st>>>(a);
     ++g_launches;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? DFC_OK : cuda_fail(e);

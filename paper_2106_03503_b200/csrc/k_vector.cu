@@ -20,9 +20,10 @@
 //          c2 : base), also independent of x, and becomes the new source.  So
 //          a warp resolves 32 cells at a time: every lane tests the carried
 //          value at its own cell, the first failing lane restarts the chain
-//          with its K, and the loop runs once per restart inside the block --
-//          one step per 32 cells where one feature owns a stretch, one step
-//          per cell in the worst case (the reference's own cost).
+//          with its K (a K equal to the carried value is no restart), and the
+//          loop runs once per restart inside the block -- one step per 32
+//          cells where one feature owns a stretch, one step per cell in the
+//          worst case (the reference's own cost).
 //
 // The current and the previous row live in shared memory (or, for rows too
 // wide for it, in a global scratch of the same layout); every finished row is
@@ -73,6 +74,18 @@ __device__ __forceinline__ void dan_block(bool valid, uint64_t Db, uint32_t by, 
     const uint32_t vmask = __ballot_sync(FULL, valid);
     uint32_t rem = vmask;
     int src = -1;
+    // self1: the cell would also restart if the cell before it had just restarted
+    // (its K, moved one step, fails here too).  Cells on the far side of their
+    // feature do that one after the other (the carried offset only grows), so a
+    // whole run of them is taken in one step.
+    uint32_t self1;
+    {
+        const uint32_t py = __shfl_up_sync(FULL, Ky, 1), px = __shfl_up_sync(FULL, Kx, 1);
+        const uint32_t qx = px + 1u;
+        const bool pset = py != kDanUnset;
+        const bool ok = pset && (dan_sq(py, qx) < T || (Ky == py && Kx == qx));
+        self1 = __ballot_sync(FULL, valid && lane > 0 && !ok);
+    }
     while (rem) {
         if (!xs) {  // nothing carried: every cell keeps its K up to the first set one
             const uint32_t m = __ballot_sync(FULL, valid && Kset) & rem;
@@ -88,7 +101,11 @@ __device__ __forceinline__ void dan_block(bool valid, uint64_t Db, uint32_t by, 
         const uint32_t cdx = xx + (uint32_t)(lane - src);
         const uint64_t D1 = dan_sq(xy, cdx);
         const bool in = (rem >> lane) & 1u;
-        const uint32_t m = __ballot_sync(FULL, in && !(D1 < T)) & rem;
+        // a cell that keeps its own K breaks the chain only if K differs from the
+        // carried value (inside one feature's region the vertical candidate and the
+        // carried one are the same offset: the chain goes on unchanged)
+        const bool same = Ky == xy && Kx == cdx;
+        const uint32_t m = __ballot_sync(FULL, in && !(D1 < T) && !same) & rem;
         const int f = m ? __ffs(m) - 1 : 32;
         if (in && lane < f) {
             rD = D1;
@@ -96,12 +113,18 @@ __device__ __forceinline__ void dan_block(bool valid, uint64_t Db, uint32_t by, 
             rx = cdx;
         }
         if (f == 32) break;
-        // lane f restarts the chain with its K (possibly unset)
-        xs = __shfl_sync(FULL, (int)Kset, f) != 0;
-        xy = __shfl_sync(FULL, Ky, f);
-        xx = __shfl_sync(FULL, Kx, f);
-        src = f;
-        rem &= ~((2u << f) - 1u);
+        // lane f restarts the chain with its K (possibly unset), and so do the
+        // cells after it for which self1 holds without a gap: the chain goes on
+        // from the last of them
+        const uint32_t after = ~((2u << f) - 1u);           // lanes > f
+        const uint32_t stop = ~self1 & after & vmask;        // first lane > f that does not restart by itself
+        const int g = stop ? __ffs(stop) - 1 : 32;           // lanes f .. g - 1 keep their K
+        const int s2 = min(g - 1, 31 - __clz(vmask));        // the new source (the last valid lane at most)
+        xs = __shfl_sync(FULL, (int)Kset, s2) != 0;
+        xy = __shfl_sync(FULL, Ky, s2);
+        xx = __shfl_sync(FULL, Kx, s2);
+        src = s2;
+        rem &= ~((2u << s2) - 1u);
     }
     // the carried value for the next block: the last valid lane's result
     const int last = 31 - __clz(vmask);
@@ -111,9 +134,11 @@ __device__ __forceinline__ void dan_block(bool valid, uint64_t Db, uint32_t by, 
     xx = lx;
 }
 
-__global__ void __launch_bounds__(32) k_danielsson(DanArgs a) {
+constexpr int kDanThreads = 128;  // warp 0 carries the row passes; all warps do the elementwise parts
+
+__global__ void __launch_bounds__(kDanThreads) k_danielsson(DanArgs a) {
     extern __shared__ uint4 dan_raw[];
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int im = blockIdx.x;
     const int W = a.cols, H = a.rows, Wb = a.Wb;
     char* base = a.scratch ? a.scratch + (size_t)im * 2 * 16 * Wb : reinterpret_cast<char*>(dan_raw);
@@ -130,21 +155,21 @@ __global__ void __launch_bounds__(32) k_danielsson(DanArgs a) {
 
     auto init_row = [&](int i, DanRow r) {  // init_state, vector_dt.cpp:98-106
         const uint8_t* p = img + (size_t)i * a.pitch;
-        for (int j = lane; j < W; j += 32) {
+        for (int j = tid; j < W; j += kDanThreads) {
             const bool obj = p[j] != 0;
             r.D[j] = obj ? 0ull : kDanInf;
             r.y[j] = r.x[j] = obj ? 0u : kDanUnset;
         }
     };
     auto load_row = [&](int i, DanRow r) {
-        for (int j = lane; j < W; j += 32) {
+        for (int j = tid; j < W; j += kDanThreads) {
             r.D[j] = oD[(size_t)i * W + j];
             r.y[j] = oy[(size_t)i * W + j];
             r.x[j] = ox[(size_t)i * W + j];
         }
     };
     auto store_row = [&](int i, DanRow r) {
-        for (int j = lane; j < W; j += 32) {
+        for (int j = tid; j < W; j += kDanThreads) {
             oD[(size_t)i * W + j] = r.D[j];
             oy[(size_t)i * W + j] = r.y[j];
             ox[(size_t)i * W + j] = r.x[j];
@@ -152,7 +177,7 @@ __global__ void __launch_bounds__(32) k_danielsson(DanArgs a) {
     };
     // one row of a sweep: cur from prev (the finished neighbouring row)
     auto row = [&](DanRow cur, DanRow prev, bool up) {
-        for (int j = lane; j < W; j += 32) {  // vertical update (:67-68, :84-85)
+        for (int j = tid; j < W; j += kDanThreads) {  // vertical update (:67-68, :84-85)
             const uint32_t py = prev.y[j];
             if (py != kDanUnset) {
                 const uint32_t ny = py + 1, nx = prev.x[j];
@@ -164,8 +189,8 @@ __global__ void __launch_bounds__(32) k_danielsson(DanArgs a) {
                 }
             }
         }
-        __syncwarp();
-        if (W < 2) return;
+        __syncthreads();
+        if (W < 2 || tid >= 32) return;
         // forward (:69-73, :86-90): from the left neighbour, then from the diagonal one
         bool xs = cur.y[0] != kDanUnset;
         uint32_t xy = cur.y[0], xx = cur.x[0];
@@ -229,20 +254,22 @@ __global__ void __launch_bounds__(32) k_danielsson(DanArgs a) {
 
     int c = 0;
     init_row(0, buf[c]);
-    __syncwarp();
+    __syncthreads();
     store_row(0, buf[c]);
     for (int i = 1; i < H; ++i) {  // sweep_down (:64-79)
         init_row(i, buf[c ^ 1]);
-        __syncwarp();
+        __syncthreads();
         row(buf[c ^ 1], buf[c], false);
+        __syncthreads();
         store_row(i, buf[c ^ 1]);
         c ^= 1;
     }
     if (a.first_only) return;
     for (int i = H - 2; i >= 0; --i) {  // sweep_up (:81-96): buf[c] holds the finished row i + 1
         load_row(i, buf[c ^ 1]);
-        __syncwarp();
+        __syncthreads();
         row(buf[c ^ 1], buf[c], true);
+        __syncthreads();
         store_row(i, buf[c ^ 1]);
         c ^= 1;
     }
