@@ -22,6 +22,7 @@ import torch
 
 from . import INF_I32, edt as _edt, label_ordinals, raster as _raster, vertical as _vertical
 from . import vertical_down_pass as _vdown, vertical_up_pass as _vup
+from . import danielsson as _danielsson
 
 INF = np.uint64(2**64 - 1)
 NO_COLUMN = np.uint32(2**32 - 1)
@@ -145,3 +146,13 @@ def chamfer34(img):
 def chessboard(img):
     """Chessboard map; the reference has only oracle::chessboard (tests/oracles.hpp:52-55)."""
     return _raster1(img, "chessboard")
+
+
+def danielsson(img, first_sweep=False):
+    """danielsson / danielsson_first_sweep -- vector_dt.cpp:108-124: (squared
+    lengths uint64 with kInfinity, dy uint32, dx uint32 with Offset::kUnset =
+    0xFFFFFFFF), the sweeps on the GPU."""
+    o = _danielsson(_to_device(img), first_sweep=first_sweep)
+    torch.cuda.synchronize()
+    return (o["sqdist"].cpu().numpy().view(np.uint64), o["dy"].cpu().numpy().view(np.uint32),
+            o["dx"].cpu().numpy().view(np.uint32))

@@ -60,6 +60,8 @@ def main():
     repeat("pts batch 64x256^2", lambda: dfc.edt_batched(pts, dist=False, label=True))
     many = torch.from_numpy(workloads.points_batch(16, 256, 256, 200, 8)).cuda()
     repeat("batch 16x256^2, 200 points", lambda: dfc.edt_batched(many, dist=True, label=True))
+    dn = torch.from_numpy(oracle.random_image(300, 400, 0.02, 6)).cuda()
+    repeat("danielsson 300x400", lambda: dfc.danielsson(dn))
     print("determinism ok")
 
 
