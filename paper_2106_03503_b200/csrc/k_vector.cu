@@ -6,8 +6,10 @@
 // i - 1 (sweep_down) or i + 1 (sweep_up), and inside a row the forward and the
 // backward pass each carry a value from cell to cell.  What is parallel:
 //
-//  images  one warp per image (batches); a single image is one warp.
-//  pass V  the vertical update of a row (vector_dt.cpp:67-68): elementwise.
+//  images  one CTA (4 warps) per image: batches run in parallel, a single image
+//          is one CTA walking its rows.
+//  pass V  the vertical update of a row (vector_dt.cpp:67-68): elementwise, all
+//          warps; so are the row loads and stores.  Warp 0 carries passes F / B:
 //  pass F/B  the carried value x reaches cell j as x + (0, j - s) from its
 //          source cell s.  With base = the cell after pass V and c2 = the
 //          diagonal neighbour's offset + (1, 1), the cell keeps the carried
